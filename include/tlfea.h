@@ -186,6 +186,13 @@ tlfea_status tlfea_coef_pattern(tlfea_ctx ctx, const int32_t** rowptr,
  * For nranks = 1 it is 0..n_coef-1. */
 tlfea_status tlfea_owned_nodes(tlfea_ctx ctx, const int32_t** nodes);
 
+/* Copies of the patterns into caller DEVICE buffers (any may be NULL):
+ * rowptr_out [3 n_owned+1], cols_out [nnz], rowptr_c_out [n_owned+1],
+ * cols_c_out [nnz_coef], owned_out [n_owned]. Asynchronous on stream. */
+tlfea_status tlfea_export_pattern(tlfea_ctx ctx, int32_t* rowptr_out, int32_t* cols_out,
+                                  int32_t* rowptr_c_out, int32_t* cols_c_out,
+                                  int32_t* owned_out, void* stream);
+
 /* Canonical slot map (reading Q16): out_host int32 [e_count][3n_en][3n_en],
  * entry [e][3a+d][3b+f] = index into the DOF CSR values of the entry
  * (row 3*conn[e][a]+d, column 3*conn[e][b]+f), or -1 when that row is not
@@ -327,6 +334,15 @@ tlfea_status tlfea_sync_status(tlfea_ctx ctx, int64_t* bad_elem,
 tlfea_status tlfea_test_constitutive(const tlfea_material* mat, int64_t n,
                                      const double* F, const double* Fdot,
                                      double* P_out, double* A_out);
+
+/* Live per-kernel timing (bench.py roofline): with enable = 1 every eval
+ * kernel of this context is bracketed by CUDA events recorded on its launch
+ * stream. tlfea_timing_report synchronizes and returns, per kernel class
+ * (0 element kernel, 1 H gather, 2 force gather / residual, 3 partition
+ * pack/unpack), the number of launches and their summed duration in ms, and
+ * resets the record. counts/ms are HOST arrays of length 4. */
+tlfea_status tlfea_set_timing(tlfea_ctx ctx, int32_t enable);
+tlfea_status tlfea_timing_report(tlfea_ctx ctx, int64_t* counts, double* ms);
 
 /* Number of kernels this library launched since load (for gpu_launches). */
 int64_t tlfea_launch_count(void);

@@ -1,0 +1,366 @@
+"""paper_2604_10357_b200 — B200-native (sm_100a, fp64) hot path of arXiv 2604.10357.
+
+Thin Python binding of ``libtlfea.so`` (C ABI in ``include/tlfea.h``): argument
+marshalling only. Every step of the path (precompute, pattern, slot map, mass,
+Stage 1/2, tangent, deterministic CSR scatter, residual) runs in the CUDA
+kernels of ``csrc/``. PyTorch supplies device memory, streams and
+``torch.distributed``. There is no CPU fallback: if the library is missing or
+no CUDA device is present, calls raise.
+
+Function names follow the C ABI (``tlfea_setup``, ``tlfea_eval``,
+``tlfea_force_only`` ...); :class:`Context` is a convenience owner of one
+``tlfea_ctx``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtlfea.so")
+_lib = None
+_lock = threading.Lock()
+
+T10, ANCF3443 = 0, 1
+Q_T10_4PT, Q_T10_KEAST5, Q_GL_4x4x3 = 0, 1, 2
+SVK, MOONEY_RIVLIN = 0, 1
+STATUS = {0: "OK", 1: "INVALID", 2: "INVERTED_ELEMENT", 3: "INVERTED_STATE", 4: "OVERFLOW", 5: "OOM",
+          6: "CUDA", 7: "UNSUPPORTED"}
+
+
+class TlfeaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"tlfea {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Material(C.Structure):
+    _fields_ = [("model", C.c_int32), ("E", C.c_double), ("nu", C.c_double), ("C10", C.c_double),
+                ("C01", C.c_double), ("kappa", C.c_double), ("rho0", C.c_double), ("eta_damp", C.c_double),
+                ("lambda_damp", C.c_double)]
+
+
+class Mesh(C.Structure):
+    _fields_ = [("element", C.c_int32), ("n_elements", C.c_int64), ("n_coef", C.c_int64),
+                ("conn", C.POINTER(C.c_int32)), ("X_ref", C.POINTER(C.c_double)),
+                ("ancf_dims", C.POINTER(C.c_double))]
+
+
+class Options(C.Structure):
+    _fields_ = [("quadrature", C.c_int32), ("mass_rule", C.c_int32), ("gravity", C.c_double * 3),
+                ("ancf_dims", C.c_double * 3), ("rank", C.c_int32), ("nranks", C.c_int32),
+                ("elem_part", C.POINTER(C.c_int32)), ("device", C.c_int32)]
+
+
+class Info(C.Structure):
+    _fields_ = [("element", C.c_int32), ("quadrature", C.c_int32), ("n_qp", C.c_int32), ("n_en", C.c_int32),
+                ("n_elements", C.c_int64), ("n_elements_global", C.c_int64), ("n_coef", C.c_int64),
+                ("n_dof", C.c_int64), ("nnz_coef", C.c_int64), ("nnz", C.c_int64), ("n_owned_nodes", C.c_int64),
+                ("affine", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32), ("device_bytes", C.c_int64)]
+
+
+_vp, _i64, _i32, _d = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+_SIGS = {
+    "tlfea_setup": [C.POINTER(Mesh), C.POINTER(Material), C.POINTER(Options), C.POINTER(_vp)],
+    "tlfea_destroy": [_vp],
+    "tlfea_info": [_vp, C.POINTER(Info)],
+    "tlfea_pattern": [_vp, C.POINTER(_vp), C.POINTER(_vp)],
+    "tlfea_coef_pattern": [_vp, C.POINTER(_vp), C.POINTER(_vp)],
+    "tlfea_owned_nodes": [_vp, C.POINTER(_vp)],
+    "tlfea_slot_map": [_vp, _i64, _i64, _vp],
+    "tlfea_export_pattern": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "tlfea_export_precompute": [_vp, _vp, _vp, _vp],
+    "tlfea_export_mass": [_vp, _vp, _vp, _vp],
+    "tlfea_eval": [_vp, _vp, _vp, _vp, _vp, _d, _vp, _vp, _vp, _vp],
+    "tlfea_force_only": [_vp, _vp, _vp, _vp, _vp],
+    "tlfea_eval_host": [_vp, _vp, _vp, _vp, _vp, _d, _vp, _vp, _vp, _vp],
+    "tlfea_compute_stress": [_vp, _vp, _vp, _vp, _vp],
+    "tlfea_internal_force_from_stress": [_vp, _vp, _vp, _vp],
+    "tlfea_compute_gradient": [_vp, _vp, _vp, _vp, _vp, _d, _vp, _vp],
+    "tlfea_assemble_hessian": [_vp, _vp, _d, _vp, _vp],
+    "tlfea_exchange_sizes": [_vp, _vp, _vp],
+    "tlfea_eval_begin": [_vp, _vp, _vp, _i32, _d, _vp, _vp, _vp],
+    "tlfea_eval_finish": [_vp, _vp, _vp, _vp, _vp, _d, _i32, _vp, _vp, _vp, _vp],
+    "tlfea_plan_partition": [_i64, _i32, _vp, _i64, _vp, _i32, _i32, _vp, C.POINTER(_i64), _vp, _vp,
+                             C.POINTER(_i64), _vp, _vp],
+    "tlfea_sync_status": [_vp, C.POINTER(_i64), C.POINTER(_i32)],
+    "tlfea_test_constitutive": [C.POINTER(Material), _i64, _vp, _vp, _vp, _vp],
+    "tlfea_set_timing": [_vp, _i32],
+    "tlfea_timing_report": [_vp, _vp, _vp],
+    "tlfea_launch_count": [],
+    "tlfea_last_error": [],
+    "tlfea_abi_version": [],
+}
+EXPORTED = tuple(_SIGS)
+
+
+def lib():
+    """Load libtlfea.so (built in-tree by ``paper_2604_10357_b200.build``)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2604_10357_b200.build` "
+                                   "(the CUDA library is required; there is no CPU fallback)")
+            L = C.CDLL(LIB_PATH)
+            for name, args in _SIGS.items():
+                fn = getattr(L, name)
+                fn.argtypes = args
+                fn.restype = C.c_int
+            L.tlfea_destroy.restype = None
+            L.tlfea_launch_count.restype = C.c_int64
+            L.tlfea_last_error.restype = C.c_char_p
+            L.tlfea_abi_version.restype = C.c_int32
+            _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise TlfeaError(st, lib().tlfea_last_error().decode())
+
+
+def _ptr(t):
+    """Device/host address of a torch tensor / numpy array, or None."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return C.c_void_p(t.data_ptr())
+    return C.c_void_p(t.ctypes.data)
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+def make_material(mat: dict) -> Material:
+    return Material(int(mat.get("model", 0)), *(float(mat.get(k, 0.0)) for k in
+                                                 ("E", "nu", "C10", "C01", "kappa", "rho0", "eta_damp",
+                                                  "lambda_damp")))
+
+
+def launch_count() -> int:
+    return int(lib().tlfea_launch_count())
+
+
+def tlfea_test_constitutive(mat: dict, F, Fdot=None, with_tangent=True):
+    """Device constitutive functions on a batch (torch CUDA tensors [n,9])."""
+    import torch
+    n = F.shape[0]
+    P = torch.empty((n, 9), dtype=torch.float64, device=F.device)
+    A = torch.empty((n, 81), dtype=torch.float64, device=F.device) if with_tangent else None
+    m = make_material(mat)
+    _check(lib().tlfea_test_constitutive(C.byref(m), n, _ptr(F), _ptr(Fdot), _ptr(P), _ptr(A)))
+    return P, A
+
+
+def tlfea_plan_partition(conn_coef: np.ndarray, n_coef: int, elem_part, nranks: int, rank: int):
+    """Host-only partition planner (no GPU needed). Returns (owner [n_coef],
+    send_blocks [n,2] (I,J), send_block_peer [n], send_nodes [m], send_node_peer [m])."""
+    L = lib()
+    conn_coef = np.ascontiguousarray(conn_coef, np.int32)
+    n_el, nen = conn_coef.shape
+    part = None if elem_part is None else np.ascontiguousarray(elem_part, np.int32)
+    nb, nn = C.c_int64(0), C.c_int64(0)
+    _check(L.tlfea_plan_partition(n_el, nen, _ptr(conn_coef), n_coef, _ptr(part), nranks, rank, None,
+                                  C.byref(nb), None, None, C.byref(nn), None, None))
+    owner = np.zeros(n_coef, np.int32)
+    sb = np.zeros((nb.value, 2), np.int64)
+    sbp = np.zeros(nb.value, np.int64)
+    sn = np.zeros(nn.value, np.int64)
+    snp = np.zeros(nn.value, np.int64)
+    _check(L.tlfea_plan_partition(n_el, nen, _ptr(conn_coef), n_coef, _ptr(part), nranks, rank, _ptr(owner),
+                                  C.byref(nb), _ptr(sb), _ptr(sbp), C.byref(nn), _ptr(sn), _ptr(snp)))
+    return owner, sb, sbp, sn, snp
+
+
+class Context:
+    """Owns one tlfea_ctx (tlfea_setup ... tlfea_destroy)."""
+
+    def __init__(self, element: int, conn: np.ndarray, X: np.ndarray, mat: dict, quadrature: int,
+                 dims: np.ndarray | None = None, mass_rule: int = 0, gravity=(0.0, 0.0, 0.0),
+                 rank: int = 0, nranks: int = 1, elem_part=None, device: int = 0):
+        L = lib()
+        self._conn = np.ascontiguousarray(conn, np.int32)
+        self._X = np.ascontiguousarray(X, np.float64)
+        self._dims = None if dims is None else np.ascontiguousarray(dims, np.float64)
+        self._part = None if elem_part is None else np.ascontiguousarray(elem_part, np.int32)
+        mesh = Mesh(element, self._conn.shape[0], self._X.shape[0],
+                    self._conn.ctypes.data_as(C.POINTER(C.c_int32)), self._X.ctypes.data_as(C.POINTER(C.c_double)),
+                    None if self._dims is None else self._dims.ctypes.data_as(C.POINTER(C.c_double)))
+        opts = Options(quadrature, mass_rule, (C.c_double * 3)(*gravity), (C.c_double * 3)(0, 0, 0), rank, nranks,
+                       None if self._part is None else self._part.ctypes.data_as(C.POINTER(C.c_int32)), device)
+        self.material = dict(mat)
+        m = make_material(mat)
+        h = C.c_void_p()
+        _check(L.tlfea_setup(C.byref(mesh), C.byref(m), C.byref(opts), C.byref(h)))
+        self.handle = h
+        self.device = device
+        info = Info()
+        _check(L.tlfea_info(h, C.byref(info)))
+        self.info = {k: getattr(info, k) for k, _ in Info._fields_}
+
+    @classmethod
+    def from_mesh(cls, mesh, mat: dict, quadrature: int, **kw):
+        """From a ``synth.Mesh``-like object (element, conn, X, dims)."""
+        return cls(int(mesh.element), mesh.conn, mesh.X, mat, quadrature, dims=mesh.dims, **kw)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().tlfea_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- sizes
+    @property
+    def n_own(self):
+        return self.info["n_owned_nodes"]
+
+    @property
+    def nnz(self):
+        return self.info["nnz"]
+
+    def _torch(self):
+        import torch
+        return torch
+
+    def empty_outputs(self):
+        torch = self._torch()
+        dev = torch.device("cuda", self.device)
+        g = torch.empty(3 * self.n_own, dtype=torch.float64, device=dev)
+        H = torch.empty(self.nnz, dtype=torch.float64, device=dev)
+        f = torch.empty(3 * self.n_own, dtype=torch.float64, device=dev)
+        return g, H, f
+
+    # -- exports
+    def export_pattern(self, stream=None):
+        """Copies (rowptr [3 n_own+1], cols [nnz], rowptr_c [n_own+1], cols_c [nnz_coef],
+        owned [n_own]) as int32 CUDA tensors (tlfea_export_pattern)."""
+        torch = self._torch()
+        dev = torch.device("cuda", self.device)
+        i = self.info
+        out = [torch.empty(n, dtype=torch.int32, device=dev) for n in
+               (3 * self.n_own + 1, self.nnz, self.n_own + 1, i["nnz_coef"], self.n_own)]
+        _check(lib().tlfea_export_pattern(self.handle, *[_ptr(t) for t in out], _stream(stream)))
+        return tuple(out)
+
+    def slot_map(self, e_begin=0, e_count=None):
+        n = self.info["n_elements"]
+        if e_count is None:
+            e_count = n - e_begin
+        nd = 3 * self.info["n_en"]
+        out = np.zeros((e_count, nd, nd), np.int32)
+        _check(lib().tlfea_slot_map(self.handle, e_begin, e_count, _ptr(out)))
+        return out
+
+    def export_precompute(self, stream=None):
+        torch = self._torch()
+        i = self.info
+        dev = torch.device("cuda", self.device)
+        gN = torch.empty((i["n_elements"], i["n_qp"], i["n_en"], 3), dtype=torch.float64, device=dev)
+        Jw = torch.empty((i["n_elements"], i["n_qp"]), dtype=torch.float64, device=dev)
+        _check(lib().tlfea_export_precompute(self.handle, _ptr(gN), _ptr(Jw), _stream(stream)))
+        return gN, Jw
+
+    def export_mass(self, stream=None):
+        torch = self._torch()
+        dev = torch.device("cuda", self.device)
+        M = torch.empty(self.info["nnz_coef"], dtype=torch.float64, device=dev)
+        fff = torch.empty(3 * self.n_own, dtype=torch.float64, device=dev)
+        _check(lib().tlfea_export_mass(self.handle, _ptr(M), _ptr(fff), _stream(stream)))
+        return M, fff
+
+    # -- evaluation
+    def eval(self, x, v, v_n=None, f_ext=None, h=1e-3, g=None, H=None, f_int=None, stream=None):
+        if g is None or H is None:
+            g0, H0, _ = self.empty_outputs()
+            g = g0 if g is None else g
+            H = H0 if H is None else H
+        _check(lib().tlfea_eval(self.handle, _ptr(x), _ptr(v), _ptr(v_n), _ptr(f_ext), float(h), _ptr(g), _ptr(H),
+                                _ptr(f_int), _stream(stream)))
+        return g, H, f_int
+
+    def force_only(self, x, v=None, f_int=None, stream=None):
+        if f_int is None:
+            f_int = self.empty_outputs()[2]
+        _check(lib().tlfea_force_only(self.handle, _ptr(x), _ptr(v), _ptr(f_int), _stream(stream)))
+        return f_int
+
+    def eval_host(self, x, v, v_n=None, f_ext=None, h=1e-3, g=None, H=None, f_int=None, stream=None):
+        """Host (numpy or pinned CPU tensors) in and out; synchronizes."""
+        _check(lib().tlfea_eval_host(self.handle, _ptr(x), _ptr(v), _ptr(v_n), _ptr(f_ext), float(h), _ptr(g),
+                                     _ptr(H), _ptr(f_int), _stream(stream)))
+        return g, H, f_int
+
+    def compute_stress(self, x, v=None, P=None, stream=None):
+        torch = self._torch()
+        i = self.info
+        if P is None:
+            P = torch.empty((i["n_elements"], i["n_qp"], 9), dtype=torch.float64, device=x.device)
+        _check(lib().tlfea_compute_stress(self.handle, _ptr(x), _ptr(v), _ptr(P), _stream(stream)))
+        return P
+
+    def internal_force_from_stress(self, P, f_int=None, stream=None):
+        if f_int is None:
+            f_int = self.empty_outputs()[2]
+        _check(lib().tlfea_internal_force_from_stress(self.handle, _ptr(P), _ptr(f_int), _stream(stream)))
+        return f_int
+
+    def compute_gradient(self, f_int, v, v_n=None, f_ext=None, h=1e-3, g=None, stream=None):
+        if g is None:
+            g = self.empty_outputs()[0]
+        _check(lib().tlfea_compute_gradient(self.handle, _ptr(f_int), _ptr(v), _ptr(v_n), _ptr(f_ext), float(h),
+                                            _ptr(g), _stream(stream)))
+        return g
+
+    def assemble_hessian(self, x, h=1e-3, H=None, stream=None):
+        if H is None:
+            H = self.empty_outputs()[1]
+        _check(lib().tlfea_assemble_hessian(self.handle, _ptr(x), float(h), _ptr(H), _stream(stream)))
+        return H
+
+    def exchange_sizes(self):
+        P = self.info["nranks"]
+        s = np.zeros(P, np.int64)
+        r = np.zeros(P, np.int64)
+        _check(lib().tlfea_exchange_sizes(self.handle, _ptr(s), _ptr(r)))
+        return s, r
+
+    def eval_begin(self, x, v, h, H, send_buf, force_only=False, stream=None):
+        _check(lib().tlfea_eval_begin(self.handle, _ptr(x), _ptr(v), int(force_only), float(h), _ptr(H),
+                                      _ptr(send_buf), _stream(stream)))
+
+    def eval_finish(self, recv_buf, v, v_n, f_ext, h, g, H, f_int=None, force_only=False, stream=None):
+        _check(lib().tlfea_eval_finish(self.handle, _ptr(recv_buf), _ptr(v), _ptr(v_n), _ptr(f_ext), float(h),
+                                       int(force_only), _ptr(g), _ptr(H), _ptr(f_int), _stream(stream)))
+
+    def set_timing(self, enable: bool):
+        _check(lib().tlfea_set_timing(self.handle, int(enable)))
+
+    def timing_report(self):
+        """{kind: (launches, total_ms)} for kinds element / gather_H / gather_f / exchange."""
+        cnt = np.zeros(4, np.int64)
+        ms = np.zeros(4, np.float64)
+        _check(lib().tlfea_timing_report(self.handle, _ptr(cnt), _ptr(ms)))
+        return {k: (int(cnt[i]), float(ms[i])) for i, k in enumerate(("element", "gather_H", "gather_f", "exchange"))}
+
+    def sync_status(self):
+        e, q = C.c_int64(0), C.c_int32(0)
+        st = lib().tlfea_sync_status(self.handle, C.byref(e), C.byref(q))
+        if st == 3:
+            return int(e.value), int(q.value)
+        _check(st)
+        return None

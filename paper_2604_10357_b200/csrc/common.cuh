@@ -1,0 +1,185 @@
+// common.cuh — internal types of libtlfea (B200 / sm_100a, fp64).
+// Nothing here is shared with oracle/ (independent implementation).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/tlfea.h"
+
+namespace tlfea {
+
+// ------------------------------------------------------------ error plumbing
+void set_error(const std::string& msg);
+tlfea_status fail(tlfea_status st, const std::string& msg);
+void count_launch(int n = 1);
+
+#define TL_CUDA(call)                                                          \
+  do {                                                                         \
+    cudaError_t err__ = (call);                                                \
+    if (err__ != cudaSuccess)                                                  \
+      return ::tlfea::fail(err__ == cudaErrorMemoryAllocation ? TLFEA_E_OOM    \
+                                                              : TLFEA_E_CUDA,  \
+                           std::string(#call) + ": " + cudaGetErrorString(err__)); \
+  } while (0)
+
+#define TL_CHECK_LAUNCH()                                                      \
+  do {                                                                         \
+    ::tlfea::count_launch();                                                   \
+    cudaError_t err__ = cudaGetLastError();                                    \
+    if (err__ != cudaSuccess)                                                  \
+      return ::tlfea::fail(TLFEA_E_CUDA, std::string("kernel launch: ") +      \
+                                             cudaGetErrorString(err__));       \
+  } while (0)
+
+// ------------------------------------------------------------------- sizes
+constexpr int kMaxQP = 48;
+constexpr int kMaxEN = 16;
+
+inline int n_en_of(int element) { return element == TLFEA_T10 ? 10 : 16; }
+inline int n_qp_of(int quadrature) {
+  return quadrature == TLFEA_Q_T10_4PT ? 4 : quadrature == TLFEA_Q_T10_KEAST5 ? 5 : 48;
+}
+// number of upper-triangular 3x3 blocks (a <= b) of the element matrix
+inline int n_ublk_of(int nen) { return nen * (nen + 1) / 2; }
+
+// Packed contribution entry of the H gather: element (local id) << 8 | a << 4 | b
+__host__ __device__ inline uint32_t pack_eab(uint32_t e, uint32_t a, uint32_t b) {
+  return (e << 8) | (a << 4) | b;
+}
+
+// Material constants as used on the device.
+struct MatDev {
+  int model;       // 0 SVK, 1 MR
+  int kv;          // Kelvin-Voigt active
+  double lam, mu;  // SVK Lame constants
+  double C10, C01, kappa;
+  double eta, lamd;
+  double rho0;
+};
+
+// Device buffer helper (raw cudaMalloc, owned by the context)
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Context {
+  // problem
+  int element = 0, quadrature = 0, nen = 10, nq = 5, mass_rule = 0;
+  MatDev mat{};
+  tlfea_material mat_in{};
+  double gravity[3] = {0, 0, 0};
+  int device = 0;
+  int rank = 0, nranks = 1;
+  int64_t n_el_global = 0, n_coef = 0;
+  int64_t n_el = 0;            // local elements
+  int64_t n_own = 0;           // owned coefficient rows
+  int64_t nnz_c = 0;           // owned-row coefficient nnz
+  int affine = 0;
+
+  // device data
+  int32_t* conn = nullptr;     // [n_el][nen] coefficient ids (local elements)
+  int64_t* elem_gid = nullptr; // [n_el] global element id of each local element
+  double* gradN = nullptr;     // [n_el][nq][nen][3]
+  double* J0w = nullptr;       // [n_el][nq]
+  int32_t* own_nodes = nullptr;   // [n_own] global coefficient ids, ascending
+  int32_t* own_idx = nullptr;     // [n_coef] local row of a coefficient or -1
+  int32_t* rowptr_c = nullptr;    // [n_own+1]
+  int32_t* cols_c = nullptr;      // [nnz_c]
+  int32_t* blk_row = nullptr;     // [nnz_c] owned row of each coefficient block
+  int32_t* rowptr = nullptr;      // [3 n_own + 1]  DOF level
+  int32_t* cols = nullptr;        // [9 nnz_c]
+  double* M = nullptr;            // [nnz_c]
+  double* fff = nullptr;          // [3 n_own]
+  int32_t* slot_c = nullptr;      // [n_el][nen][nen] coefficient-level slot (-1 not owned)
+  int32_t* blk_ptr = nullptr;     // [nnz_c+1]
+  uint32_t* blk_ent = nullptr;    // [...] packed (e,a,b), e ascending per block
+  int32_t* node_ptr = nullptr;    // [n_own+1]
+  uint32_t* node_ent = nullptr;   // [...] (e << 4 | a)
+  double* Kscr = nullptr;         // [n_el][n_ublk][9]
+  double* fscr = nullptr;         // [n_el][nen][3]
+  unsigned long long* err_flag = nullptr;  // min over (e*64+q) with det F <= 0 (MR)
+
+  // partition exchange (nranks > 1)
+  std::vector<int64_t> send_counts, recv_counts;     // fp64 values per peer
+  int64_t n_send_blk = 0, n_recv_blk = 0, n_send_node = 0, n_recv_node = 0;
+  int32_t* sblk_ptr = nullptr;   // [n_send_blk+1] contribution lists of sent blocks
+  uint32_t* sblk_ent = nullptr;
+  int32_t* snode_ptr = nullptr;  // [n_send_node+1]
+  uint32_t* snode_ent = nullptr;
+  int64_t send_blk_vals = 0;     // 9 * n_send_blk (first part of send buffer)
+  int32_t* rblk_slot = nullptr;  // [n_recv_blk] owned coefficient block receiving
+  int32_t* rnode_row = nullptr;  // [n_recv_node] owned row receiving
+  int64_t* send_blk_off = nullptr;   // [n_send_blk] offset in the send buffer
+  int64_t* send_node_off = nullptr;  // [n_send_node]
+  int64_t* recv_peer_blk_off = nullptr;  // host copies are enough
+  std::vector<int64_t> recv_blk_count, recv_node_count, send_blk_count, send_node_count;
+  double* fpart = nullptr;       // [3 n_own] local partial force (partitioned mode)
+
+  // live timing (tlfea_set_timing)
+  bool timing = false;
+  struct TimedLaunch {
+    int kind;
+    cudaEvent_t start, stop;
+  };
+  std::vector<TimedLaunch> timed;
+  std::vector<cudaEvent_t> event_pool;
+  // persistent staging of tlfea_eval_host
+  double *h_x = nullptr, *h_v = nullptr, *h_vn = nullptr, *h_fe = nullptr, *h_g = nullptr, *h_H = nullptr,
+         *h_f = nullptr;
+
+  std::vector<DevBuf> owned;     // every cudaMalloc of this context
+  int64_t device_bytes = 0;
+  cudaStream_t last_stream = nullptr;
+
+  ~Context();
+  template <class T>
+  tlfea_status alloc(T** p, size_t count);
+};
+
+template <class T>
+tlfea_status Context::alloc(T** p, size_t count) {
+  size_t bytes = count * sizeof(T);
+  if (bytes == 0) bytes = sizeof(T);
+  void* q = nullptr;
+  cudaError_t err = cudaMalloc(&q, bytes);
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    return fail(TLFEA_E_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed: " +
+                                 cudaGetErrorString(err));
+  }
+  owned.push_back({q, bytes});
+  device_bytes += (int64_t)bytes;
+  *p = static_cast<T*>(q);
+  return TLFEA_OK;
+}
+
+// Entry points implemented in setup.cu / eval.cu
+tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_material* mat,
+                           const tlfea_options* opts);
+tlfea_status launch_element_kernel(Context* c, const double* x, const double* v,
+                                   bool tangent, cudaStream_t s);
+tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s);
+tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, const double* fext,
+                             double h, double* g, double* fint, bool partial_only,
+                             cudaStream_t s);
+tlfea_status launch_stress_only(Context* c, const double* x, const double* v, double* P,
+                                cudaStream_t s);
+tlfea_status launch_force_from_stress(Context* c, const double* P, cudaStream_t s);
+tlfea_status launch_residual(Context* c, const double* fint, const double* v, const double* vn,
+                             const double* fext, double h, double* g, cudaStream_t s);
+tlfea_status launch_pack_send(Context* c, double* send, bool force_only, cudaStream_t s);
+tlfea_status launch_unpack_recv(Context* c, const double* recv, double h, double* H,
+                                bool force_only, cudaStream_t s);
+tlfea_status launch_test_constitutive(const MatDev& m, int64_t n, const double* F,
+                                      const double* Fd, double* P, double* A);
+MatDev make_matdev(const tlfea_material& m);
+tlfea_status setup_exchange(Context* c, const std::vector<int32_t>& cc, const std::vector<int32_t>& part,
+                            const std::vector<int32_t>& owner, const std::vector<int64_t>& local);
+const char* last_error();
+int64_t launch_count();
+
+}  // namespace tlfea

@@ -1,0 +1,722 @@
+// setup.cu — tlfea_setup: a-1 reference precompute and a-2 fixed-sparsity
+// pattern / slot map / mass / f_ff, on the device (§4.1-4.2,
+// P:278-379).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <numeric>
+
+#include "common.cuh"
+#include "material.cuh"
+#include "shape.cuh"
+
+namespace tlfea {
+
+// ------------------------------------------------------------ error plumbing
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_err = msg; }
+tlfea_status fail(tlfea_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+void count_launch(int n) { g_launches += n; }
+const char* last_error() { return g_err.c_str(); }
+int64_t launch_count() { return g_launches.load(); }
+
+Context::~Context() {
+  for (auto& t : timed) {
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.stop);
+  }
+  for (auto& ev : event_pool) cudaEventDestroy(ev);
+  for (auto& b : owned) cudaFree(b.p);
+}
+
+MatDev make_matdev(const tlfea_material& m) {
+  MatDev d{};
+  d.model = m.model;
+  d.lam = m.E * m.nu / ((1.0 + m.nu) * (1.0 - 2.0 * m.nu));
+  d.mu = m.E / (2.0 * (1.0 + m.nu));
+  d.C10 = m.C10;
+  d.C01 = m.C01;
+  d.kappa = m.kappa;
+  d.eta = m.eta_damp;
+  d.lamd = m.lambda_damp;
+  d.kv = (m.eta_damp != 0.0 || m.lambda_damp != 0.0) ? 1 : 0;
+  d.rho0 = m.rho0;
+  return d;
+}
+
+// Temporary device storage for CUB calls (freed on scope exit)
+struct Tmp {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~Tmp() {
+    if (p) cudaFree(p);
+  }
+  tlfea_status get(size_t b) {
+    if (b <= bytes) return TLFEA_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t err = cudaMalloc(&p, b ? b : 8);
+    if (err != cudaSuccess) {
+      cudaGetLastError();
+      return fail(TLFEA_E_OOM, "temporary cudaMalloc failed");
+    }
+    bytes = b;
+    return TLFEA_OK;
+  }
+};
+
+template <class T>
+struct TmpArr {
+  T* p = nullptr;
+  ~TmpArr() {
+    if (p) cudaFree(p);
+  }
+  tlfea_status get(size_t n) {
+    cudaError_t err = cudaMalloc(&p, (n ? n : 1) * sizeof(T));
+    if (err != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      return fail(TLFEA_E_OOM, "temporary cudaMalloc of " + std::to_string(n * sizeof(T)) + " B failed");
+    }
+    return TLFEA_OK;
+  }
+};
+
+#define TL_TRY(expr)                      \
+  do {                                    \
+    tlfea_status st__ = (expr);           \
+    if (st__ != TLFEA_OK) return st__;    \
+  } while (0)
+
+static inline unsigned grid_for(int64_t n, int block) {
+  return (unsigned)std::max<int64_t>(1, (n + block - 1) / block);
+}
+
+// ----------------------------------------------------------------- kernels
+
+// a-1: per (e,q): J = sum_a X_a (x) dN_a/dxi, J0 = det J, grad_X N = dN/dxi J^{-1}
+// (P:312-320). One thread per (e,q).
+__global__ void k_precompute(int element, int64_t n_el, int nq, int nen, const int32_t* __restrict__ conn,
+                             const double* __restrict__ X, const double* __restrict__ dims,
+                             const double* __restrict__ qxi, const double* __restrict__ qw,
+                             double* __restrict__ gradN, double* __restrict__ J0w,
+                             unsigned long long* __restrict__ bad) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_el * nq) return;
+  const int64_t e = t / nq;
+  const int q = (int)(t % nq);
+  double dN[16][3];
+  const double xi[3] = {qxi[3 * q], qxi[3 * q + 1], qxi[3 * q + 2]};
+  if (element == TLFEA_T10) {
+    t10_shape(xi, nullptr, dN);
+  } else {
+    ancf_shape(xi, dims + 3 * e, nullptr, dN);
+  }
+  double J[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int a = 0; a < nen; ++a) {
+    const int64_t I = conn[e * nen + a];
+    const double x0 = X[3 * I], x1 = X[3 * I + 1], x2 = X[3 * I + 2];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      J[k] += x0 * dN[a][k];
+      J[3 + k] += x1 * dN[a][k];
+      J[6 + k] += x2 * dN[a][k];
+    }
+  }
+  const double det = det3(J);
+  if (!(det > 0.0)) atomicMin(bad, (unsigned long long)e);
+  const double r = 1.0 / det;
+  double Ji[9];
+  Ji[0] = (J[4] * J[8] - J[5] * J[7]) * r;
+  Ji[1] = (J[2] * J[7] - J[1] * J[8]) * r;
+  Ji[2] = (J[1] * J[5] - J[2] * J[4]) * r;
+  Ji[3] = (J[5] * J[6] - J[3] * J[8]) * r;
+  Ji[4] = (J[0] * J[8] - J[2] * J[6]) * r;
+  Ji[5] = (J[2] * J[3] - J[0] * J[5]) * r;
+  Ji[6] = (J[3] * J[7] - J[4] * J[6]) * r;
+  Ji[7] = (J[1] * J[6] - J[0] * J[7]) * r;
+  Ji[8] = (J[0] * J[4] - J[1] * J[3]) * r;
+  double* out = gradN + t * nen * 3;
+  for (int a = 0; a < nen; ++a)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      out[3 * a + k] = dN[a][0] * Ji[k] + dN[a][1] * Ji[3 + k] + dN[a][2] * Ji[6 + k];
+  J0w[t] = det * qw[q];
+}
+
+// Straight-sided T10 test: every mid-edge node at the midpoint of its edge.
+__global__ void k_affine_check(int64_t n_el, const int32_t* __restrict__ conn,
+                               const double* __restrict__ X, unsigned int* __restrict__ nonaffine) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n_el) return;
+  const int ea[6] = {0, 1, 2, 0, 1, 2}, eb[6] = {1, 2, 0, 3, 3, 3};
+  const int32_t* c = conn + e * 10;
+  double h = 0.0, dev = 0.0;
+  for (int m = 0; m < 6; ++m)
+    for (int k = 0; k < 3; ++k) {
+      const double xa = X[3 * (int64_t)c[ea[m]] + k], xb = X[3 * (int64_t)c[eb[m]] + k];
+      h = fmax(h, fabs(xa - xb));
+      dev = fmax(dev, fabs(X[3 * (int64_t)c[4 + m] + k] - 0.5 * (xa + xb)));
+    }
+  if (dev > 1e-12 * h) atomicOr(nonaffine, 1u);
+}
+
+// Pattern keys: (owned row << 32) | column for every element-local pair whose
+// row is owned; non-owned pairs get the sentinel ~0.
+__global__ void k_keys(int64_t n_el, int nen, const int32_t* __restrict__ conn,
+                       const int32_t* __restrict__ own_idx, unsigned long long* __restrict__ keys) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)nen * nen;
+  if (t >= n_el * per) return;
+  const int64_t e = t / per;
+  const int ab = (int)(t % per), a = ab / nen, b = ab % nen;
+  const int32_t I = conn[e * nen + a], J = conn[e * nen + b];
+  const int32_t r = own_idx[I];
+  keys[t] = r >= 0 ? (((unsigned long long)r << 32) | (unsigned)J) : ~0ull;
+}
+
+__global__ void k_split_keys(int64_t nnz, const unsigned long long* __restrict__ keys,
+                             int32_t* __restrict__ cols, int32_t* __restrict__ row,
+                             int32_t* __restrict__ cnt) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  const int32_t r = (int32_t)(keys[p] >> 32);
+  cols[p] = (int32_t)(keys[p] & 0xffffffffu);
+  row[p] = r;
+  atomicAdd(cnt + r, 1);
+}
+
+// DOF lift: row 3i+d holds 3J+e for the sorted coefficient columns J.
+__global__ void k_lift(int64_t n_own, int64_t nnz_c, const int32_t* __restrict__ rowptr_c,
+                       const int32_t* __restrict__ cols_c, const int32_t* __restrict__ blk_row,
+                       int32_t* __restrict__ rowptr, int32_t* __restrict__ cols) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < n_own) {
+    const int32_t b = rowptr_c[p], deg = rowptr_c[p + 1] - b;
+    for (int d = 0; d < 3; ++d) rowptr[3 * p + d] = 9 * b + 3 * d * deg;
+    if (p == n_own - 1) rowptr[3 * n_own] = (int32_t)(9 * nnz_c);
+  }
+  if (p >= nnz_c) return;
+  const int32_t i = blk_row[p], b = rowptr_c[i], deg = rowptr_c[i + 1] - b, k = (int32_t)p - b;
+  const int32_t J = cols_c[p];
+  for (int d = 0; d < 3; ++d)
+    for (int e = 0; e < 3; ++e) cols[9 * b + 3 * d * deg + 3 * k + e] = 3 * J + e;
+}
+
+__device__ __forceinline__ int32_t find_in_row(const int32_t* __restrict__ rowptr_c,
+                                               const int32_t* __restrict__ cols_c, int32_t r,
+                                               int32_t J) {
+  int32_t lo = rowptr_c[r], hi = rowptr_c[r + 1];
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (cols_c[mid] < J)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// Coefficient-level slot map of local elements + contribution pairs for the
+// H gather (key = slot, value = packed (e,a,b); invalid -> INT_MAX).
+__global__ void k_slots(int64_t n_el, int nen, const int32_t* __restrict__ conn,
+                        const int32_t* __restrict__ own_idx, const int32_t* __restrict__ rowptr_c,
+                        const int32_t* __restrict__ cols_c, int32_t* __restrict__ slot,
+                        int32_t* __restrict__ pkey, uint32_t* __restrict__ pval) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)nen * nen;
+  if (t >= n_el * per) return;
+  const int64_t e = t / per;
+  const int ab = (int)(t % per), a = ab / nen, b = ab % nen;
+  const int32_t r = own_idx[conn[e * nen + a]];
+  int32_t s = -1;
+  if (r >= 0) s = find_in_row(rowptr_c, cols_c, r, conn[e * nen + b]);
+  slot[t] = s;
+  if (pkey) {
+    pkey[t] = s >= 0 ? s : 0x7fffffff;
+    pval[t] = pack_eab((uint32_t)e, (uint32_t)a, (uint32_t)b);
+  }
+}
+
+__global__ void k_node_pairs(int64_t n_el, int nen, const int32_t* __restrict__ conn,
+                             const int32_t* __restrict__ own_idx, int32_t* __restrict__ key,
+                             uint32_t* __restrict__ val) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_el * nen) return;
+  const int64_t e = t / nen;
+  const int a = (int)(t % nen);
+  const int32_t r = own_idx[conn[t]];
+  key[t] = r >= 0 ? r : 0x7fffffff;
+  val[t] = ((uint32_t)e << 4) | (uint32_t)a;
+}
+
+__global__ void k_count(int64_t n, const int32_t* __restrict__ key, int32_t limit,
+                        int32_t* __restrict__ cnt) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int32_t k = key[t];
+  if (k < limit) atomicAdd(cnt + k, 1);
+}
+
+// Element mass m_ab = sum_q rho0 N_a N_b J w for the elements in
+// `conn` (setup elements); output me [n][nen][nen].
+__global__ void k_element_mass(int element, int64_t n_el, int nen, int nq, const int32_t* __restrict__ conn,
+                               const double* __restrict__ X, const double* __restrict__ dims,
+                               const double* __restrict__ qxi, const double* __restrict__ qw,
+                               double rho, double* __restrict__ me) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n_el) return;
+  double* m = me + e * nen * nen;
+  for (int r = 0; r < nen * nen; ++r) m[r] = 0.0;
+  for (int q = 0; q < nq; ++q) {
+    double N[16], dN[16][3];
+    const double xi[3] = {qxi[3 * q], qxi[3 * q + 1], qxi[3 * q + 2]};
+    if (element == TLFEA_T10)
+      t10_shape(xi, N, dN);
+    else
+      ancf_shape(xi, dims + 3 * e, N, dN);
+    double J[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int a = 0; a < nen; ++a) {
+      const int64_t I = conn[e * nen + a];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) J[3 * i + k] += X[3 * I + i] * dN[a][k];
+    }
+    const double wq = rho * det3(J) * qw[q];
+    for (int a = 0; a < nen; ++a)
+      for (int b = 0; b < nen; ++b) m[a * nen + b] += wq * N[a] * N[b];
+  }
+}
+
+// Setup-element contribution pairs for the mass gather.
+__global__ void k_mass_pairs(int64_t n_el, int nen, const int32_t* __restrict__ conn,
+                             const int32_t* __restrict__ own_idx, const int32_t* __restrict__ rowptr_c,
+                             const int32_t* __restrict__ cols_c, int32_t* __restrict__ key,
+                             int64_t* __restrict__ val) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)nen * nen;
+  if (t >= n_el * per) return;
+  const int64_t e = t / per;
+  const int ab = (int)(t % per), a = ab / nen, b = ab % nen;
+  const int32_t r = own_idx[conn[e * nen + a]];
+  key[t] = r >= 0 ? find_in_row(rowptr_c, cols_c, r, conn[e * nen + b]) : 0x7fffffff;
+  val[t] = t;
+}
+
+__global__ void k_mass_gather(int64_t nnz_c, const int32_t* __restrict__ ptr,
+                              const int64_t* __restrict__ ent, const double* __restrict__ me,
+                              double* __restrict__ M) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nnz_c) return;
+  double s = 0.0;
+  for (int32_t k = ptr[p]; k < ptr[p + 1]; ++k) s += me[ent[k]];
+  M[p] = s;
+}
+
+__global__ void k_force_field(int64_t n_own, const int32_t* __restrict__ rowptr_c,
+                              const double* __restrict__ M, double g0, double g1, double g2,
+                              double* __restrict__ fff) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_own) return;
+  double s = 0.0;
+  for (int32_t p = rowptr_c[i]; p < rowptr_c[i + 1]; ++p) s += M[p];
+  fff[3 * i] = g0 * s;
+  fff[3 * i + 1] = g1 * s;
+  fff[3 * i + 2] = g2 * s;
+}
+
+// ------------------------------------------------------------- host helpers
+
+// Sort (key,value) pairs stably by key, then build a CSR pointer over
+// [0, n_seg) and return the number of valid entries (key < n_seg).
+template <class V>
+static tlfea_status sort_and_ptr(int64_t n, int32_t* key, V* val, int64_t n_seg, int32_t* ptr_out,
+                                 V** sorted_val_out, int64_t* n_valid, TmpArr<V>& val_sorted) {
+  TmpArr<int32_t> key_sorted;
+  TL_TRY(key_sorted.get(n));
+  TL_TRY(val_sorted.get(n));
+  Tmp tmp;
+  size_t bytes = 0;
+  int end_bit = 31;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, key, key_sorted.p, val, val_sorted.p, (int64_t)n, 0, end_bit);
+  TL_TRY(tmp.get(bytes));
+  TL_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key, key_sorted.p, val, val_sorted.p, (int64_t)n, 0, end_bit));
+  count_launch();
+  // counts -> exclusive scan
+  TmpArr<int32_t> cnt;
+  TL_TRY(cnt.get(n_seg + 1));
+  TL_CUDA(cudaMemset(cnt.p, 0, (n_seg + 1) * sizeof(int32_t)));
+  k_count<<<grid_for(n, 256), 256>>>(n, key_sorted.p, (int32_t)n_seg, cnt.p);
+  TL_CHECK_LAUNCH();
+  bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, ptr_out, (int64_t)(n_seg + 1));
+  TL_TRY(tmp.get(bytes));
+  TL_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, ptr_out, (int64_t)(n_seg + 1)));
+  count_launch();
+  int32_t nv = 0;
+  TL_CUDA(cudaMemcpy(&nv, ptr_out + n_seg, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  *n_valid = nv;
+  *sorted_val_out = val_sorted.p;
+  return TLFEA_OK;
+}
+
+static tlfea_status validate(const tlfea_mesh* mesh, const tlfea_material* mat,
+                             const tlfea_options* opts) {
+  if (!mesh || !mat || !opts) return fail(TLFEA_E_INVALID, "NULL mesh/material/options");
+  if (mesh->element != TLFEA_T10 && mesh->element != TLFEA_ANCF3443)
+    return fail(TLFEA_E_INVALID, "unknown element type");
+  if (mesh->n_elements <= 0 || mesh->n_coef <= 0 || !mesh->conn || !mesh->X_ref)
+    return fail(TLFEA_E_INVALID, "empty mesh or NULL conn/X_ref");
+  if (mesh->element == TLFEA_T10 &&
+      !(opts->quadrature == TLFEA_Q_T10_4PT || opts->quadrature == TLFEA_Q_T10_KEAST5))
+    return fail(TLFEA_E_INVALID, "T10 needs quadrature TLFEA_Q_T10_4PT or TLFEA_Q_T10_KEAST5");
+  if (mesh->element == TLFEA_ANCF3443 && opts->quadrature != TLFEA_Q_GL_4x4x3)
+    return fail(TLFEA_E_INVALID, "ANCF3443 needs quadrature TLFEA_Q_GL_4x4x3");
+  if (mesh->element == TLFEA_ANCF3443 && (mesh->n_coef % 4) != 0)
+    return fail(TLFEA_E_INVALID, "ANCF3443 n_coef must be 4 * n_nodes");
+  if (mat->model == TLFEA_SVK) {
+    if (!(mat->E > 0.0) || !(mat->nu > -1.0 && mat->nu < 0.5))
+      return fail(TLFEA_E_INVALID, "SVK needs E > 0 and -1 < nu < 0.5");
+  } else if (mat->model == TLFEA_MOONEY_RIVLIN) {
+    if (!(mat->C10 >= 0.0) || !(mat->C01 >= 0.0) || !(mat->kappa > 0.0))
+      return fail(TLFEA_E_INVALID, "Mooney-Rivlin needs C10, C01 >= 0 and kappa > 0");
+  } else {
+    return fail(TLFEA_E_INVALID, "unknown material model");
+  }
+  if (!(mat->rho0 >= 0.0) || !(mat->eta_damp >= 0.0) || !(mat->lambda_damp >= 0.0))
+    return fail(TLFEA_E_INVALID, "rho0 and damping must be >= 0");
+  if (opts->mass_rule != 0 && opts->mass_rule != 1) return fail(TLFEA_E_INVALID, "mass_rule must be 0 or 1");
+  if (opts->nranks < 1 || opts->rank < 0 || opts->rank >= opts->nranks)
+    return fail(TLFEA_E_INVALID, "bad rank / nranks");
+  if (mesh->n_elements >= (1ll << 24)) return fail(TLFEA_E_OVERFLOW, "n_elements >= 2^24 (packed gather entries)");
+  if (3 * mesh->n_coef >= (1ll << 31)) return fail(TLFEA_E_OVERFLOW, "3 n_coef >= 2^31");
+  return TLFEA_OK;
+}
+
+tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_material* mat,
+                           const tlfea_options* opts) {
+  TL_TRY(validate(mesh, mat, opts));
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(TLFEA_E_CUDA, "no CUDA device available (libtlfea has no CPU fallback)");
+  }
+  if (opts->device < 0 || opts->device >= ndev) return fail(TLFEA_E_INVALID, "bad device ordinal");
+  TL_CUDA(cudaSetDevice(opts->device));
+  c->device = opts->device;
+  c->element = mesh->element;
+  c->quadrature = opts->quadrature;
+  c->nen = n_en_of(mesh->element);
+  c->nq = n_qp_of(opts->quadrature);
+  c->mass_rule = opts->mass_rule;
+  c->mat_in = *mat;
+  c->mat = make_matdev(*mat);
+  for (int k = 0; k < 3; ++k) c->gravity[k] = opts->gravity[k];
+  c->rank = opts->rank;
+  c->nranks = opts->nranks;
+  c->n_el_global = mesh->n_elements;
+  c->n_coef = mesh->n_coef;
+  const int nen = c->nen, nq = c->nq;
+  const int npe = mesh->element == TLFEA_T10 ? 10 : 4;
+  const int64_t NE = mesh->n_elements;
+
+  // ---- host: coefficient connectivity + validation (ids, distinct nodes)
+  std::vector<int32_t> cc((size_t)NE * nen);
+  for (int64_t e = 0; e < NE; ++e) {
+    const int32_t* row = mesh->conn + e * npe;
+    for (int a = 0; a < npe; ++a) {
+      const int64_t id = row[a];
+      const int64_t lim = mesh->element == TLFEA_T10 ? mesh->n_coef : mesh->n_coef / 4;
+      if (id < 0 || id >= lim)
+        return fail(TLFEA_E_INVALID, "element " + std::to_string(e) + " references node " +
+                                         std::to_string(id) + " out of range");
+      for (int b = 0; b < a; ++b)
+        if (row[b] == row[a])
+          return fail(TLFEA_E_INVALID, "element " + std::to_string(e) + " repeats node " + std::to_string(id));
+    }
+    if (mesh->element == TLFEA_T10) {
+      for (int a = 0; a < 10; ++a) cc[e * 10 + a] = row[a];
+    } else {
+      for (int k = 0; k < 4; ++k)
+        for (int m = 0; m < 4; ++m) cc[e * 16 + 4 * k + m] = 4 * row[k] + m;
+    }
+  }
+  std::vector<double> dims;
+  if (mesh->element == TLFEA_ANCF3443) {
+    dims.resize((size_t)NE * 3);
+    for (int64_t e = 0; e < NE; ++e)
+      for (int k = 0; k < 3; ++k) {
+        const double d = mesh->ancf_dims ? mesh->ancf_dims[3 * e + k] : opts->ancf_dims[k];
+        if (!(d > 0.0)) return fail(TLFEA_E_INVALID, "ANCF element dims must be > 0");
+        dims[3 * e + k] = d;
+      }
+  }
+
+  // ---- host: partition (reading Q20)
+  std::vector<int32_t> part((size_t)NE, 0);
+  if (c->nranks > 1) {
+    for (int64_t e = 0; e < NE; ++e) {
+      part[e] = opts->elem_part ? opts->elem_part[e] : (int32_t)((e * c->nranks) / NE);
+      if (part[e] < 0 || part[e] >= c->nranks) return fail(TLFEA_E_INVALID, "elem_part out of range");
+    }
+  }
+  std::vector<int32_t> owner((size_t)c->n_coef, c->nranks);
+  for (int64_t e = 0; e < NE; ++e)
+    for (int a = 0; a < nen; ++a) owner[cc[e * nen + a]] = std::min(owner[cc[e * nen + a]], part[e]);
+  for (auto& o : owner)
+    if (o == c->nranks) o = 0;  // unreferenced coefficient: owned by rank 0
+  std::vector<int32_t> own_idx((size_t)c->n_coef, -1), own_nodes;
+  for (int64_t I = 0; I < c->n_coef; ++I)
+    if (owner[I] == c->rank) {
+      own_idx[I] = (int32_t)own_nodes.size();
+      own_nodes.push_back((int32_t)I);
+    }
+  c->n_own = (int64_t)own_nodes.size();
+  std::vector<int64_t> local, setup_el;   // local elements; setup elements (touch an owned row)
+  for (int64_t e = 0; e < NE; ++e) {
+    if (part[e] == c->rank) local.push_back(e);
+    bool touches = false;
+    for (int a = 0; a < nen && !touches; ++a) touches = owner[cc[e * nen + a]] == c->rank;
+    if (touches) setup_el.push_back(e);
+  }
+  c->n_el = (int64_t)local.size();
+  const int64_t NS = (int64_t)setup_el.size();
+
+  // ---- uploads
+  double* dX = nullptr;
+  double* ddims = nullptr;
+  TL_TRY(c->alloc(&dX, (size_t)c->n_coef * 3));
+  TL_CUDA(cudaMemcpy(dX, mesh->X_ref, sizeof(double) * 3 * c->n_coef, cudaMemcpyHostToDevice));
+  std::vector<int32_t> lconn((size_t)std::max<int64_t>(c->n_el, 1) * nen), sconn((size_t)std::max<int64_t>(NS, 1) * nen);
+  std::vector<double> ldims, sdims;
+  for (int64_t i = 0; i < c->n_el; ++i)
+    std::copy(cc.begin() + local[i] * nen, cc.begin() + (local[i] + 1) * nen, lconn.begin() + i * nen);
+  for (int64_t i = 0; i < NS; ++i)
+    std::copy(cc.begin() + setup_el[i] * nen, cc.begin() + (setup_el[i] + 1) * nen, sconn.begin() + i * nen);
+  if (!dims.empty()) {
+    ldims.resize((size_t)std::max<int64_t>(c->n_el, 1) * 3);
+    sdims.resize((size_t)std::max<int64_t>(NS, 1) * 3);
+    for (int64_t i = 0; i < c->n_el; ++i)
+      for (int k = 0; k < 3; ++k) ldims[3 * i + k] = dims[3 * local[i] + k];
+    for (int64_t i = 0; i < NS; ++i)
+      for (int k = 0; k < 3; ++k) sdims[3 * i + k] = dims[3 * setup_el[i] + k];
+  }
+  TL_TRY(c->alloc(&c->conn, (size_t)c->n_el * nen));
+  TL_CUDA(cudaMemcpy(c->conn, lconn.data(), sizeof(int32_t) * c->n_el * nen, cudaMemcpyHostToDevice));
+  TL_TRY(c->alloc(&c->elem_gid, (size_t)c->n_el));
+  TL_CUDA(cudaMemcpy(c->elem_gid, local.data(), sizeof(int64_t) * c->n_el, cudaMemcpyHostToDevice));
+  if (!dims.empty()) {
+    TL_TRY(c->alloc(&ddims, ldims.size()));
+    TL_CUDA(cudaMemcpy(ddims, ldims.data(), sizeof(double) * ldims.size(), cudaMemcpyHostToDevice));
+  }
+  TL_TRY(c->alloc(&c->own_nodes, (size_t)c->n_own));
+  TL_CUDA(cudaMemcpy(c->own_nodes, own_nodes.data(), sizeof(int32_t) * c->n_own, cudaMemcpyHostToDevice));
+  TL_TRY(c->alloc(&c->own_idx, (size_t)c->n_coef));
+  TL_CUDA(cudaMemcpy(c->own_idx, own_idx.data(), sizeof(int32_t) * c->n_coef, cudaMemcpyHostToDevice));
+  TmpArr<int32_t> dsconn;
+  TmpArr<double> dsdims;
+  TL_TRY(dsconn.get((size_t)NS * nen));
+  TL_CUDA(cudaMemcpy(dsconn.p, sconn.data(), sizeof(int32_t) * NS * nen, cudaMemcpyHostToDevice));
+  if (!dims.empty()) {
+    TL_TRY(dsdims.get(sdims.size()));
+    TL_CUDA(cudaMemcpy(dsdims.p, sdims.data(), sizeof(double) * sdims.size(), cudaMemcpyHostToDevice));
+  }
+
+  // ---- a-1 precompute on local elements
+  double hq[48 * 3], hw[48];
+  const int nrule = make_rule(c->quadrature, hq, hw);
+  (void)nrule;
+  TmpArr<double> dq, dw;
+  TL_TRY(dq.get(3 * 64));
+  TL_TRY(dw.get(64));
+  TL_CUDA(cudaMemcpy(dq.p, hq, sizeof(double) * 3 * nq, cudaMemcpyHostToDevice));
+  TL_CUDA(cudaMemcpy(dw.p, hw, sizeof(double) * nq, cudaMemcpyHostToDevice));
+  TL_TRY(c->alloc(&c->gradN, (size_t)c->n_el * nq * nen * 3));
+  TL_TRY(c->alloc(&c->J0w, (size_t)c->n_el * nq));
+  TL_TRY(c->alloc(&c->err_flag, 2));
+  const unsigned long long none = ~0ull;
+  TL_CUDA(cudaMemcpy(c->err_flag, &none, sizeof(none), cudaMemcpyHostToDevice));
+  if (c->n_el > 0) {
+    k_precompute<<<grid_for(c->n_el * nq, 128), 128>>>(c->element, c->n_el, nq, nen, c->conn, dX, ddims,
+                                                       dq.p, dw.p, c->gradN, c->J0w, c->err_flag);
+    TL_CHECK_LAUNCH();
+  }
+  unsigned long long bad = 0;
+  TL_CUDA(cudaMemcpy(&bad, c->err_flag, sizeof(bad), cudaMemcpyDeviceToHost));
+  if (bad != ~0ull)
+    return fail(TLFEA_E_INVERTED_ELEMENT, "inverted element " + std::to_string(local[bad]) +
+                                              " (J0 <= 0 at a quadrature point)");
+  TL_CUDA(cudaMemcpy(c->err_flag, &none, sizeof(none), cudaMemcpyHostToDevice));
+  if (c->element == TLFEA_T10 && c->n_el > 0) {
+    unsigned int* dna = nullptr;
+    TL_TRY(c->alloc(&dna, 1));
+    TL_CUDA(cudaMemset(dna, 0, sizeof(unsigned int)));
+    k_affine_check<<<grid_for(c->n_el, 256), 256>>>(c->n_el, c->conn, dX, dna);
+    TL_CHECK_LAUNCH();
+    unsigned int na = 0;
+    TL_CUDA(cudaMemcpy(&na, dna, sizeof(na), cudaMemcpyDeviceToHost));
+    c->affine = na ? 0 : 1;
+  }
+
+  // ---- a-2 pattern over setup elements (64-bit keys, sort, unique)
+  const int64_t nkeys = NS * nen * nen;
+  {
+    TmpArr<unsigned long long> keys, keys2;
+    TL_TRY(keys.get(nkeys));
+    TL_TRY(keys2.get(nkeys));
+    k_keys<<<grid_for(nkeys, 256), 256>>>(NS, nen, dsconn.p, c->own_idx, keys.p);
+    TL_CHECK_LAUNCH();
+    Tmp tmp;
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys.p, keys2.p, (int64_t)nkeys);
+    TL_TRY(tmp.get(bytes));
+    TL_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, keys.p, keys2.p, (int64_t)nkeys));
+    count_launch();
+    TmpArr<int64_t> nsel;
+    TL_TRY(nsel.get(1));
+    bytes = 0;
+    cub::DeviceSelect::Unique(nullptr, bytes, keys2.p, keys.p, nsel.p, (int64_t)nkeys);
+    TL_TRY(tmp.get(bytes));
+    TL_CUDA(cub::DeviceSelect::Unique(tmp.p, bytes, keys2.p, keys.p, nsel.p, (int64_t)nkeys));
+    count_launch();
+    int64_t nu = 0;
+    TL_CUDA(cudaMemcpy(&nu, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    unsigned long long last = 0;
+    if (nu > 0) TL_CUDA(cudaMemcpy(&last, keys.p + nu - 1, sizeof(last), cudaMemcpyDeviceToHost));
+    c->nnz_c = nu - (nu > 0 && last == ~0ull ? 1 : 0);
+    if (9 * c->nnz_c >= (1ll << 31))
+      return fail(TLFEA_E_OVERFLOW, "DOF-level nnz = " + std::to_string(9 * c->nnz_c) + " >= 2^31");
+    TL_TRY(c->alloc(&c->cols_c, (size_t)c->nnz_c));
+    TL_TRY(c->alloc(&c->blk_row, (size_t)c->nnz_c));
+    TL_TRY(c->alloc(&c->rowptr_c, (size_t)c->n_own + 1));
+    TmpArr<int32_t> cnt;
+    TL_TRY(cnt.get(c->n_own + 1));
+    TL_CUDA(cudaMemset(cnt.p, 0, sizeof(int32_t) * (c->n_own + 1)));
+    if (c->nnz_c > 0) {
+      k_split_keys<<<grid_for(c->nnz_c, 256), 256>>>(c->nnz_c, keys.p, c->cols_c, c->blk_row, cnt.p);
+      TL_CHECK_LAUNCH();
+    }
+    bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, c->rowptr_c, (int64_t)(c->n_own + 1));
+    TL_TRY(tmp.get(bytes));
+    TL_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, c->rowptr_c, (int64_t)(c->n_own + 1)));
+    count_launch();
+  }
+  TL_TRY(c->alloc(&c->rowptr, (size_t)3 * c->n_own + 1));
+  TL_TRY(c->alloc(&c->cols, (size_t)9 * c->nnz_c));
+  if (c->n_own > 0) {
+    k_lift<<<grid_for(std::max(c->nnz_c, c->n_own), 256), 256>>>(c->n_own, c->nnz_c, c->rowptr_c, c->cols_c,
+                                                                c->blk_row, c->rowptr, c->cols);
+    TL_CHECK_LAUNCH();
+  } else {
+    TL_CUDA(cudaMemset(c->rowptr, 0, sizeof(int32_t)));
+  }
+
+  // ---- slot map of local elements + H gather lists (the slot map replaces the
+  // paper's binary search at P:520)
+  const int64_t nloc = c->n_el * nen * nen;
+  TL_TRY(c->alloc(&c->slot_c, (size_t)nloc));
+  TL_TRY(c->alloc(&c->blk_ptr, (size_t)c->nnz_c + 1));
+  {
+    TmpArr<int32_t> pkey;
+    TmpArr<uint32_t> pval, sorted;
+    TL_TRY(pkey.get(nloc));
+    TL_TRY(pval.get(nloc));
+    if (c->n_el > 0) {
+      k_slots<<<grid_for(nloc, 256), 256>>>(c->n_el, nen, c->conn, c->own_idx, c->rowptr_c, c->cols_c,
+                                            c->slot_c, pkey.p, pval.p);
+      TL_CHECK_LAUNCH();
+    }
+    uint32_t* sv = nullptr;
+    int64_t nvalid = 0;
+    TL_TRY(sort_and_ptr<uint32_t>(nloc, pkey.p, pval.p, c->nnz_c, c->blk_ptr, &sv, &nvalid, sorted));
+    TL_TRY(c->alloc(&c->blk_ent, (size_t)nvalid));
+    TL_CUDA(cudaMemcpy(c->blk_ent, sv, sizeof(uint32_t) * nvalid, cudaMemcpyDeviceToDevice));
+  }
+  TL_TRY(c->alloc(&c->node_ptr, (size_t)c->n_own + 1));
+  {
+    const int64_t n = c->n_el * nen;
+    TmpArr<int32_t> key;
+    TmpArr<uint32_t> val, sorted;
+    TL_TRY(key.get(n));
+    TL_TRY(val.get(n));
+    if (n > 0) {
+      k_node_pairs<<<grid_for(n, 256), 256>>>(c->n_el, nen, c->conn, c->own_idx, key.p, val.p);
+      TL_CHECK_LAUNCH();
+    }
+    uint32_t* sv = nullptr;
+    int64_t nvalid = 0;
+    TL_TRY(sort_and_ptr<uint32_t>(n, key.p, val.p, c->n_own, c->node_ptr, &sv, &nvalid, sorted));
+    TL_TRY(c->alloc(&c->node_ent, (size_t)nvalid));
+    TL_CUDA(cudaMemcpy(c->node_ent, sv, sizeof(uint32_t) * nvalid, cudaMemcpyDeviceToDevice));
+  }
+
+  // ---- consistent mass over the setup elements (reading Q4) and f_ff
+  TL_TRY(c->alloc(&c->M, (size_t)c->nnz_c));
+  TL_TRY(c->alloc(&c->fff, (size_t)3 * c->n_own));
+  {
+    double mq[64 * 3], mw[64];
+    int nmq;
+    if (c->element == TLFEA_T10 && c->mass_rule == 0) {
+      nmq = make_mass_rule_t10(mq, mw);
+    } else {
+      nmq = make_rule(c->quadrature, mq, mw);
+    }
+    TmpArr<double> dmq, dmw, me;
+    TL_TRY(dmq.get(3 * 64));
+    TL_TRY(dmw.get(64));
+    TL_CUDA(cudaMemcpy(dmq.p, mq, sizeof(double) * 3 * nmq, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(dmw.p, mw, sizeof(double) * nmq, cudaMemcpyHostToDevice));
+    const int64_t nm = NS * nen * nen;
+    TL_TRY(me.get(nm));
+    if (NS > 0) {
+      k_element_mass<<<grid_for(NS, 64), 64>>>(c->element, NS, nen, nmq, dsconn.p, dX, dsdims.p, dmq.p,
+                                              dmw.p, c->mat.rho0, me.p);
+      TL_CHECK_LAUNCH();
+    }
+    TmpArr<int32_t> key;
+    TmpArr<int64_t> val, sorted;
+    TL_TRY(key.get(nm));
+    TL_TRY(val.get(nm));
+    if (nm > 0) {
+      k_mass_pairs<<<grid_for(nm, 256), 256>>>(NS, nen, dsconn.p, c->own_idx, c->rowptr_c, c->cols_c, key.p,
+                                               val.p);
+      TL_CHECK_LAUNCH();
+    }
+    TmpArr<int32_t> mptr;
+    TL_TRY(mptr.get(c->nnz_c + 1));
+    int64_t* sv = nullptr;
+    int64_t nvalid = 0;
+    TL_TRY(sort_and_ptr<int64_t>(nm, key.p, val.p, c->nnz_c, mptr.p, &sv, &nvalid, sorted));
+    if (c->nnz_c > 0) {
+      k_mass_gather<<<grid_for(c->nnz_c, 256), 256>>>(c->nnz_c, mptr.p, sv, me.p, c->M);
+      TL_CHECK_LAUNCH();
+    }
+    if (c->n_own > 0) {
+      k_force_field<<<grid_for(c->n_own, 256), 256>>>(c->n_own, c->rowptr_c, c->M, c->gravity[0],
+                                                      c->gravity[1], c->gravity[2], c->fff);
+      TL_CHECK_LAUNCH();
+    }
+  }
+
+  // ---- eval scratch
+  TL_TRY(c->alloc(&c->Kscr, (size_t)c->n_el * n_ublk_of(nen) * 9));
+  TL_TRY(c->alloc(&c->fscr, (size_t)c->n_el * nen * 3));
+  TL_TRY(c->alloc(&c->fpart, (size_t)3 * std::max<int64_t>(c->n_own, 1)));
+
+  // ---- partition exchange lists
+  if (c->nranks > 1) TL_TRY(setup_exchange(c, cc, part, owner, local));
+  TL_CUDA(cudaDeviceSynchronize());
+  return TLFEA_OK;
+}
+
+}  // namespace tlfea
