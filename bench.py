@@ -384,6 +384,7 @@ def run_ours(args):
                        "material": ["svk", "mooney_rivlin"][cfg.material["model"]] + ("+kv" if kv else ""),
                        "path": "force_only" if force_only else "force+tangent+residual (tlfea_eval)",
                        "parallelism": f"element-partition x{world}" if world > 1 else "1 GPU",
+                       "geometry_classes": info["n_geometry_classes"],
                        "l2": "inputs/outputs larger than L2 (no flush needed)",
                        "nnz_per_s": 9 * info["nnz_coef"] * world / (ms_step / 1e3) if world == 1 else None,
                        "path_hbm_frac": path_b / (ms_step / 1e3) / 1e9 / hbm_peak,

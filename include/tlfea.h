@@ -146,6 +146,10 @@ typedef struct {
   int32_t affine;          /* 1 if every T10 is straight-sided (compressed layout) */
   int32_t rank, nranks;
   int64_t device_bytes;    /* device memory held by the context            */
+  int32_t n_geometry_classes; /* > 0: congruent elements share reference
+                                 tables (staged in shared memory); 0: the
+                                 per-(e,q) tables of §4.1 are read from HBM */
+  int32_t reserved;
 } tlfea_info_t;
 
 /* ---------------------------------------------------------------- setup -- */

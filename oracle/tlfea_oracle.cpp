@@ -422,9 +422,61 @@ T element_energy_t(int elem, int rule, int model, const double* mat, const doubl
 //    vertex | 8 opposite} (textbook; requires an affine element).
 //  otherwise: the element's quadrature rule, sum_q rho0 N_a N_b J0 w_q
 //    (P:309-310 literally; for ANCF3443 GL 4x4x3 is exact).
+// Gauss-Legendre nodes/weights on [-1,1] by Newton's method on P_n (plain).
+void gauss_legendre(int n, double* x, double* w) {
+  const double pi = 3.14159265358979323846;
+  for (int i = 0; i < n; ++i) {
+    double z = std::cos(pi * (i + 0.75) / (n + 0.5)), dp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= n; ++k) {
+        const double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (z * p1 - p0) / (z * z - 1.0);
+      const double dz = p1 / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-16) break;
+    }
+    x[i] = z;
+    w[i] = 2.0 / ((1.0 - z * z) * dp * dp);
+  }
+}
+
+bool t10_is_affine(const double* X, const int64_t* cf) {
+  double h = 0.0, dev = 0.0;
+  for (int m = 0; m < 6; ++m)
+    for (int k = 0; k < 3; ++k) {
+      const double xa = X[3 * cf[kT10Edge[m][0]] + k], xb = X[3 * cf[kT10Edge[m][1]] + k];
+      h = std::max(h, std::fabs(xa - xb));
+      dev = std::max(dev, std::fabs(X[3 * cf[4 + m] + k] - 0.5 * (xa + xb)));
+    }
+  return dev <= 1e-12 * h;
+}
+
 void element_mass(int elem, int rule, int mass_rule, double rho, const double* X,
                   const int64_t* cf, const double* LWH, double* me) {
   const int nen = n_en_of(elem);
+  if (elem == 0 && mass_rule == 0 && !t10_is_affine(X, cf)) {
+    // Exact mass of a curved T10 (reading Q4): N_a N_b det J has degree <= 7;
+    // collapsed (Duffy) 6x6x6 Gauss-Legendre rule, exact to degree 9.
+    double g[6], gw[6];
+    gauss_legendre(6, g, gw);
+    for (int r = 0; r < 100; ++r) me[r] = 0.0;
+    for (int i = 0; i < 6; ++i)
+      for (int j = 0; j < 6; ++j)
+        for (int k = 0; k < 6; ++k) {
+          const double u = 0.5 * (g[i] + 1.0), s = 0.5 * (g[j] + 1.0), t = 0.5 * (g[k] + 1.0);
+          const double xi[3] = {u, s * (1.0 - u), t * (1.0 - u) * (1.0 - s)};
+          const double wq = 0.125 * gw[i] * gw[j] * gw[k] * (1.0 - u) * (1.0 - u) * (1.0 - s);
+          double gN[16][3], N[16];
+          const double J0 = geom_at(elem, X, cf, LWH, xi, gN, N);
+          for (int a = 0; a < 10; ++a)
+            for (int b = 0; b < 10; ++b) me[a * 10 + b] += rho * N[a] * N[b] * J0 * wq;
+        }
+    return;
+  }
   if (elem == 0 && mass_rule == 0) {
     const double* p[4];
     for (int i = 0; i < 4; ++i) p[i] = X + 3 * cf[i];

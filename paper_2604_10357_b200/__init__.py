@@ -20,7 +20,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtlfea.so")
+LIB_PATH = os.environ.get("TLFEA_LIB") or os.path.join(_HERE, "libtlfea.so")
 _lib = None
 _lock = threading.Lock()
 
@@ -59,7 +59,8 @@ class Info(C.Structure):
     _fields_ = [("element", C.c_int32), ("quadrature", C.c_int32), ("n_qp", C.c_int32), ("n_en", C.c_int32),
                 ("n_elements", C.c_int64), ("n_elements_global", C.c_int64), ("n_coef", C.c_int64),
                 ("n_dof", C.c_int64), ("nnz_coef", C.c_int64), ("nnz", C.c_int64), ("n_owned_nodes", C.c_int64),
-                ("affine", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32), ("device_bytes", C.c_int64)]
+                ("affine", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32), ("device_bytes", C.c_int64),
+                ("n_geometry_classes", C.c_int32), ("reserved", C.c_int32)]
 
 
 _vp, _i64, _i32, _d = C.c_void_p, C.c_int64, C.c_int32, C.c_double

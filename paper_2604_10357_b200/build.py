@@ -15,8 +15,10 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libtlfea.so")
-BUILD = os.path.join(HERE, "build")
+VARIANT = os.environ.get("TLFEA_VARIANT", "")          # e.g. "minb2" -> libtlfea_minb2.so
+DEFINES = os.environ.get("TLFEA_DEFINES", "").split()   # e.g. "-DTLFEA_T10_MINB=2"
+OUT = os.path.join(HERE, f"libtlfea{'_' + VARIANT if VARIANT else ''}.so")
+BUILD = os.path.join(HERE, "build" + (f"_{VARIANT}" if VARIANT else ""))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2",
@@ -46,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *DEFINES, *extra, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

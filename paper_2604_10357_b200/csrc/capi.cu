@@ -113,6 +113,8 @@ tlfea_status tlfea_info(tlfea_ctx ctx, tlfea_info_t* o) {
   o->rank = c.rank;
   o->nranks = c.nranks;
   o->device_bytes = c.device_bytes;
+  o->n_geometry_classes = c.n_cls;
+  o->reserved = 0;
   return TLFEA_OK;
 }
 

@@ -99,6 +99,21 @@ struct Context {
   uint32_t* blk_ent = nullptr;    // [...] packed (e,a,b), e ascending per block
   int32_t* node_ptr = nullptr;    // [n_own+1]
   uint32_t* node_ent = nullptr;   // [...] (e << 4 | a)
+  // geometry classes: congruent elements share one reference table
+  // (gradN + J0w); the eval kernels then read it from shared memory.
+  int n_cls = 0;                  // 0 = per-element tables (gradN / J0w above)
+  uint8_t* cls = nullptr;         // [n_el] class id
+  double* cls_tab = nullptr;      // [n_cls][nq][nen*3 + 1]  (gradN then J0w)
+  // symmetric H gather units (upper blocks + blocks whose transpose is not owned)
+  int64_t n_units = 0;
+  int32_t* unit_p = nullptr;      // [n_units] coefficient block of (I,J)
+  int32_t* unit_pT = nullptr;     // [n_units] block of (J,I) in row J, -1 if none
+  // gather-sorted scratch (single-rank contexts): element upper block ub of
+  // element e is written to position dest[e][ub] >> 1 (transposed if the low
+  // bit is set), so the H gather streams unit_ptr[u] .. unit_ptr[u+1].
+  int32_t* dest = nullptr;        // [n_el][n_ublk]
+  int32_t* unit_ptr = nullptr;    // [n_units+1]
+  int32_t* fdest = nullptr;       // [n_el][nen] position of f_a in the node-sorted force scratch
   double* Kscr = nullptr;         // [n_el][n_ublk][9]
   double* fscr = nullptr;         // [n_el][nen][3]
   unsigned long long* err_flag = nullptr;  // min over (e*64+q) with det F <= 0 (MR)

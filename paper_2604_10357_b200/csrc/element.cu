@@ -1,0 +1,541 @@
+// element.cu — fused Stage 1 + Stage 2 element kernel and the deterministic
+// symmetric H gather of libtlfea (B200 / sm_100a, fp64).
+//
+// k_element (§4.3 Stage 1/2, Eq. tangent_block):
+//   one lane per element node a (T10: 10 lanes, 3 elements per warp; ANCF3443:
+//   32 lanes = 2 per node, 1 element per warp). Per quadrature point the lanes
+//   reduce F = sum_a x_a (x) grad N_a (Eq. F_assembly) through a conflict-light
+//   shared-memory transpose, evaluate S and P in registers (Stage 1 never
+//   touches HBM), accumulate f_a = sum_q P grad N_a J0 w (Eq. fint_local) and
+//   the upper 3x3 tangent blocks K_ab (a <= b) each lane owns: a circulant
+//   split of the n(n+1)/2 blocks (5-6 per T10 lane, 4-5 per ANCF lane).
+//   SVK: K_ab = s_ab I + lam g_a g_b^T + mu g_b g_a^T + mu d_ab F F^T with
+//   g_a = F grad N_a, s_ab = grad N_a . S grad N_b, d_ab = grad N_a . grad N_b
+//   (three FMAs per entry); MR: K_ab = s_ab I + B_a^T C B_b (C the 6x6
+//   material tangent, 6 lanes per element build its columns).
+//   Reference data come either from per-(e,q) tables in HBM (the paper's
+//   layout) or, for congruent elements, from per-class tables staged once per
+//   CTA in shared memory (no per-q global loads).
+// k_gather_units (north star (d), deterministic scatter): one thread per
+//   symmetric pair of coefficient blocks {(I,J),(J,I)}: sums the contributing
+//   element blocks in ascending element order through the inverse slot map,
+//   writes h K + M/h to (I,J) and its transpose to (J,I); every H value is
+//   written exactly once and every scratch block is read exactly once.
+#include "common.cuh"
+#include "material.cuh"
+
+namespace tlfea {
+
+static inline unsigned gridn(int64_t n, int block) {
+  return (unsigned)std::max<int64_t>(1, (n + block - 1) / block);
+}
+
+template <int ELEM>
+struct Geo;
+template <>
+struct Geo<0> {  // T10
+  static constexpr int NEN = 10, GROUP = 10, EPW = 3, NUB = 55, NB = 6;
+};
+template <>
+struct Geo<1> {  // ANCF3443
+  static constexpr int NEN = 16, GROUP = 32, EPW = 1, NUB = 136, NB = 5;
+};
+
+__host__ __device__ __forceinline__ int ublk(int n, int a, int b) {  // a <= b
+  return a * n - (a * (a - 1)) / 2 + (b - a);
+}
+
+constexpr int kWarps = 4;  // warps per CTA
+constexpr int kLD = 33;    // padded lane stride of the per-warp shared tables
+
+// Blocks owned by a lane: index j -> partner b (-1 when none).
+template <int ELEM>
+__device__ __forceinline__ int partner(int a, int half, int j) {
+  if (ELEM == 0) {
+    if (j < 5) return (a + j) % 10;
+    return a < 5 ? a + 5 : -1;
+  } else {
+    if (half == 0) return j < 4 ? (a + j) & 15 : -1;
+    if (j < 4) return (a + 4 + j) & 15;
+    return a < 8 ? a + 8 : -1;
+  }
+}
+
+#ifndef TLFEA_T10_MINB
+#define TLFEA_T10_MINB 3  // T10 SVK: 3 CTAs of 4 warps per SM (<= 168 registers)
+#endif
+
+template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS>
+__global__ void __launch_bounds__(kWarps * 32, (ELEM == 0 && MODEL == 0) ? TLFEA_T10_MINB : 2)
+    k_element(int64_t n_el, const int32_t* __restrict__ conn, const double* __restrict__ gradN,
+              const double* __restrict__ J0w, const uint8_t* __restrict__ cls, const double* __restrict__ cls_tab,
+              int n_cls, const double* __restrict__ x, const double* __restrict__ v, MatDev mat,
+              double* __restrict__ fscr, double* __restrict__ Kscr, const int32_t* __restrict__ dest,
+              const int32_t* __restrict__ fdest, unsigned long long* __restrict__ err) {
+  using G = Geo<ELEM>;
+  constexpr int NEN = G::NEN, GROUP = G::GROUP, EPW = G::EPW, NUB = G::NUB, NB = G::NB;
+  constexpr int NC = KV ? 18 : 9;            // reduced components (F, Fdot)
+  constexpr int ND = MODEL == 0 ? 6 : 21;    // per-node data shared for the blocks
+  constexpr int TABW = NEN * 3 + 1;          // class table row: gradN (3 NEN) + J0w
+  __shared__ double s_part[kWarps][NC][kLD];
+  __shared__ double s_F[kWarps][EPW][NC];
+  __shared__ double s_node[kWarps][TAN ? ND : 1][kLD];
+  __shared__ double s_C[kWarps][EPW][MODEL == 1 && TAN ? 36 : 1];
+  extern __shared__ double s_tab[];          // CLS: [n_cls][NQ][TABW]
+
+  if (CLS) {
+    const int tot = n_cls * NQ * TABW;
+    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_tab[t] = cls_tab[t];
+    __syncthreads();
+  }
+
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const bool lane_active = ELEM == 0 ? (lane < EPW * GROUP) : true;
+  const int g = (ELEM == 0 && lane_active) ? lane / GROUP : 0;
+  const int a = ELEM == 0 ? (lane_active ? lane % GROUP : 0) : (lane & 15);
+  const int half = ELEM == 0 ? 0 : (lane >> 4);
+  const int64_t e = ((int64_t)blockIdx.x * kWarps + wib) * EPW + g;
+  const bool valid = lane_active && e < n_el;
+  const int gbase = g * GROUP;
+
+  double xa[3] = {0, 0, 0}, va[3] = {0, 0, 0};
+  int ce = 0;
+  if (valid) {
+    const int64_t I = conn[e * NEN + a];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) xa[i] = x[3 * I + i];
+    if (KV) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) va[i] = v[3 * I + i];
+    }
+    if (CLS) ce = cls[e];
+  }
+  double fa[3] = {0, 0, 0};
+  double K[TAN ? NB : 1][9];
+#pragma unroll
+  for (int j = 0; j < (TAN ? NB : 1); ++j)
+#pragma unroll
+    for (int r = 0; r < 9; ++r) K[j][r] = 0.0;
+
+#pragma unroll 1
+  for (int q = 0; q < NQ; ++q) {
+    double gN[3] = {0, 0, 0}, w = 0.0;
+    if (valid) {
+      if (CLS) {
+        const double* t = s_tab + (ce * NQ + q) * TABW;
+        gN[0] = t[3 * a];
+        gN[1] = t[3 * a + 1];
+        gN[2] = t[3 * a + 2];
+        w = t[3 * NEN];
+      } else {
+        const double* src = gradN + ((e * NQ + q) * NEN + a) * 3;
+        gN[0] = src[0];
+        gN[1] = src[1];
+        gN[2] = src[2];
+        w = J0w[e * NQ + q];
+      }
+    }
+    // ---- F (and Fdot) = sum_a x_a (x) grad N_a, reduced over the element's lanes
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int J = 0; J < 3; ++J) {
+        s_part[wib][3 * i + J][lane] = xa[i] * gN[J];
+        if (KV) s_part[wib][9 + 3 * i + J][lane] = va[i] * gN[J];
+      }
+    __syncwarp();
+    if (ELEM == 0) {
+      if (lane_active && a < 9) {
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < NEN; ++b) s += s_part[wib][a][gbase + b];
+        s_F[wib][g][a] = s;
+        if (KV) {
+          double sd = 0.0;
+#pragma unroll
+          for (int b = 0; b < NEN; ++b) sd += s_part[wib][9 + a][gbase + b];
+          s_F[wib][g][9 + a] = sd;
+        }
+      }
+    } else {
+      const int comp = lane & 15;
+      if (comp < 9 && (KV || half == 0)) {
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < NEN; ++b) s += s_part[wib][9 * half + comp][b];
+        s_F[wib][0][9 * half + comp] = s;
+      }
+    }
+    __syncwarp();
+    double F[9], Fd[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      F[r] = s_F[wib][g][r];
+      if (KV) Fd[r] = s_F[wib][g][9 + r];
+    }
+    // ---- Stage 1: constitutive update (registers only)
+    double S[6], St[6];
+    MRState ms;
+    if (MODEL == 0) {
+      svk_S(F, mat.lam, mat.mu, S);
+    } else {
+      mr_state(F, ms);
+      if (valid && !(ms.J > 0.0) && a == 0 && half == 0) atomicMin(err, (unsigned long long)(e * 64 + q));
+      mr_S(ms, mat.C10, mat.C01, mat.kappa, S);
+    }
+#pragma unroll
+    for (int r = 0; r < 6; ++r) St[r] = S[r];
+    if (KV) {
+      double Sv[6];
+      kv_S(F, Fd, mat.eta, mat.lamd, Sv);
+#pragma unroll
+      for (int r = 0; r < 6; ++r) St[r] += Sv[r];
+    }
+    // ---- Stage 2 force: f_a += F (w S_tot grad N_a)
+    {
+      double t[3];
+#pragma unroll
+      for (int I = 0; I < 3; ++I)
+        t[I] = w * (sget(St, I, 0) * gN[0] + sget(St, I, 1) * gN[1] + sget(St, I, 2) * gN[2]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) fa[i] = fma(F[3 * i], t[0], fma(F[3 * i + 1], t[1], fma(F[3 * i + 2], t[2], fa[i])));
+    }
+    if (TAN) {
+      double tw[3];  // w * S_el grad N_a (geometric stiffness)
+#pragma unroll
+      for (int I = 0; I < 3; ++I)
+        tw[I] = w * (sget(S, I, 0) * gN[0] + sget(S, I, 1) * gN[1] + sget(S, I, 2) * gN[2]);
+      if (MODEL == 0) {
+        double ga[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ga[i] = F[3 * i] * gN[0] + F[3 * i + 1] * gN[1] + F[3 * i + 2] * gN[2];
+        double B[6];  // F F^T (Voigt)
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv) {
+          int i, k;
+          voigt_pair(vv, i, k);
+          B[vv] = F[3 * i] * F[3 * k] + F[3 * i + 1] * F[3 * k + 1] + F[3 * i + 2] * F[3 * k + 2];
+        }
+        s_node[wib][0][lane] = ga[0];
+        s_node[wib][1][lane] = ga[1];
+        s_node[wib][2][lane] = ga[2];
+        s_node[wib][3][lane] = gN[0];
+        s_node[wib][4][lane] = gN[1];
+        s_node[wib][5][lane] = gN[2];
+        const double lw = mat.lam * w, mw = mat.mu * w;
+        const double gl[3] = {lw * ga[0], lw * ga[1], lw * ga[2]};
+        const double gm[3] = {mw * ga[0], mw * ga[1], mw * ga[2]};
+        const double gNm[3] = {mw * gN[0], mw * gN[1], mw * gN[2]};
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          const int b = partner<ELEM>(a, half, j);
+          if (b < 0) continue;
+          const int lb = gbase + b;
+          const double gb[3] = {s_node[wib][0][lb], s_node[wib][1][lb], s_node[wib][2][lb]};
+          const double nb[3] = {s_node[wib][3][lb], s_node[wib][4][lb], s_node[wib][5][lb]};
+          const double s = fma(tw[0], nb[0], fma(tw[1], nb[1], tw[2] * nb[2]));
+          const double d = fma(gNm[0], nb[0], fma(gNm[1], nb[1], gNm[2] * nb[2]));
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              double acc = fma(gl[i], gb[k], fma(gb[i], gm[k], fma(d, B[vidx(i, k)], K[j][3 * i + k])));
+              K[j][3 * i + k] = (i == k) ? acc + s : acc;
+            }
+        }
+      } else {
+        // MR: material tangent columns (6 lanes per element), B_a, w C B_a
+        if (lane_active && (ELEM == 0 || half == 0)) {
+          const int col = ELEM == 0 ? a : lane;
+          if (col < 6) {
+            double cc[6];
+            mr_Cv_column_dispatch(ms, mat.C10, mat.C01, mat.kappa, col, cc);
+#pragma unroll
+            for (int vv = 0; vv < 6; ++vv) s_C[wib][g][6 * vv + col] = w * cc[vv];
+          }
+        }
+        double Ba[6][3];
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv) {
+          int I, J;
+          voigt_pair(vv, I, J);
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+            Ba[vv][i] = (I == J) ? F[3 * i + I] * gN[I] : F[3 * i + I] * gN[J] + F[3 * i + J] * gN[I];
+        }
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv)
+#pragma unroll
+          for (int i = 0; i < 3; ++i) s_node[wib][3 * vv + i][lane] = Ba[vv][i];
+        s_node[wib][18][lane] = gN[0];
+        s_node[wib][19][lane] = gN[1];
+        s_node[wib][20][lane] = gN[2];
+        __syncwarp();
+        double CB[6][3];
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv)
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < 6; ++ww) s = fma(s_C[wib][g][6 * vv + ww], Ba[ww][i], s);
+            CB[vv][i] = s;
+          }
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          const int b = partner<ELEM>(a, half, j);
+          if (b < 0) continue;
+          const int lb = gbase + b;
+          const double s = fma(tw[0], s_node[wib][18][lb], fma(tw[1], s_node[wib][19][lb], tw[2] * s_node[wib][20][lb]));
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            double bb[6];
+#pragma unroll
+            for (int vv = 0; vv < 6; ++vv) bb[vv] = s_node[wib][3 * vv + k][lb];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              double acc = K[j][3 * i + k];
+#pragma unroll
+              for (int vv = 0; vv < 6; ++vv) acc = fma(CB[vv][i], bb[vv], acc);
+              K[j][3 * i + k] = (i == k) ? acc + s : acc;
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  if (!valid) return;
+  if (ELEM == 0 || half == 0) {
+    double* fo = fscr + (fdest ? (int64_t)fdest[e * NEN + a] : e * NEN + a) * 3;
+    fo[0] = fa[0];
+    fo[1] = fa[1];
+    fo[2] = fa[2];
+  }
+  if (TAN) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int b = partner<ELEM>(a, half, j);
+      if (b < 0) continue;
+      const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
+      // element-major: store the upper block K_{min,max}; gather-sorted: the
+      // orientation the receiving unit needs (dest low bit)
+      bool tr = a > b;
+      int64_t pos = e * NUB + ub;
+      if (dest) {
+        const int32_t d = dest[e * NUB + ub];
+        pos = d >> 1;
+        tr = tr != ((d & 1) != 0);
+      }
+      double* o = Kscr + pos * 9;
+      if (!tr) {
+#pragma unroll
+        for (int r = 0; r < 9; ++r) o[r] = K[j][r];
+      } else {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) o[3 * k + i] = K[j][3 * i + k];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ gather
+
+__device__ __forceinline__ void sum_block(const uint32_t* __restrict__ ent, int32_t t0, int32_t t1, int nen,
+                                          int nub, const double* __restrict__ Kscr, double acc[9]) {
+#pragma unroll
+  for (int r = 0; r < 9; ++r) acc[r] = 0.0;
+  for (int32_t t = t0; t < t1; ++t) {
+    const uint32_t en = __ldg(ent + t);
+    const int64_t e = en >> 8;
+    const int a = (en >> 4) & 15, b = en & 15;
+    double s[9];
+    const double* src = Kscr + (e * nub + (a <= b ? ublk(nen, a, b) : ublk(nen, b, a))) * 9;
+#pragma unroll
+    for (int r = 0; r < 9; ++r) s[r] = __ldcs(src + r);  // streamed: each block is read once
+    if (a <= b) {
+#pragma unroll
+      for (int r = 0; r < 9; ++r) acc[r] += s[r];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[3 * i + k] += s[3 * k + i];
+    }
+  }
+}
+
+// One thread per gather unit (I,J) [+ its transpose (J,I)]:
+//   H(I,J) = h sum_e K_e + M_IJ/h I,  H(J,I) = H(I,J)^T   (Eq. hessian)
+__global__ void k_gather_units(int64_t n_units, int nen, int nub, const int32_t* __restrict__ unit_p,
+                               const int32_t* __restrict__ unit_pT, const int32_t* __restrict__ blk_row,
+                               const int32_t* __restrict__ rowptr_c, const int32_t* __restrict__ blk_ptr,
+                               const uint32_t* __restrict__ blk_ent, const int32_t* __restrict__ unit_ptr,
+                               const double* __restrict__ Kscr, const double* __restrict__ M, double h,
+                               double* __restrict__ H) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n_units) return;
+  const int32_t p = unit_p[u], pT = unit_pT[u];
+  double acc[9];
+  if (unit_ptr) {  // gather-sorted scratch: contiguous, already oriented
+#pragma unroll
+    for (int r = 0; r < 9; ++r) acc[r] = 0.0;
+    for (int32_t t = unit_ptr[u]; t < unit_ptr[u + 1]; ++t) {
+      const double* src = Kscr + (int64_t)t * 9;
+#pragma unroll
+      for (int r = 0; r < 9; ++r) acc[r] += src[r];
+    }
+  } else {
+    sum_block(blk_ent, blk_ptr[p], blk_ptr[p + 1], nen, nub, Kscr, acc);
+  }
+  const double mh = M[p] / h;
+  {
+    const int32_t i = blk_row[p], b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0, k = p - b0;
+    double* out = H + 9 * (int64_t)b0 + 3 * k;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int f = 0; f < 3; ++f) out[3 * d * deg + f] = fma(h, acc[3 * d + f], d == f ? mh : 0.0);
+  }
+  if (pT >= 0) {
+    const int32_t i = blk_row[pT], b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0, k = pT - b0;
+    double* out = H + 9 * (int64_t)b0 + 3 * k;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int f = 0; f < 3; ++f) out[3 * d * deg + f] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
+  }
+}
+
+// Warp-cooperative variant for the gather-sorted scratch: a warp owns 32
+// consecutive units whose scratch blocks form one contiguous range; the warp
+// streams that range with coalesced loads through a shared-memory window and
+// each lane then sums its own unit's blocks (fixed order = element order).
+constexpr int kGWarps = 8;
+constexpr int kGWin = 720;  // doubles of staging per warp (80 blocks, 5.6 KB; 45 KB per CTA)
+
+__global__ void __launch_bounds__(kGWarps * 32)
+    k_gather_units_sorted(int64_t n_units, const int32_t* __restrict__ unit_p, const int32_t* __restrict__ unit_pT,
+                          const int32_t* __restrict__ blk_row, const int32_t* __restrict__ rowptr_c,
+                          const int32_t* __restrict__ unit_ptr, const double* __restrict__ Kscr,
+                          const double* __restrict__ M, double h, double* __restrict__ H) {
+  __shared__ double s_win[kGWarps][kGWin];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t u0 = ((int64_t)blockIdx.x * kGWarps + wib) * 32;
+  if (u0 >= n_units) return;
+  const int64_t u = u0 + lane;
+  const bool valid = u < n_units;
+  const int64_t uend = min(u0 + 32, n_units);
+  const int64_t P0 = unit_ptr[u0], P1 = unit_ptr[uend];
+  const int32_t my0 = valid ? unit_ptr[u] : 0, my1 = valid ? unit_ptr[u + 1] : 0;
+  double acc[9];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) acc[r] = 0.0;
+  // stream [P0, P1) blocks in windows of kGWin/9 blocks
+  constexpr int WB = kGWin / 9;
+  for (int64_t w0 = P0; w0 < P1; w0 += WB) {
+    const int64_t w1 = min(w0 + (int64_t)WB, P1);
+    const int64_t nd = (w1 - w0) * 9;
+    const double* src = Kscr + w0 * 9;
+    for (int64_t t = lane; t < nd; t += 32) s_win[wib][t] = __ldcs(src + t);
+    __syncwarp();
+    const int64_t a0 = max((int64_t)my0, w0), a1 = min((int64_t)my1, w1);
+    for (int64_t t = a0; t < a1; ++t) {
+      const double* sb = &s_win[wib][(t - w0) * 9];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) acc[r] += sb[r];
+    }
+    __syncwarp();
+  }
+  if (!valid) return;
+  const int32_t p = unit_p[u], pT = unit_pT[u];
+  const double mh = M[p] / h;
+  {
+    const int32_t i = blk_row[p], b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0, k = p - b0;
+    double* out = H + 9 * (int64_t)b0 + 3 * k;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int f = 0; f < 3; ++f) out[3 * d * deg + f] = fma(h, acc[3 * d + f], d == f ? mh : 0.0);
+  }
+  if (pT >= 0) {
+    const int32_t i = blk_row[pT], b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0, k = pT - b0;
+    double* out = H + 9 * (int64_t)b0 + 3 * k;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int f = 0; f < 3; ++f) out[3 * d * deg + f] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
+  }
+}
+
+// ------------------------------------------------------------- launchers
+
+template <int ELEM, int NQ, int MODEL, bool KV, bool TAN>
+static tlfea_status launch_el(Context* c, const double* x, const double* v, cudaStream_t s) {
+  using G = Geo<ELEM>;
+  const int64_t per_cta = (int64_t)kWarps * G::EPW;
+  const unsigned grid = (unsigned)((c->n_el + per_cta - 1) / per_cta);
+  if (grid == 0) return TLFEA_OK;
+  if (c->n_cls > 0) {
+    const size_t smem = sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
+    static size_t smem_set = 0;  // per template instantiation
+    if (smem > smem_set) {
+      TL_CUDA(cudaFuncSetAttribute(k_element<ELEM, NQ, MODEL, KV, TAN, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      smem_set = smem;
+    }
+    k_element<ELEM, NQ, MODEL, KV, TAN, true><<<grid, kWarps * 32, smem, s>>>(
+        c->n_el, c->conn, c->gradN, c->J0w, c->cls, c->cls_tab, c->n_cls, x, v, c->mat, c->fscr, c->Kscr,
+        c->dest, c->fdest, c->err_flag);
+  } else {
+    k_element<ELEM, NQ, MODEL, KV, TAN, false><<<grid, kWarps * 32, 0, s>>>(
+        c->n_el, c->conn, c->gradN, c->J0w, c->cls, c->cls_tab, 0, x, v, c->mat, c->fscr, c->Kscr, c->dest,
+        c->fdest, c->err_flag);
+  }
+  TL_CHECK_LAUNCH();
+  return TLFEA_OK;
+}
+
+template <int ELEM, int NQ, int MODEL>
+static tlfea_status launch_el_kv(Context* c, const double* x, const double* v, bool tan, cudaStream_t s) {
+  const bool kv = c->mat.kv && v != nullptr;
+  if (tan) return kv ? launch_el<ELEM, NQ, MODEL, true, true>(c, x, v, s) : launch_el<ELEM, NQ, MODEL, false, true>(c, x, v, s);
+  return kv ? launch_el<ELEM, NQ, MODEL, true, false>(c, x, v, s) : launch_el<ELEM, NQ, MODEL, false, false>(c, x, v, s);
+}
+
+template <int ELEM, int NQ>
+static tlfea_status launch_el_model(Context* c, const double* x, const double* v, bool tan, cudaStream_t s) {
+  if (c->mat.model == TLFEA_SVK) return launch_el_kv<ELEM, NQ, 0>(c, x, v, tan, s);
+  return launch_el_kv<ELEM, NQ, 1>(c, x, v, tan, s);
+}
+
+tlfea_status launch_element_kernel(Context* c, const double* x, const double* v, bool tangent,
+                                   cudaStream_t s) {
+  if (c->element == TLFEA_T10) {
+    if (c->nq == 4) return launch_el_model<0, 4>(c, x, v, tangent, s);
+    return launch_el_model<0, 5>(c, x, v, tangent, s);
+  }
+  return launch_el_model<1, 48>(c, x, v, tangent, s);
+}
+
+tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
+  if (c->n_units == 0) return TLFEA_OK;
+  if (c->unit_ptr) {
+    const int64_t per = (int64_t)kGWarps * 32;
+    k_gather_units_sorted<<<(unsigned)((c->n_units + per - 1) / per), kGWarps * 32, 0, s>>>(
+        c->n_units, c->unit_p, c->unit_pT, c->blk_row, c->rowptr_c, c->unit_ptr, c->Kscr, c->M, h, H);
+    TL_CHECK_LAUNCH();
+    return TLFEA_OK;
+  }
+  k_gather_units<<<gridn(c->n_units, 256), 256, 0, s>>>(c->n_units, c->nen, n_ublk_of(c->nen), c->unit_p,
+                                                        c->unit_pT, c->blk_row, c->rowptr_c, c->blk_ptr,
+                                                        c->blk_ent, c->unit_ptr, c->Kscr, c->M, h, H);
+  TL_CHECK_LAUNCH();
+  return TLFEA_OK;
+}
+
+}  // namespace tlfea

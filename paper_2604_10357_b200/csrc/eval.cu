@@ -25,325 +25,6 @@ static inline unsigned grid_for(int64_t n, int block) {
   return (unsigned)std::max<int64_t>(1, (n + block - 1) / block);
 }
 
-template <int ELEM>
-struct Geo;
-template <>
-struct Geo<0> {  // T10
-  static constexpr int NEN = 10, GROUP = 10, EPW = 3, NUB = 55;
-};
-template <>
-struct Geo<1> {  // ANCF3443
-  static constexpr int NEN = 16, GROUP = 32, EPW = 1, NUB = 136;
-};
-
-__host__ __device__ __forceinline__ int ublk(int n, int a, int b) {  // a <= b
-  return a * n - (a * (a - 1)) / 2 + (b - a);
-}
-
-constexpr int kWarps = 4;  // warps per CTA of the element kernel
-
-template <int ELEM>
-__device__ __forceinline__ int max_blocks() {
-  return ELEM == 0 ? 6 : 5;
-}
-
-// Blocks owned by a lane: index j -> partner b (returns -1 when none).
-template <int ELEM>
-__device__ __forceinline__ int partner(int a, int half, int j) {
-  if (ELEM == 0) {
-    if (j < 5) return (a + j) % 10;
-    return a < 5 ? a + 5 : -1;
-  } else {
-    if (half == 0) return j < 4 ? (a + j) & 15 : -1;
-    if (j < 4) return (a + 4 + j) & 15;
-    return a < 8 ? a + 8 : -1;
-  }
-}
-
-template <int ELEM, int NQ, int MODEL, bool KV, bool TAN>
-__global__ void __launch_bounds__(kWarps * 32)
-    k_element(int64_t n_el, const int32_t* __restrict__ conn, const double* __restrict__ gradN,
-              const double* __restrict__ J0w, const double* __restrict__ x, const double* __restrict__ v,
-              MatDev mat, double* __restrict__ fscr, double* __restrict__ Kscr,
-              unsigned long long* __restrict__ err) {
-  using G = Geo<ELEM>;
-  constexpr int NEN = G::NEN, GROUP = G::GROUP, EPW = G::EPW, NUB = G::NUB;
-  constexpr int NB = ELEM == 0 ? 6 : 5;
-  constexpr int ND = MODEL == 0 ? 6 : 21;  // per-node shared data for the blocks
-  __shared__ double s_part[kWarps][32][KV ? 18 : 9];
-  __shared__ double s_F[kWarps][EPW][KV ? 18 : 9];
-  __shared__ double s_node[kWarps][32][TAN ? ND : 1];
-  __shared__ double s_C[kWarps][EPW][MODEL == 1 && TAN ? 36 : 1];
-
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const bool lane_active = ELEM == 0 ? (lane < EPW * GROUP) : true;
-  const int g = (ELEM == 0 && lane_active) ? lane / GROUP : 0;  // element slot in the warp
-  const int a = ELEM == 0 ? (lane_active ? lane % GROUP : 0) : (lane & 15);
-  const int half = ELEM == 0 ? 0 : (lane >> 4);
-  const int64_t e = ((int64_t)blockIdx.x * kWarps + wib) * EPW + (lane_active ? g : 0);
-  const bool valid = lane_active && e < n_el;
-  const int gbase = g * GROUP;  // first lane of this element's group
-
-  // gather nodal coordinates (and velocities) once
-  double xa[3] = {0, 0, 0}, va[3] = {0, 0, 0};
-  if (valid) {
-    const int64_t I = conn[e * NEN + a];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) xa[i] = x[3 * I + i];
-    if (KV) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i) va[i] = v[3 * I + i];
-    }
-  }
-  double fa[3] = {0, 0, 0};
-  double K[TAN ? NB : 1][9];
-#pragma unroll
-  for (int j = 0; j < (TAN ? NB : 1); ++j)
-#pragma unroll
-    for (int r = 0; r < 9; ++r) K[j][r] = 0.0;
-
-  for (int q = 0; q < NQ; ++q) {
-    double gN[3] = {0, 0, 0}, w = 0.0;
-    if (valid) {
-      const double* src = gradN + ((e * NQ + q) * NEN + a) * 3;
-      gN[0] = src[0];
-      gN[1] = src[1];
-      gN[2] = src[2];
-      w = J0w[e * NQ + q];
-    }
-    // ---- F (and Fdot) reduction over the element's nodes
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int J = 0; J < 3; ++J) {
-        s_part[wib][lane][3 * i + J] = xa[i] * gN[J];
-        if (KV) s_part[wib][lane][9 + 3 * i + J] = va[i] * gN[J];
-      }
-    __syncwarp();
-    {
-      // lanes 0..8 (ANCF also 16..24 for Fdot) of each group reduce one component
-      const int comp = ELEM == 0 ? a : (lane & 15);
-      const int which = ELEM == 0 ? 0 : half;  // ANCF: half 1 reduces Fdot
-      if (lane_active && comp < 9 && (KV || which == 0)) {
-        if (ELEM == 0) {
-          double s = 0.0;
-#pragma unroll
-          for (int b = 0; b < NEN; ++b) s += s_part[wib][gbase + b][comp];
-          s_F[wib][g][comp] = s;
-          if (KV) {
-            double sd = 0.0;
-#pragma unroll
-            for (int b = 0; b < NEN; ++b) sd += s_part[wib][gbase + b][9 + comp];
-            s_F[wib][g][9 + comp] = sd;
-          }
-        } else {
-          double s = 0.0;
-#pragma unroll
-          for (int b = 0; b < NEN; ++b) s += s_part[wib][b][9 * which + comp];
-          s_F[wib][0][9 * which + comp] = s;
-        }
-      }
-    }
-    __syncwarp();
-    double F[9], Fd[9];
-#pragma unroll
-    for (int r = 0; r < 9; ++r) {
-      F[r] = s_F[wib][g][r];
-      if (KV) Fd[r] = s_F[wib][g][9 + r];
-    }
-    // ---- Stage 1: constitutive update (never leaves the SM)
-    double S[6], St[6];
-    MRState ms;
-    if (MODEL == 0) {
-      svk_S(F, mat.lam, mat.mu, S);
-    } else {
-      mr_state(F, ms);
-      if (valid && !(ms.J > 0.0) && a == 0 && half == 0) atomicMin(err, (unsigned long long)(e * 64 + q));
-      mr_S(ms, mat.C10, mat.C01, mat.kappa, S);
-    }
-#pragma unroll
-    for (int r = 0; r < 6; ++r) St[r] = S[r];
-    if (KV) {
-      double Sv[6];
-      kv_S(F, Fd, mat.eta, mat.lamd, Sv);
-#pragma unroll
-      for (int r = 0; r < 6; ++r) St[r] += Sv[r];
-    }
-    // ---- Stage 2 force: f_a += w F (S_tot grad N_a)
-    {
-      double t[3];
-#pragma unroll
-      for (int I = 0; I < 3; ++I) t[I] = sget(St, I, 0) * gN[0] + sget(St, I, 1) * gN[1] + sget(St, I, 2) * gN[2];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) fa[i] += w * (F[3 * i] * t[0] + F[3 * i + 1] * t[1] + F[3 * i + 2] * t[2]);
-    }
-    if (TAN) {
-      double te[3];  // elastic S grad N_a (geometric stiffness)
-#pragma unroll
-      for (int I = 0; I < 3; ++I) te[I] = sget(S, I, 0) * gN[0] + sget(S, I, 1) * gN[1] + sget(S, I, 2) * gN[2];
-      if (MODEL == 0) {
-        double ga[3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) ga[i] = F[3 * i] * gN[0] + F[3 * i + 1] * gN[1] + F[3 * i + 2] * gN[2];
-        double B[6];  // F F^T
-#pragma unroll
-        for (int vv = 0; vv < 6; ++vv) {
-          int i, k;
-          voigt_pair(vv, i, k);
-          B[vv] = F[3 * i] * F[3 * k] + F[3 * i + 1] * F[3 * k + 1] + F[3 * i + 2] * F[3 * k + 2];
-        }
-        s_node[wib][lane][0] = ga[0];
-        s_node[wib][lane][1] = ga[1];
-        s_node[wib][lane][2] = ga[2];
-        s_node[wib][lane][3] = gN[0];
-        s_node[wib][lane][4] = gN[1];
-        s_node[wib][lane][5] = gN[2];
-        __syncwarp();
-        const double lw = mat.lam * w, mw = mat.mu * w;
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          const int b = partner<ELEM>(a, half, j);
-          if (b < 0) continue;
-          const double* nb = s_node[wib][gbase + b];
-          const double gb0 = nb[0], gb1 = nb[1], gb2 = nb[2];
-          const double s = w * (te[0] * nb[3] + te[1] * nb[4] + te[2] * nb[5]);
-          const double d = mw * (gN[0] * nb[3] + gN[1] * nb[4] + gN[2] * nb[5]);
-          const double gb[3] = {gb0, gb1, gb2};
-#pragma unroll
-          for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-              K[j][3 * i + k] += lw * ga[i] * gb[k] + mw * gb[i] * ga[k] + d * B[vidx(i, k)] + (i == k ? s : 0.0);
-        }
-      } else {
-        // MR: material tangent columns (6 lanes per element), B_a, C B_a
-        if (lane_active) {
-          const int col = ELEM == 0 ? a : lane;
-          if (col < 6 && (ELEM == 0 || half == 0)) {
-            double cc[6];
-            mr_Cv_column(ms, mat.C10, mat.C01, mat.kappa, col, cc);
-#pragma unroll
-            for (int vv = 0; vv < 6; ++vv) s_C[wib][g][6 * vv + col] = cc[vv];
-          }
-        }
-        double Ba[6][3];
-#pragma unroll
-        for (int vv = 0; vv < 6; ++vv) {
-          int I, J;
-          voigt_pair(vv, I, J);
-#pragma unroll
-          for (int i = 0; i < 3; ++i)
-            Ba[vv][i] = (I == J) ? F[3 * i + I] * gN[I] : F[3 * i + I] * gN[J] + F[3 * i + J] * gN[I];
-        }
-#pragma unroll
-        for (int vv = 0; vv < 6; ++vv)
-#pragma unroll
-          for (int i = 0; i < 3; ++i) s_node[wib][lane][3 * vv + i] = Ba[vv][i];
-        s_node[wib][lane][18] = gN[0];
-        s_node[wib][lane][19] = gN[1];
-        s_node[wib][lane][20] = gN[2];
-        __syncwarp();
-        double CB[6][3];
-#pragma unroll
-        for (int vv = 0; vv < 6; ++vv)
-#pragma unroll
-          for (int i = 0; i < 3; ++i) {
-            double s = 0.0;
-#pragma unroll
-            for (int ww = 0; ww < 6; ++ww) s += s_C[wib][g][6 * vv + ww] * Ba[ww][i];
-            CB[vv][i] = w * s;
-          }
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          const int b = partner<ELEM>(a, half, j);
-          if (b < 0) continue;
-          const double* nb = s_node[wib][gbase + b];
-          const double s = w * (te[0] * nb[18] + te[1] * nb[19] + te[2] * nb[20]);
-#pragma unroll
-          for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              double acc = (i == k ? s : 0.0);
-#pragma unroll
-              for (int vv = 0; vv < 6; ++vv) acc += CB[vv][i] * nb[3 * vv + k];
-              K[j][3 * i + k] += acc;
-            }
-        }
-      }
-    }
-    __syncwarp();
-  }
-
-  if (!valid) return;
-  if (ELEM == 0 || half == 0) {
-    double* fo = fscr + (e * NEN + a) * 3;
-    fo[0] = fa[0];
-    fo[1] = fa[1];
-    fo[2] = fa[2];
-  }
-  if (TAN) {
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      const int b = partner<ELEM>(a, half, j);
-      if (b < 0) continue;
-      if (a <= b) {
-        double* o = Kscr + (e * NUB + ublk(NEN, a, b)) * 9;
-#pragma unroll
-        for (int r = 0; r < 9; ++r) o[r] = K[j][r];
-      } else {  // store K_ba = K_ab^T
-        double* o = Kscr + (e * NUB + ublk(NEN, b, a)) * 9;
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-          for (int k = 0; k < 3; ++k) o[3 * k + i] = K[j][3 * i + k];
-      }
-    }
-  }
-}
-
-// ------------------------------------------------------------------ gathers
-
-__device__ __forceinline__ void sum_block(const uint32_t* __restrict__ ent, int32_t t0, int32_t t1, int nen,
-                                          int nub, const double* __restrict__ Kscr, double acc[9]) {
-#pragma unroll
-  for (int r = 0; r < 9; ++r) acc[r] = 0.0;
-  for (int32_t t = t0; t < t1; ++t) {
-    const uint32_t en = ent[t];
-    const int64_t e = en >> 8;
-    const int a = (en >> 4) & 15, b = en & 15;
-    if (a <= b) {
-      const double* s = Kscr + (e * nub + ublk(nen, a, b)) * 9;
-#pragma unroll
-      for (int r = 0; r < 9; ++r) acc[r] += s[r];
-    } else {
-      const double* s = Kscr + (e * nub + ublk(nen, b, a)) * 9;
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) acc[3 * i + k] += s[3 * k + i];
-    }
-  }
-}
-
-// H = M/h (diagonal of each 3x3 block) + h K, one thread per
-// coefficient block, every H value written once.
-__global__ void k_gather_H(int64_t nnz_c, int nen, int nub, const int32_t* __restrict__ blk_row,
-                           const int32_t* __restrict__ rowptr_c, const int32_t* __restrict__ blk_ptr,
-                           const uint32_t* __restrict__ blk_ent, const double* __restrict__ Kscr,
-                           const double* __restrict__ M, double h, double* __restrict__ H) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= nnz_c) return;
-  const int32_t i = blk_row[p], b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0, k = (int32_t)p - b0;
-  double acc[9];
-  sum_block(blk_ent, blk_ptr[p], blk_ptr[p + 1], nen, nub, Kscr, acc);
-  const double mh = M[p] / h;
-  double* out = H + 9 * (int64_t)b0 + 3 * k;
-#pragma unroll
-  for (int d = 0; d < 3; ++d)
-#pragma unroll
-    for (int f = 0; f < 3; ++f) out[3 * d * deg + f] = h * acc[3 * d + f] + (d == f ? mh : 0.0);
-}
-
 // f_int and the residual g = (1/h) M (v - v_n) + f_int - f_ext - f_ff
 // (Eq. residual / grad_L), one thread per owned node.
 __global__ void k_gather_f(int64_t n_own, int nen, const int32_t* __restrict__ node_ptr,
@@ -352,7 +33,7 @@ __global__ void k_gather_f(int64_t n_own, int nen, const int32_t* __restrict__ n
                            const int32_t* __restrict__ rowptr_c, const int32_t* __restrict__ cols_c,
                            const double* __restrict__ M, const double* __restrict__ fff,
                            const double* __restrict__ v, const double* __restrict__ vn,
-                           const double* __restrict__ fext, double h, int mode,
+                           const double* __restrict__ fext, double h, int mode, int sorted,
                            double* __restrict__ g, double* __restrict__ fint) {
   // mode 0: full (f from scratch + residual); 1: f only -> fint; 2: residual from fpart_in
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -364,8 +45,13 @@ __global__ void k_gather_f(int64_t n_own, int nen, const int32_t* __restrict__ n
     f2 = fpart_in[3 * i + 2];
   } else {
     for (int32_t t = node_ptr[i]; t < node_ptr[i + 1]; ++t) {
-      const uint32_t en = node_ent[t];
-      const double* s = fscr + ((int64_t)(en >> 4) * nen + (en & 15)) * 3;
+      const double* s;
+      if (sorted) {
+        s = fscr + (int64_t)t * 3;  // node-sorted force scratch
+      } else {
+        const uint32_t en = node_ent[t];
+        s = fscr + ((int64_t)(en >> 4) * nen + (en & 15)) * 3;
+      }
       f0 += s[0];
       f1 += s[1];
       f2 += s[2];
@@ -443,7 +129,7 @@ __global__ void k_stress(int64_t n_el, int nq, int nen, const int32_t* __restric
 
 __global__ void k_force_from_stress(int64_t n_el, int nq, int nen, const double* __restrict__ gradN,
                                     const double* __restrict__ J0w, const double* __restrict__ P,
-                                    double* __restrict__ fscr) {
+                                    const int32_t* __restrict__ fdest, double* __restrict__ fscr) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n_el * nen) return;
   const int64_t e = t / nen;
@@ -455,7 +141,8 @@ __global__ void k_force_from_stress(int64_t n_el, int nq, int nen, const double*
     const double w = J0w[e * nq + q];
     for (int i = 0; i < 3; ++i) f[i] += w * (Pq[3 * i] * gN[0] + Pq[3 * i + 1] * gN[1] + Pq[3 * i + 2] * gN[2]);
   }
-  for (int i = 0; i < 3; ++i) fscr[t * 3 + i] = f[i];
+  const int64_t pos = fdest ? (int64_t)fdest[t] : t;
+  for (int i = 0; i < 3; ++i) fscr[pos * 3 + i] = f[i];
 }
 
 // ------------------------------------------------------ constitutive hook
@@ -502,54 +189,68 @@ __global__ void k_constitutive(int64_t n, MatDev m, const double* __restrict__ F
 
 // ------------------------------------------------------------- launchers
 
-template <int ELEM, int NQ, int MODEL, bool KV, bool TAN>
-static tlfea_status launch_el(Context* c, const double* x, const double* v, cudaStream_t s) {
-  using G = Geo<ELEM>;
-  const int64_t per_cta = (int64_t)kWarps * G::EPW;
-  const unsigned grid = (unsigned)((c->n_el + per_cta - 1) / per_cta);
-  if (grid == 0) return TLFEA_OK;
-  k_element<ELEM, NQ, MODEL, KV, TAN><<<grid, kWarps * 32, 0, s>>>(c->n_el, c->conn, c->gradN, c->J0w, x, v,
-                                                                   c->mat, c->fscr, c->Kscr, c->err_flag);
-  TL_CHECK_LAUNCH();
-  return TLFEA_OK;
+// Measured on B200 (cfg3): warp-per-node 4.2 ms vs thread-per-node 1.3 ms, so
+// the thread version is the default.
+constexpr bool kUseWarpGatherF = false;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
-template <int ELEM, int NQ, int MODEL>
-static tlfea_status launch_el_kv(Context* c, const double* x, const double* v, bool tan, cudaStream_t s) {
-  const bool kv = c->mat.kv && v != nullptr;
-  if (tan) return kv ? launch_el<ELEM, NQ, MODEL, true, true>(c, x, v, s) : launch_el<ELEM, NQ, MODEL, false, true>(c, x, v, s);
-  return kv ? launch_el<ELEM, NQ, MODEL, true, false>(c, x, v, s) : launch_el<ELEM, NQ, MODEL, false, false>(c, x, v, s);
-}
-
-template <int ELEM, int NQ>
-static tlfea_status launch_el_model(Context* c, const double* x, const double* v, bool tan, cudaStream_t s) {
-  if (c->mat.model == TLFEA_SVK) return launch_el_kv<ELEM, NQ, 0>(c, x, v, tan, s);
-  return launch_el_kv<ELEM, NQ, 1>(c, x, v, tan, s);
-}
-
-tlfea_status launch_element_kernel(Context* c, const double* x, const double* v, bool tangent,
-                                   cudaStream_t s) {
-  if (c->element == TLFEA_T10) {
-    if (c->nq == 4) return launch_el_model<0, 4>(c, x, v, tangent, s);
-    return launch_el_model<0, 5>(c, x, v, tangent, s);
+// Warp per owned node (node-sorted force scratch): the lanes stream the node's
+// contiguous force contributions and its mass-CSR row (coalesced), then reduce
+// with a fixed butterfly (deterministic). mode as in k_gather_f.
+__global__ void k_gather_f_warp(int64_t n_own, const int32_t* __restrict__ node_ptr,
+                                const double* __restrict__ fscr, const double* __restrict__ fpart_in,
+                                const int32_t* __restrict__ own_nodes, const int32_t* __restrict__ rowptr_c,
+                                const int32_t* __restrict__ cols_c, const double* __restrict__ M,
+                                const double* __restrict__ fff, const double* __restrict__ v,
+                                const double* __restrict__ vn, const double* __restrict__ fext, double h, int mode,
+                                double* __restrict__ g, double* __restrict__ fint) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (i >= n_own) return;
+  double f[3] = {0, 0, 0};
+  if (mode == 2) {
+    if (lane < 3) f[lane] = fpart_in[3 * i + lane];
+  } else {
+    const int64_t t0 = 3 * (int64_t)node_ptr[i], t1 = 3 * (int64_t)node_ptr[i + 1];
+    for (int64_t t = t0 + lane; t < t1; t += 32) f[(t - t0) % 3] += fscr[t];
   }
-  return launch_el_model<1, 48>(c, x, v, tangent, s);
-}
-
-tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
-  if (c->nnz_c == 0) return TLFEA_OK;
-  k_gather_H<<<grid_for(c->nnz_c, 256), 256, 0, s>>>(c->nnz_c, c->nen, n_ublk_of(c->nen), c->blk_row, c->rowptr_c,
-                                                     c->blk_ptr, c->blk_ent, c->Kscr, c->M, h, H);
-  TL_CHECK_LAUNCH();
-  return TLFEA_OK;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) f[d] = warp_sum(f[d]);
+  if (fint && lane < 3) fint[3 * i + lane] = f[lane];
+  if (mode == 1 || !g) return;
+  double m[3] = {0, 0, 0};
+  for (int32_t p = rowptr_c[i] + lane; p < rowptr_c[i + 1]; p += 32) {
+    const int64_t J = cols_c[p];
+    const double mm = M[p];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) m[d] += mm * (v[3 * J + d] - (vn ? vn[3 * J + d] : 0.0));
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) m[d] = warp_sum(m[d]);
+  if (lane < 3) {
+    const int64_t I = own_nodes[i];
+    g[3 * i + lane] = m[lane] / h + f[lane] - (fext ? fext[3 * I + lane] : 0.0) - fff[3 * i + lane];
+  }
 }
 
 tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, const double* fext, double h,
                              double* g, double* fint, bool partial_only, cudaStream_t s) {
   if (c->n_own == 0) return TLFEA_OK;
+  if (c->fdest && kUseWarpGatherF) {
+    k_gather_f_warp<<<grid_for(32 * c->n_own, 256), 256, 0, s>>>(
+        c->n_own, c->node_ptr, c->fscr, nullptr, c->own_nodes, c->rowptr_c, c->cols_c, c->M, c->fff, v, vn, fext, h,
+        partial_only ? 1 : 0, g, fint);
+    TL_CHECK_LAUNCH();
+    return TLFEA_OK;
+  }
   k_gather_f<<<grid_for(c->n_own, 256), 256, 0, s>>>(c->n_own, c->nen, c->node_ptr, c->node_ent, c->fscr, nullptr,
                                                      c->own_nodes, c->rowptr_c, c->cols_c, c->M, c->fff, v, vn,
-                                                     fext, h, partial_only ? 1 : 0, g, fint);
+                                                     fext, h, partial_only ? 1 : 0, c->fdest != nullptr, g, fint);
   TL_CHECK_LAUNCH();
   return TLFEA_OK;
 }
@@ -557,9 +258,16 @@ tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, cons
 tlfea_status launch_residual(Context* c, const double* fint, const double* v, const double* vn,
                              const double* fext, double h, double* g, cudaStream_t s) {
   if (c->n_own == 0) return TLFEA_OK;
+  if (g && kUseWarpGatherF) {
+    k_gather_f_warp<<<grid_for(32 * c->n_own, 256), 256, 0, s>>>(
+        c->n_own, c->node_ptr, c->fscr, fint, c->own_nodes, c->rowptr_c, c->cols_c, c->M, c->fff, v, vn, fext, h, 2,
+        g, nullptr);
+    TL_CHECK_LAUNCH();
+    return TLFEA_OK;
+  }
   k_gather_f<<<grid_for(c->n_own, 256), 256, 0, s>>>(c->n_own, c->nen, c->node_ptr, c->node_ent, c->fscr, fint,
                                                      c->own_nodes, c->rowptr_c, c->cols_c, c->M, c->fff, v, vn,
-                                                     fext, h, 2, g, nullptr);
+                                                     fext, h, 2, c->fdest != nullptr, g, nullptr);
   TL_CHECK_LAUNCH();
   return TLFEA_OK;
 }
@@ -580,7 +288,7 @@ tlfea_status launch_stress_only(Context* c, const double* x, const double* v, do
 tlfea_status launch_force_from_stress(Context* c, const double* P, cudaStream_t s) {
   const int64_t n = c->n_el * c->nen;
   if (n == 0) return TLFEA_OK;
-  k_force_from_stress<<<grid_for(n, 128), 128, 0, s>>>(c->n_el, c->nq, c->nen, c->gradN, c->J0w, P, c->fscr);
+  k_force_from_stress<<<grid_for(n, 128), 128, 0, s>>>(c->n_el, c->nq, c->nen, c->gradN, c->J0w, P, c->fdest, c->fscr);
   TL_CHECK_LAUNCH();
   return TLFEA_OK;
 }

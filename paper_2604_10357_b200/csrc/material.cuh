@@ -19,9 +19,9 @@ __host__ __device__ __forceinline__ int vidx(int i, int j) {
   return i == j ? i : (3 - i - j) + 3;  // (1,2)->3, (0,2)->4, (0,1)->5
 }
 __host__ __device__ __forceinline__ void voigt_pair(int v, int& i, int& j) {
-  const int I[6] = {0, 1, 2, 1, 0, 0}, J[6] = {0, 1, 2, 2, 2, 1};
-  i = I[v];
-  j = J[v];
+  // (0,0) (1,1) (2,2) (1,2) (0,2) (0,1) — arithmetic, so a runtime v stays in registers
+  i = v < 3 ? v : (v == 3 ? 1 : 0);
+  j = v < 3 ? v : (v == 5 ? 1 : 2);
 }
 
 // C = F^T F (Voigt)
@@ -134,6 +134,24 @@ __host__ __device__ __forceinline__ void mr_Cv_column(const MRState& s, double C
     const double dC = (v == w) ? (K == L ? 2.0 : 1.0) : 0.0;
     col[v] = da * id + db * (s.I1 * id - s.C[v]) + b * (dI1 * id - dC) + dcinv * s.Ci[v] +
              cinv * dCi;
+  }
+}
+
+// Column selection with a compile-time column so MRState stays in registers.
+template <int W>
+__host__ __device__ __forceinline__ void mr_Cv_col_t(const MRState& s, double C10, double C01, double kappa,
+                                                     double col[6]) {
+  mr_Cv_column(s, C10, C01, kappa, W, col);
+}
+__host__ __device__ __forceinline__ void mr_Cv_column_dispatch(const MRState& s, double C10, double C01,
+                                                               double kappa, int w, double col[6]) {
+  switch (w) {
+    case 0: mr_Cv_col_t<0>(s, C10, C01, kappa, col); break;
+    case 1: mr_Cv_col_t<1>(s, C10, C01, kappa, col); break;
+    case 2: mr_Cv_col_t<2>(s, C10, C01, kappa, col); break;
+    case 3: mr_Cv_col_t<3>(s, C10, C01, kappa, col); break;
+    case 4: mr_Cv_col_t<4>(s, C10, C01, kappa, col); break;
+    default: mr_Cv_col_t<5>(s, C10, C01, kappa, col); break;
   }
 }
 

@@ -120,10 +120,17 @@ __global__ void k_precompute(int element, int64_t n_el, int nq, int nen, const i
   } else {
     ancf_shape(xi, dims + 3 * e, nullptr, dN);
   }
+  // J = sum_a (X_a - X_o) (x) dN_a/dxi over position coefficients (sum_a dN_a = 0
+  // for them), so the element's absolute placement does not enter the rounding:
+  // congruent elements get (nearly) bit-identical tables.
+  const int64_t Io = conn[e * nen];
+  const double o0 = X[3 * Io], o1 = X[3 * Io + 1], o2 = X[3 * Io + 2];
   double J[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int a = 0; a < nen; ++a) {
     const int64_t I = conn[e * nen + a];
-    const double x0 = X[3 * I], x1 = X[3 * I + 1], x2 = X[3 * I + 2];
+    const bool pos = element == TLFEA_T10 || (a & 3) == 0;
+    const double x0 = X[3 * I] - (pos ? o0 : 0.0), x1 = X[3 * I + 1] - (pos ? o1 : 0.0),
+                 x2 = X[3 * I + 2] - (pos ? o2 : 0.0);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       J[k] += x0 * dN[a][k];
@@ -334,6 +341,141 @@ __global__ void k_force_field(int64_t n_own, const int32_t* __restrict__ rowptr_
   fff[3 * i + 2] = g2 * s;
 }
 
+// Geometry classes: hash of an element's reference table (gradN, J0w)
+// quantised at ~2^-36 of its largest entry. Congruent (translated) elements
+// hash equal; every member is validated against its class representative.
+__global__ void k_geom_hash(int64_t n_el, int len_g, int len_w, const double* __restrict__ gradN,
+                            const double* __restrict__ J0w, unsigned long long* __restrict__ key,
+                            int64_t* __restrict__ idx) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n_el) return;
+  const double* g = gradN + e * len_g;
+  const double* w = J0w + e * len_w;
+  double sg = 0.0, sw = 0.0;
+  for (int i = 0; i < len_g; ++i) sg = fmax(sg, fabs(g[i]));
+  for (int i = 0; i < len_w; ++i) sw = fmax(sw, fabs(w[i]));
+  unsigned long long h = 1469598103934665603ull;
+  auto mix = [&](double v, double s) {
+    // coarse (2^-20 relative) so rounding-level differences between congruent
+    // elements almost never straddle a bucket; exactness is checked afterwards
+    const long long qv = s > 0.0 ? llrint(v / s * 1048576.0) : 0;
+    h = (h ^ (unsigned long long)qv) * 1099511628211ull;
+  };
+  for (int i = 0; i < len_g; ++i) mix(g[i], sg);
+  for (int i = 0; i < len_w; ++i) mix(w[i], sw);
+  key[e] = h >> 1;  // keep clear of the all-ones sentinel
+  idx[e] = e;
+}
+
+// cls_of_sorted: class id per sorted position (run index); rep = first e of the run.
+__global__ void k_geom_assign(int64_t n, const unsigned long long* __restrict__ skey,
+                              const int64_t* __restrict__ sidx, const int32_t* __restrict__ run_id,
+                              uint8_t* __restrict__ cls) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  cls[sidx[t]] = (uint8_t)run_id[t];
+}
+
+__global__ void k_run_flags(int64_t n, const unsigned long long* __restrict__ skey, int32_t* __restrict__ flag) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  flag[t] = (t == 0 || skey[t] != skey[t - 1]) ? 1 : 0;
+}
+
+__global__ void k_geom_validate(int64_t n_el, int len, const double* __restrict__ gradN,
+                                const double* __restrict__ J0w, int nq, const uint8_t* __restrict__ cls,
+                                const double* __restrict__ tab, unsigned int* __restrict__ bad) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n_el) return;
+  const int lg = len - nq;
+  const double* t = tab + (int64_t)cls[e] * len;  // len = nq * (per + 1) per class
+  // table layout per class: [q][lg/nq gradN entries ..., J0w]
+  const int per = lg / nq;
+  double sg = 0.0, dg = 0.0, sw = 0.0, dw = 0.0;
+  for (int q = 0; q < nq; ++q) {
+    for (int i = 0; i < per; ++i) {
+      const double a = gradN[(e * nq + q) * per + i], b = t[q * (per + 1) + i];
+      sg = fmax(sg, fabs(b));
+      dg = fmax(dg, fabs(a - b));
+    }
+    const double a = J0w[e * nq + q], b = t[q * (per + 1) + per];
+    sw = fmax(sw, fabs(b));
+    dw = fmax(dw, fabs(a - b));
+  }
+  if (dg > 1e-12 * sg || dw > 1e-12 * sw) atomicOr(bad, 1u);
+}
+
+__global__ void k_geom_gather_rep(int n_cls, int nq, int per, const int64_t* __restrict__ rep,
+                                  const double* __restrict__ gradN, const double* __restrict__ J0w,
+                                  double* __restrict__ tab) {
+  const int c = blockIdx.x;
+  if (c >= n_cls) return;
+  const int64_t e = rep[c];
+  for (int t = threadIdx.x; t < nq * (per + 1); t += blockDim.x) {
+    const int q = t / (per + 1), i = t % (per + 1);
+    tab[(int64_t)c * nq * (per + 1) + t] = i < per ? gradN[(e * nq + q) * per + i] : J0w[e * nq + q];
+  }
+}
+
+// Symmetric gather units: block p=(I,J) is a unit when I <= J (global ids) or
+// when the transpose row J is not owned; pT = position of (J,I) in row J.
+__global__ void k_units(int64_t nnz_c, const int32_t* __restrict__ blk_row, const int32_t* __restrict__ cols_c,
+                        const int32_t* __restrict__ own_nodes, const int32_t* __restrict__ own_idx,
+                        const int32_t* __restrict__ rowptr_c, int32_t* __restrict__ is_unit,
+                        int32_t* __restrict__ pT) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nnz_c) return;
+  const int32_t I = own_nodes[blk_row[p]], J = cols_c[p];
+  const int32_t rJ = own_idx[J];
+  int32_t t = -1;
+  if (rJ >= 0 && J != I) {
+    int32_t lo = rowptr_c[rJ], hi = rowptr_c[rJ + 1];
+    while (lo < hi) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (cols_c[mid] < I)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    t = lo;
+  }
+  is_unit[p] = (J >= I || rJ < 0) ? 1 : 0;
+  pT[p] = (J > I) ? t : -1;
+}
+
+__device__ __forceinline__ int ublk_s(int n, int a, int b) { return a * n - (a * (a - 1)) / 2 + (b - a); }
+
+__global__ void k_unit_len(int64_t n_units, const int32_t* __restrict__ unit_p, const int32_t* __restrict__ blk_ptr,
+                           int32_t* __restrict__ len) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n_units) return;
+  const int32_t p = unit_p[u];
+  len[u] = blk_ptr[p + 1] - blk_ptr[p];
+}
+
+// dest[e][ub] = (position in the gather-sorted scratch << 1) | transpose
+__global__ void k_unit_dest(int64_t n_units, int nen, int nub, const int32_t* __restrict__ unit_p,
+                            const int32_t* __restrict__ unit_ptr, const int32_t* __restrict__ blk_ptr,
+                            const uint32_t* __restrict__ blk_ent, int32_t* __restrict__ dest) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n_units) return;
+  const int32_t p = unit_p[u], t0 = blk_ptr[p], t1 = blk_ptr[p + 1], base = unit_ptr[u];
+  for (int32_t t = t0; t < t1; ++t) {
+    const uint32_t en = blk_ent[t];
+    const int64_t e = en >> 8;
+    const int a = (en >> 4) & 15, b = en & 15;
+    const int ub = a <= b ? ublk_s(nen, a, b) : ublk_s(nen, b, a);
+    dest[e * nub + ub] = ((base + (t - t0)) << 1) | (a > b ? 1 : 0);
+  }
+}
+
+__global__ void k_force_dest(int64_t n, int nen, const uint32_t* __restrict__ node_ent, int32_t* __restrict__ fdest) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const uint32_t en = node_ent[t];
+  fdest[(int64_t)(en >> 4) * nen + (en & 15)] = (int32_t)t;
+}
+
 // ------------------------------------------------------------- host helpers
 
 // Sort (key,value) pairs stably by key, then build a CSR pointer over
@@ -366,6 +508,148 @@ static tlfea_status sort_and_ptr(int64_t n, int32_t* key, V* val, int64_t n_seg,
   TL_CUDA(cudaMemcpy(&nv, ptr_out + n_seg, sizeof(int32_t), cudaMemcpyDeviceToHost));
   *n_valid = nv;
   *sorted_val_out = val_sorted.p;
+  return TLFEA_OK;
+}
+
+static tlfea_status build_geometry_classes(Context* c) {
+  const int64_t n = c->n_el;
+  const int nq = c->nq, per = c->nen * 3;
+  const int max_cls = c->element == TLFEA_T10 ? 32 : 4;
+  c->n_cls = 0;
+  if (n == 0) return TLFEA_OK;
+  TmpArr<unsigned long long> key, key2;
+  TmpArr<int64_t> idx, idx2;
+  TmpArr<int32_t> flag, run;
+  TL_TRY(key.get(n));
+  TL_TRY(key2.get(n));
+  TL_TRY(idx.get(n));
+  TL_TRY(idx2.get(n));
+  TL_TRY(flag.get(n));
+  TL_TRY(run.get(n));
+  k_geom_hash<<<grid_for(n, 128), 128>>>(n, nq * per, nq, c->gradN, c->J0w, key.p, idx.p);
+  TL_CHECK_LAUNCH();
+  Tmp tmp;
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, idx.p, idx2.p, (int64_t)n);
+  TL_TRY(tmp.get(bytes));
+  TL_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, idx.p, idx2.p, (int64_t)n));
+  count_launch();
+  k_run_flags<<<grid_for(n, 256), 256>>>(n, key2.p, flag.p);
+  TL_CHECK_LAUNCH();
+  bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, bytes, flag.p, run.p, (int64_t)n);
+  TL_TRY(tmp.get(bytes));
+  TL_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, bytes, flag.p, run.p, (int64_t)n));
+  count_launch();
+  int32_t nruns = 0;
+  TL_CUDA(cudaMemcpy(&nruns, run.p + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (nruns > max_cls) return TLFEA_OK;  // unstructured: keep per-element tables
+  // representatives: the smallest element id of each run (stable sort)
+  std::vector<int32_t> hflag(n);
+  std::vector<int64_t> hidx(n);
+  TL_CUDA(cudaMemcpy(hflag.data(), flag.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  TL_CUDA(cudaMemcpy(hidx.data(), idx2.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> rep;
+  for (int64_t t = 0; t < n; ++t)
+    if (hflag[t]) rep.push_back(hidx[t]);
+  // run ids are 1-based from the inclusive scan: shift to 0-based via a decrement kernel-free trick
+  std::vector<int32_t> hrun(n);
+  TL_CUDA(cudaMemcpy(hrun.data(), run.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  for (auto& r : hrun) r -= 1;
+  TL_CUDA(cudaMemcpy(run.p, hrun.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  TL_TRY(c->alloc(&c->cls, (size_t)n));
+  k_geom_assign<<<grid_for(n, 256), 256>>>(n, key2.p, idx2.p, run.p, c->cls);
+  TL_CHECK_LAUNCH();
+  TmpArr<int64_t> drep;
+  TL_TRY(drep.get(rep.size()));
+  TL_CUDA(cudaMemcpy(drep.p, rep.data(), sizeof(int64_t) * rep.size(), cudaMemcpyHostToDevice));
+  TL_TRY(c->alloc(&c->cls_tab, (size_t)nruns * nq * (per + 1)));
+  k_geom_gather_rep<<<nruns, 128>>>(nruns, nq, per, drep.p, c->gradN, c->J0w, c->cls_tab);
+  TL_CHECK_LAUNCH();
+  unsigned int* dbad = nullptr;
+  TL_TRY(c->alloc(&dbad, 1));
+  TL_CUDA(cudaMemset(dbad, 0, sizeof(unsigned int)));
+  k_geom_validate<<<grid_for(n, 128), 128>>>(n, nq * (per + 1), c->gradN, c->J0w, nq, c->cls, c->cls_tab, dbad);
+  TL_CHECK_LAUNCH();
+  unsigned int hb = 0;
+  TL_CUDA(cudaMemcpy(&hb, dbad, sizeof(hb), cudaMemcpyDeviceToHost));
+  if (hb == 0) c->n_cls = nruns;
+  return TLFEA_OK;
+}
+
+static tlfea_status build_units(Context* c) {
+  c->n_units = 0;
+  if (c->nnz_c == 0) return TLFEA_OK;
+  const int64_t n = c->nnz_c;
+  TmpArr<int32_t> isu, pT;
+  TL_TRY(isu.get(n));
+  TL_TRY(pT.get(n));
+  k_units<<<grid_for(n, 256), 256>>>(n, c->blk_row, c->cols_c, c->own_nodes, c->own_idx, c->rowptr_c, isu.p, pT.p);
+  TL_CHECK_LAUNCH();
+  TmpArr<int64_t> nsel;
+  TL_TRY(nsel.get(1));
+  TmpArr<int32_t> up, upT;
+  TL_TRY(up.get(n));
+  TL_TRY(upT.get(n));
+  Tmp tmp;
+  size_t bytes = 0;
+  cub::CountingInputIterator<int32_t> it(0);
+  cub::DeviceSelect::Flagged(nullptr, bytes, it, isu.p, up.p, nsel.p, (int64_t)n);
+  TL_TRY(tmp.get(bytes));
+  TL_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, isu.p, up.p, nsel.p, (int64_t)n));
+  count_launch();
+  bytes = 0;
+  cub::DeviceSelect::Flagged(nullptr, bytes, pT.p, isu.p, upT.p, nsel.p, (int64_t)n);
+  TL_TRY(tmp.get(bytes));
+  TL_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, pT.p, isu.p, upT.p, nsel.p, (int64_t)n));
+  count_launch();
+  int64_t nu = 0;
+  TL_CUDA(cudaMemcpy(&nu, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  c->n_units = nu;
+  TL_TRY(c->alloc(&c->unit_p, (size_t)nu));
+  TL_TRY(c->alloc(&c->unit_pT, (size_t)nu));
+  TL_CUDA(cudaMemcpy(c->unit_p, up.p, sizeof(int32_t) * nu, cudaMemcpyDeviceToDevice));
+  TL_CUDA(cudaMemcpy(c->unit_pT, upT.p, sizeof(int32_t) * nu, cudaMemcpyDeviceToDevice));
+  return TLFEA_OK;
+}
+
+// Gather-sorted scratch layout (single-rank contexts; the partitioned path
+// keeps element-major scratch for its pack lists).
+static tlfea_status build_sorted_scratch(Context* c) {
+  const int nen = c->nen, nub = n_ublk_of(nen);
+  TL_TRY(c->alloc(&c->unit_ptr, (size_t)c->n_units + 1));
+  TL_TRY(c->alloc(&c->dest, (size_t)std::max<int64_t>(c->n_el, 1) * nub));
+  TL_TRY(c->alloc(&c->fdest, (size_t)std::max<int64_t>(c->n_el, 1) * nen));
+  TL_CUDA(cudaMemset(c->dest, 0xff, sizeof(int32_t) * std::max<int64_t>(c->n_el, 1) * nub));
+  TmpArr<int32_t> len;
+  TL_TRY(len.get(c->n_units + 1));
+  TL_CUDA(cudaMemset(len.p, 0, sizeof(int32_t) * (c->n_units + 1)));
+  if (c->n_units > 0) {
+    k_unit_len<<<grid_for(c->n_units, 256), 256>>>(c->n_units, c->unit_p, c->blk_ptr, len.p);
+    TL_CHECK_LAUNCH();
+  }
+  Tmp tmp;
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, len.p, c->unit_ptr, (int64_t)(c->n_units + 1));
+  TL_TRY(tmp.get(bytes));
+  TL_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, len.p, c->unit_ptr, (int64_t)(c->n_units + 1)));
+  count_launch();
+  int32_t npos = 0;
+  TL_CUDA(cudaMemcpy(&npos, c->unit_ptr + c->n_units, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if ((int64_t)npos != c->n_el * nub)
+    return fail(TLFEA_E_CUDA, "internal: gather-sorted scratch covers " + std::to_string(npos) + " of " +
+                                  std::to_string(c->n_el * nub) + " element blocks");
+  if (c->n_units > 0) {
+    k_unit_dest<<<grid_for(c->n_units, 256), 256>>>(c->n_units, nen, nub, c->unit_p, c->unit_ptr, c->blk_ptr,
+                                                    c->blk_ent, c->dest);
+    TL_CHECK_LAUNCH();
+  }
+  int32_t nf = 0;
+  TL_CUDA(cudaMemcpy(&nf, c->node_ptr + c->n_own, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (nf > 0) {
+    k_force_dest<<<grid_for(nf, 256), 256>>>(nf, nen, c->node_ent, c->fdest);
+    TL_CHECK_LAUNCH();
+  }
   return TLFEA_OK;
 }
 
@@ -566,6 +850,7 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     TL_CUDA(cudaMemcpy(&na, dna, sizeof(na), cudaMemcpyDeviceToHost));
     c->affine = na ? 0 : 1;
   }
+  TL_TRY(build_geometry_classes(c));
 
   // ---- a-2 pattern over setup elements (64-bit keys, sort, unique)
   const int64_t nkeys = NS * nen * nen;
@@ -660,11 +945,14 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     TL_CUDA(cudaMemcpy(c->node_ent, sv, sizeof(uint32_t) * nvalid, cudaMemcpyDeviceToDevice));
   }
 
+  TL_TRY(build_units(c));
+  if (c->nranks == 1) TL_TRY(build_sorted_scratch(c));
+
   // ---- consistent mass over the setup elements (reading Q4) and f_ff
   TL_TRY(c->alloc(&c->M, (size_t)c->nnz_c));
   TL_TRY(c->alloc(&c->fff, (size_t)3 * c->n_own));
   {
-    double mq[64 * 3], mw[64];
+    double mq[kMassRuleT10 * 3], mw[kMassRuleT10];
     int nmq;
     if (c->element == TLFEA_T10 && c->mass_rule == 0) {
       nmq = make_mass_rule_t10(mq, mw);
@@ -672,8 +960,8 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
       nmq = make_rule(c->quadrature, mq, mw);
     }
     TmpArr<double> dmq, dmw, me;
-    TL_TRY(dmq.get(3 * 64));
-    TL_TRY(dmw.get(64));
+    TL_TRY(dmq.get(3 * kMassRuleT10));
+    TL_TRY(dmw.get(kMassRuleT10));
     TL_CUDA(cudaMemcpy(dmq.p, mq, sizeof(double) * 3 * nmq, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(dmw.p, mw, sizeof(double) * nmq, cudaMemcpyHostToDevice));
     const int64_t nm = NS * nen * nen;

@@ -58,18 +58,20 @@ inline int make_rule(int rule, double* xi /*[n][3]*/, double* w) {
   return n;
 }
 
-// Host: collapsed (Duffy) Gauss rule with 4 points per direction on the unit
-// tetrahedron: exact for polynomials of total degree <= 5 (used for the exact
-// T10 consistent mass, reading Q4). 64 points.
+// Host: collapsed (Duffy) Gauss rule with 5 points per direction on the unit
+// tetrahedron: exact for polynomials of total degree <= 7, i.e. for
+// N_a N_b det J of curved (isoparametric) T10 elements; used for the exact
+// consistent mass (reading Q4). 125 points.
+constexpr int kMassRuleT10 = 125;
 inline int make_mass_rule_t10(double* xi, double* w) {
-  const double t = 2.0 * std::sqrt(1.2) / 7.0;
-  const double x4o = std::sqrt(3.0 / 7.0 + t), x4i = std::sqrt(3.0 / 7.0 - t);
-  const double w4o = 0.5 - std::sqrt(30.0) / 36.0, w4i = 0.5 + std::sqrt(30.0) / 36.0;
-  const double g[4] = {-x4o, -x4i, x4i, x4o}, gw[4] = {w4o, w4i, w4i, w4o};
+  const double r = 2.0 * std::sqrt(10.0 / 7.0);
+  const double xo = std::sqrt(5.0 + r) / 3.0, xi_ = std::sqrt(5.0 - r) / 3.0;
+  const double wo = (322.0 - 13.0 * std::sqrt(70.0)) / 900.0, wi = (322.0 + 13.0 * std::sqrt(70.0)) / 900.0;
+  const double g[5] = {-xo, -xi_, 0.0, xi_, xo}, gw[5] = {wo, wi, 128.0 / 225.0, wi, wo};
   int n = 0;
-  for (int i = 0; i < 4; ++i)
-    for (int j = 0; j < 4; ++j)
-      for (int k = 0; k < 4; ++k, ++n) {
+  for (int i = 0; i < 5; ++i)
+    for (int j = 0; j < 5; ++j)
+      for (int k = 0; k < 5; ++k, ++n) {
         const double u = 0.5 * (g[i] + 1.0), s = 0.5 * (g[j] + 1.0), r = 0.5 * (g[k] + 1.0);
         xi[3 * n + 0] = u;
         xi[3 * n + 1] = s * (1.0 - u);

@@ -98,6 +98,14 @@ def kuhn_t10_box(nx: int, ny: int, nz: int, Lx: float, Ly: float, Lz: float,
     return Mesh(0, X, conn, name=f"kuhn{nx}x{ny}x{nz}")
 
 
+def perturbed(mesh: Mesh, amp: float = 0.05, seed: int = SEED_BASE + 7) -> Mesh:
+    """Unstructured variant: every node (mid-edge nodes included, so edges
+    become curved) moved by U(-amp, amp) x node spacing. No two elements stay
+    congruent, which exercises the per-(e,q) reference-table path."""
+    X = mesh.X + np.random.default_rng(seed).uniform(-amp, amp, mesh.X.shape) * _node_spacing(mesh.X)
+    return Mesh(mesh.element, X, mesh.conn.copy(), mesh.dims, name=mesh.name + "_perturbed")
+
+
 def _morton3(c: np.ndarray) -> np.ndarray:
     code = np.zeros(c.shape[0], dtype=np.int64)
     for bit in range(21):

@@ -60,6 +60,10 @@ CASES = {
                                             dict(synth.SVK_PAPER, **synth.KV_TIRE), 0),
     "t10_single_element": lambda: (synth.Mesh(0, synth.kuhn_t10_box(1, 1, 1, 1, 1, 1).X,
                                               synth.kuhn_t10_box(1, 1, 1, 1, 1, 1).conn[:1]), dict(synth.MR_PAPER), 1),
+    "t10_4x3x2_perturbed_svk_kv_keast5": lambda: (synth.perturbed(synth.kuhn_t10_box(4, 3, 2, 0.8, 0.6, 0.4)),
+                                                  dict(synth.SVK_PAPER, **synth.KV_TIRE), 1),
+    "t10_3x3x2_perturbed_mr_4pt": lambda: (synth.perturbed(synth.kuhn_t10_box(3, 3, 2, 0.6, 0.6, 0.4)),
+                                           dict(synth.MR_PAPER), 0),
     "ancf_3x3_svk": lambda: (synth.ancf_plate(3), dict(synth.SVK_PAPER), 2),
     "ancf_5x5_mr_kv": lambda: (synth.ancf_plate(5), dict(synth.MR_PAPER, **synth.KV_TIRE), 2),
 }
@@ -84,6 +88,14 @@ def test_eval_parity(torch_cuda, case):
     g0, H0, f0 = pr.eval(x, v, vn, fext, h)
     ctx, g, H, f = gpu_eval(torch_cuda, mesh, mat, rule, x, v, vn, fext, h, gravity=grav)
     check_pattern(ctx, pr)
+    # congruent (Kuhn / uniform plate) meshes use shared-memory geometry classes,
+    # perturbed meshes the per-(e,q) tables
+    if "perturbed" in case:
+        assert ctx.info["n_geometry_classes"] == 0
+    elif mesh.element == 0 and mesh.n_el >= 6:
+        assert ctx.info["n_geometry_classes"] == 6
+    else:
+        assert ctx.info["n_geometry_classes"] >= 1
     assert rel(f, f0) <= TOL, rel(f, f0)
     assert rel(g, g0) <= TOL, rel(g, g0)
     assert rel(H, H0) <= TOL, rel(H, H0)

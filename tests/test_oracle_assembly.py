@@ -96,6 +96,34 @@ def test_t10_exact_mass_closed_form_vs_brute_force():
     assert np.all(np.linalg.eigvalsh(me) > 0)
 
 
+def test_t10_exact_mass_curved_element():
+    """Curved (isoparametric) T10: N_a N_b det J has degree 7; the oracle's
+    exact mass must equal an independent 8x8x8 collapsed-Gauss integral
+    computed here, and its total must equal rho * volume (det J is cubic, so
+    the degree-3 Keast rule gives the volume exactly)."""
+    rng = np.random.default_rng(22)
+    X = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], float)
+    Xf = np.vstack([X] + [(X[a] + X[b]) / 2 for a, b in synth.T10_EDGES])
+    Xf[4:] += rng.uniform(-0.08, 0.08, (6, 3))                    # bend the edges
+    conn = np.arange(10, dtype=np.int32)
+    me = oracle.element_mass(0, 1, 0, 1000.0, conn, Xf)
+    g, w = np.polynomial.legendre.leggauss(8)
+    g, w = (g + 1) / 2, w / 2
+    ref = np.zeros((10, 10))
+    for i in range(8):
+        for j in range(8):
+            for k in range(8):
+                u, s, t = g[i], g[j], g[k]
+                xi = np.array([u, s * (1 - u), t * (1 - u) * (1 - s)])
+                N, dN = oracle.t10_shape(xi)
+                detJ = np.linalg.det(Xf.T @ dN)
+                ref += np.outer(N, N) * detJ * (1 - u) ** 2 * (1 - s) * w[i] * w[j] * w[k] * 1000.0
+    assert np.abs(me - ref).max() < 1e-13 * np.abs(ref).max()
+    mesh = synth.Mesh(0, Xf, conn[None, :])
+    pr = oracle.Problem(mesh, synth.SVK_PAPER, 1, with_pattern=False)
+    assert abs(me.sum() - 1000.0 * pr.J0w.sum()) < 1e-13 * 1000.0 * pr.J0w.sum()
+
+
 def test_t10_force_rule_mass_literal_reading():
     """mass_rule = 1 (P:309-310 literally): 4-point rule gives a rank-4 element
     mass; Keast-5 one negative eigenvalue (reading Q4)."""
