@@ -254,15 +254,8 @@ def run_ours(args):
         roff = np.concatenate([[0], np.cumsum(rcount)])
 
     def exchange():
-        ops = []
-        for p in range(world):
-            if scount[p] > 0:
-                ops.append(dist.P2POp(dist.isend, sbuf[soff[p]:soff[p + 1]], p))
-            if rcount[p] > 0:
-                ops.append(dist.P2POp(dist.irecv, rbuf[roff[p]:roff[p + 1]], p))
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
+        from paper_2604_10357_b200 import dist as tdist
+        tdist.exchange(sbuf, rbuf, scount, rcount)
 
     def step():
         if world == 1:

@@ -1,0 +1,37 @@
+"""Multi-GPU transport of the partitioned evaluation.
+
+libtlfea packs, per peer, the partial 3x3 H blocks and partial nodal forces of
+rows it touches but does not own (tlfea_eval_begin) and adds the received
+partials in ascending peer order (tlfea_eval_finish). This module only moves
+the packed buffers between ranks with torch.distributed point-to-point
+operations (NCCL over NVLink on a GPU box; gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def offsets(counts) -> np.ndarray:
+    return np.concatenate([[0], np.cumsum(np.asarray(counts, np.int64))])
+
+
+def exchange(send_buf, recv_buf, send_counts, recv_counts, group=None):
+    """Send send_buf[soff[p]:soff[p+1]] to every peer p and receive
+    recv_buf[roff[p]:roff[p+1]] from it (one batched group of P2P ops)."""
+    import torch.distributed as dist
+    soff, roff = offsets(send_counts), offsets(recv_counts)
+    ops = []
+    for p in range(len(send_counts)):
+        if send_counts[p] > 0:
+            ops.append(dist.P2POp(dist.isend, send_buf[int(soff[p]):int(soff[p + 1])], p, group))
+        if recv_counts[p] > 0:
+            ops.append(dist.P2POp(dist.irecv, recv_buf[int(roff[p]):int(roff[p + 1])], p, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+def contiguous_partition(n_el: int, nranks: int) -> np.ndarray:
+    """Default element partition: contiguous equal blocks of the element order
+    (x-slabs for the lexicographic Kuhn meshes)."""
+    return ((np.arange(n_el, dtype=np.int64) * nranks) // n_el).astype(np.int32)

@@ -1,0 +1,147 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (tlfea_eval / tlfea_force_only on the whole mesh):
+
+* config 2 (98,784 T10, Mooney-Rivlin + Kelvin-Voigt): every output compared
+  with the full CPU oracle (pattern bit-exact, g / H / f <= 1e-11).
+* config 3 (3,981,312 T10), config 4 (ANCF 200x200), config 5 (2,000 bodies):
+  seeded samples of rows (interior, boundary, corner nodes) computed one by
+  one by the oracle (`oracle.eval_rows`); CSR columns bit-exact, values
+  <= 1e-11 normwise over the sample.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-11
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def T():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_10357_b200 as T
+    T.lib()
+    return T
+
+
+def d(a):
+    import torch
+    return None if a is None else torch.from_numpy(np.ascontiguousarray(a, np.float64)).cuda()
+
+
+def test_config2_full_oracle(T):
+    cfg = synth.config(2)
+    mesh = cfg.mesh
+    x, v, vn, fext = synth.t10_state(mesh, with_fext=True)
+    ctx = T.Context.from_mesh(mesh, cfg.material, cfg.quadrature)
+    g, H, f = ctx.empty_outputs()
+    ctx.eval(d(x), d(v), d(vn), d(fext), cfg.h, g, H, f)
+    rowptr, cols = [t.cpu().numpy().astype(np.int64) for t in ctx.export_pattern()[:2]]
+    g, H, f = g.cpu().numpy(), H.cpu().numpy(), f.cpu().numpy()
+    del ctx
+    pr = oracle.Problem(mesh, cfg.material, cfg.quadrature, with_precompute=False)
+    assert np.array_equal(rowptr, pr.rowptr) and np.array_equal(cols, pr.cols)
+    g0, H0, f0 = pr.eval(x, v, vn, fext, cfg.h)
+    assert rel(f, f0) <= TOL and rel(g, g0) <= TOL and rel(H, H0) <= TOL, (rel(f, f0), rel(g, g0), rel(H, H0))
+
+
+def sample_nodes(mesh, n, seed):
+    """Seeded sample: random nodes plus the extreme ones (first, last, and the
+    node farthest from the centroid) so corners and faces are covered."""
+    rng = np.random.default_rng(seed)
+    if mesh.element == 0:
+        pos = mesh.X
+        ids = np.arange(mesh.n_coef)
+    else:
+        pos = mesh.X.reshape(-1, 4, 3)[:, 0]
+        ids = np.arange(mesh.n_coef // 4)
+    far = int(np.argmax(np.linalg.norm(pos - pos.mean(0), axis=1)))
+    pick = np.unique(np.concatenate([[0, ids[-1], far], rng.choice(ids, n, replace=False)]))
+    if mesh.element == 0:
+        return pick
+    return np.unique((4 * pick[:, None] + np.arange(4)[None, :]).ravel())   # all 4 coefficients
+
+
+def gpu_rows(T, ctx, H, nodes):
+    """Columns and H values of the sampled coefficient rows (GPU side)."""
+    import torch
+    rowptr, cols = ctx.export_pattern()[:2]
+    nodes_t = torch.as_tensor(nodes, device=rowptr.device, dtype=torch.int64)
+    out_cols, out_vals = [], []
+    rp = rowptr.cpu().numpy()
+    for I in nodes:
+        r0, r1 = rp[3 * I], rp[3 * I + 3]
+        out_cols.append(cols[r0:r1].cpu().numpy())
+        out_vals.append(H[r0:r1].cpu().numpy())
+    del nodes_t
+    return rp, out_cols, out_vals
+
+
+@pytest.mark.parametrize("cfg_idx,n_sample", [(3, 48), (4, 24)])
+def test_full_size_sampled_rows(T, cfg_idx, n_sample):
+    cfg = synth.config(cfg_idx)
+    mesh = cfg.mesh
+    if mesh.element == 0:
+        x, v, vn, fext = synth.t10_state(mesh, with_fext=True)
+    else:
+        x, v, vn = synth.ancf_state(mesh)
+        fext = None
+    ctx = T.Context.from_mesh(mesh, cfg.material, cfg.quadrature)
+    g, H, f = ctx.empty_outputs()
+    ctx.eval(d(x), d(v), d(vn), d(fext), cfg.h, g, H, f)
+    nodes = sample_nodes(mesh, n_sample, synth.SEED_BASE + 100 + cfg_idx)
+    rp, gcols, gvals = gpu_rows(T, ctx, H, nodes)
+    fg = f.cpu().numpy()
+    gg = g.cpu().numpy()
+    del ctx, H
+    ocols, oH, of, oM = oracle.eval_rows(mesh, cfg.material, cfg.quadrature, 0, x, v, cfg.h, nodes)
+    num = den = 0.0
+    fn = fd = gn = gd = 0.0
+    for s, I in enumerate(nodes):
+        c = ocols[s][ocols[s] >= 0]
+        deg = len(c)
+        # DOF columns of row 3I+d are 3J+e for J in c (bit-exact pattern)
+        exp_cols = np.tile((3 * c[:, None] + np.arange(3)[None, :]).ravel(), 3)
+        assert np.array_equal(gcols[s].astype(np.int64), exp_cols), I
+        ov = oH[s][:, :deg, :].reshape(-1)          # [d][k][f]
+        num += np.sum((gvals[s] - ov) ** 2)
+        den += np.sum(ov ** 2)
+        fn += np.sum((fg[3 * I:3 * I + 3] - of[s]) ** 2)
+        fd += np.sum(of[s] ** 2)
+        # residual g = (1/h) M (v - v_n) + f - f_ext - f_ff (gravity 0)
+        m = oM[s][:deg]
+        vd = (v - vn).reshape(-1, 3)[c]
+        g0 = m @ vd / cfg.h + of[s] - (fext[3 * I:3 * I + 3] if fext is not None else 0.0)
+        gn += np.sum((gg[3 * I:3 * I + 3] - g0) ** 2)
+        gd += np.sum(g0 ** 2)
+    assert np.sqrt(num / den) <= TOL, np.sqrt(num / den)
+    assert np.sqrt(fn / fd) <= TOL, np.sqrt(fn / fd)
+    assert np.sqrt(gn / gd) <= TOL, np.sqrt(gn / gd)
+
+
+def test_config5_many_body_sampled_bodies(T):
+    mesh, x, v = synth.many_body()
+    cfg = synth.config(5)
+    ctx = T.Context.from_mesh(mesh, cfg.material, cfg.quadrature)
+    f = ctx.force_only(d(x), d(v)).cpu().numpy()
+    del ctx
+    per = mesh.n_coef // 2000
+    rng = np.random.default_rng(synth.SEED_BASE + 105)
+    nodes = np.concatenate([b * per + rng.choice(per, 6, replace=False) for b in (0, 777, 1999)])
+    _, _, of, _ = oracle.eval_rows(mesh, cfg.material, cfg.quadrature, 0, x, v, cfg.h, nodes)
+    assert rel(f.reshape(-1, 3)[nodes], of) <= TOL
+    # per-body balance on the GPU result (catches cross-body mixing)
+    fb = f.reshape(2000, per, 3)
+    xb = x.reshape(2000, per, 3)
+    s = np.abs(fb).max()
+    assert np.abs(fb.sum(1)).max() < 1e-9 * s * per
+    assert np.abs(np.cross(xb, fb).sum(1)).max() < 1e-8 * s * per
