@@ -114,6 +114,11 @@ struct Context {
   int32_t* dest = nullptr;        // [n_el][n_ublk]
   int32_t* unit_ptr = nullptr;    // [n_units+1]
   int32_t* fdest = nullptr;       // [n_el][nen] position of f_a in the node-sorted force scratch
+  // flattened per-unit output metadata (no dependent index chains in the gather)
+  int32_t* u_off = nullptr;       // [n_units] H offset of block (I,J): 9 rowptr_c[i] + 3 k
+  int32_t* u_offT = nullptr;      // [n_units] H offset of (J,I) or -1
+  int32_t* u_deg = nullptr;       // [n_units] deg(I) | deg(J) << 16
+  double* u_m = nullptr;          // [n_units] M_IJ
   double* Kscr = nullptr;         // [n_el][n_ublk][9]
   double* fscr = nullptr;         // [n_el][nen][3]
   unsigned long long* err_flag = nullptr;  // min over (e*64+q) with det F <= 0 (MR)

@@ -65,8 +65,20 @@ __device__ __forceinline__ int partner(int a, int half, int j) {
 #define TLFEA_T10_MINB 3  // T10 SVK: 3 CTAs of 4 warps per SM (<= 168 registers)
 #endif
 
-template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS>
-__global__ void __launch_bounds__(kWarps * 32, (ELEM == 0 && MODEL == 0) ? TLFEA_T10_MINB : 2)
+#ifndef TLFEA_NPASS
+#define TLFEA_NPASS 1  // block passes per lane (2 halves the live accumulators)
+#endif
+#ifndef TLFEA_T10_MINB2P
+#define TLFEA_T10_MINB2P 4
+#endif
+
+template <int ELEM, int MODEL, int NPASS>
+__host__ __device__ constexpr int el_minb() {
+  return (ELEM == 0 && MODEL == 0) ? (NPASS == 1 ? TLFEA_T10_MINB : TLFEA_T10_MINB2P) : (NPASS == 1 ? 2 : 3);
+}
+
+template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS>
+__global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>())
     k_element(int64_t n_el, const int32_t* __restrict__ conn, const double* __restrict__ gradN,
               const double* __restrict__ J0w, const uint8_t* __restrict__ cls, const double* __restrict__ cls_tab,
               int n_cls, const double* __restrict__ x, const double* __restrict__ v, MatDev mat,
@@ -111,9 +123,15 @@ __global__ void __launch_bounds__(kWarps * 32, (ELEM == 0 && MODEL == 0) ? TLFEA
     if (CLS) ce = cls[e];
   }
   double fa[3] = {0, 0, 0};
-  double K[TAN ? NB : 1][9];
+  // NPASS > 1 splits each lane's blocks over sequential passes that redo the
+  // per-q kinematics: fewer live accumulators -> more resident warps.
+  constexpr int NBP = (NB + NPASS - 1) / NPASS;
+  double K[TAN ? NBP : 1][9];
+
+#pragma unroll 1
+  for (int pass = 0; pass < (TAN ? NPASS : 1); ++pass) {
 #pragma unroll
-  for (int j = 0; j < (TAN ? NB : 1); ++j)
+  for (int j = 0; j < (TAN ? NBP : 1); ++j)
 #pragma unroll
     for (int r = 0; r < 9; ++r) K[j][r] = 0.0;
 
@@ -146,15 +164,13 @@ __global__ void __launch_bounds__(kWarps * 32, (ELEM == 0 && MODEL == 0) ? TLFEA
     __syncwarp();
     if (ELEM == 0) {
       if (lane_active && a < 9) {
-        double s = 0.0;
-#pragma unroll
-        for (int b = 0; b < NEN; ++b) s += s_part[wib][a][gbase + b];
-        s_F[wib][g][a] = s;
+        // pairwise tree over the 10 node partials (short dependency chain)
+        const double* p = &s_part[wib][a][gbase];
+        s_F[wib][g][a] = (((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]))) + (p[8] + p[9]);
         if (KV) {
-          double sd = 0.0;
-#pragma unroll
-          for (int b = 0; b < NEN; ++b) sd += s_part[wib][9 + a][gbase + b];
-          s_F[wib][g][9 + a] = sd;
+          const double* pd = &s_part[wib][9 + a][gbase];
+          s_F[wib][g][9 + a] =
+              (((pd[0] + pd[1]) + (pd[2] + pd[3])) + ((pd[4] + pd[5]) + (pd[6] + pd[7]))) + (pd[8] + pd[9]);
         }
       }
     } else {
@@ -197,8 +213,10 @@ __global__ void __launch_bounds__(kWarps * 32, (ELEM == 0 && MODEL == 0) ? TLFEA
 #pragma unroll
       for (int I = 0; I < 3; ++I)
         t[I] = w * (sget(St, I, 0) * gN[0] + sget(St, I, 1) * gN[1] + sget(St, I, 2) * gN[2]);
+      if (pass == 0) {
 #pragma unroll
-      for (int i = 0; i < 3; ++i) fa[i] = fma(F[3 * i], t[0], fma(F[3 * i + 1], t[1], fma(F[3 * i + 2], t[2], fa[i])));
+        for (int i = 0; i < 3; ++i) fa[i] = fma(F[3 * i], t[0], fma(F[3 * i + 1], t[1], fma(F[3 * i + 2], t[2], fa[i])));
+      }
     }
     if (TAN) {
       double tw[3];  // w * S_el grad N_a (geometric stiffness)
@@ -228,9 +246,11 @@ __global__ void __launch_bounds__(kWarps * 32, (ELEM == 0 && MODEL == 0) ? TLFEA
         const double gNm[3] = {mw * gN[0], mw * gN[1], mw * gN[2]};
         __syncwarp();
 #pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          const int b = partner<ELEM>(a, half, j);
+        for (int jj = 0; jj < NBP; ++jj) {
+          const int j = pass * NBP + jj;
+          const int b = j < NB ? partner<ELEM>(a, half, j) : -1;
           if (b < 0) continue;
+          double* Kj = K[jj];
           const int lb = gbase + b;
           const double gb[3] = {s_node[wib][0][lb], s_node[wib][1][lb], s_node[wib][2][lb]};
           const double nb[3] = {s_node[wib][3][lb], s_node[wib][4][lb], s_node[wib][5][lb]};
@@ -240,8 +260,8 @@ __global__ void __launch_bounds__(kWarps * 32, (ELEM == 0 && MODEL == 0) ? TLFEA
           for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-              double acc = fma(gl[i], gb[k], fma(gb[i], gm[k], fma(d, B[vidx(i, k)], K[j][3 * i + k])));
-              K[j][3 * i + k] = (i == k) ? acc + s : acc;
+              double acc = fma(gl[i], gb[k], fma(gb[i], gm[k], fma(d, B[vidx(i, k)], Kj[3 * i + k])));
+              Kj[3 * i + k] = (i == k) ? acc + s : acc;
             }
         }
       } else {
@@ -283,9 +303,11 @@ __global__ void __launch_bounds__(kWarps * 32, (ELEM == 0 && MODEL == 0) ? TLFEA
             CB[vv][i] = s;
           }
 #pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          const int b = partner<ELEM>(a, half, j);
+        for (int jj = 0; jj < NBP; ++jj) {
+          const int j = pass * NBP + jj;
+          const int b = j < NB ? partner<ELEM>(a, half, j) : -1;
           if (b < 0) continue;
+          double* Kj = K[jj];
           const int lb = gbase + b;
           const double s = fma(tw[0], s_node[wib][18][lb], fma(tw[1], s_node[wib][19][lb], tw[2] * s_node[wib][20][lb]));
 #pragma unroll
@@ -295,10 +317,10 @@ __global__ void __launch_bounds__(kWarps * 32, (ELEM == 0 && MODEL == 0) ? TLFEA
             for (int vv = 0; vv < 6; ++vv) bb[vv] = s_node[wib][3 * vv + k][lb];
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
-              double acc = K[j][3 * i + k];
+              double acc = Kj[3 * i + k];
 #pragma unroll
               for (int vv = 0; vv < 6; ++vv) acc = fma(CB[vv][i], bb[vv], acc);
-              K[j][3 * i + k] = (i == k) ? acc + s : acc;
+              Kj[3 * i + k] = (i == k) ? acc + s : acc;
             }
           }
         }
@@ -307,18 +329,19 @@ __global__ void __launch_bounds__(kWarps * 32, (ELEM == 0 && MODEL == 0) ? TLFEA
     __syncwarp();
   }
 
-  if (!valid) return;
-  if (ELEM == 0 || half == 0) {
+  if (valid && pass == 0 && (ELEM == 0 || half == 0)) {
     double* fo = fscr + (fdest ? (int64_t)fdest[e * NEN + a] : e * NEN + a) * 3;
     fo[0] = fa[0];
     fo[1] = fa[1];
     fo[2] = fa[2];
   }
-  if (TAN) {
+  if (TAN && valid) {
 #pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      const int b = partner<ELEM>(a, half, j);
+    for (int jj = 0; jj < NBP; ++jj) {
+      const int j = pass * NBP + jj;
+      const int b = j < NB ? partner<ELEM>(a, half, j) : -1;
       if (b < 0) continue;
+      const double* Kj = K[jj];
       const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
       // element-major: store the upper block K_{min,max}; gather-sorted: the
       // orientation the receiving unit needs (dest low bit)
@@ -332,15 +355,16 @@ __global__ void __launch_bounds__(kWarps * 32, (ELEM == 0 && MODEL == 0) ? TLFEA
       double* o = Kscr + pos * 9;
       if (!tr) {
 #pragma unroll
-        for (int r = 0; r < 9; ++r) o[r] = K[j][r];
+        for (int r = 0; r < 9; ++r) o[r] = Kj[r];
       } else {
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-          for (int k = 0; k < 3; ++k) o[3 * k + i] = K[j][3 * i + k];
+          for (int k = 0; k < 3; ++k) o[3 * k + i] = Kj[3 * i + k];
       }
     }
   }
+  }  // pass
 }
 
 // ------------------------------------------------------------------ gather
@@ -441,7 +465,20 @@ __global__ void __launch_bounds__(kGWarps * 32)
     const int64_t w1 = min(w0 + (int64_t)WB, P1);
     const int64_t nd = (w1 - w0) * 9;
     const double* src = Kscr + w0 * 9;
-    for (int64_t t = lane; t < nd; t += 32) s_win[wib][t] = __ldcs(src + t);
+    // batches of 8 independent loads per lane in flight before any store
+    for (int64_t t0 = lane; t0 < nd; t0 += 32 * 8) {
+      double r[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t t = t0 + 32 * k;
+        r[k] = t < nd ? __ldcs(src + t) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t t = t0 + 32 * k;
+        if (t < nd) s_win[wib][t] = r[k];
+      }
+    }
     __syncwarp();
     const int64_t a0 = max((int64_t)my0, w0), a1 = min((int64_t)my1, w1);
     for (int64_t t = a0; t < a1; ++t) {
@@ -472,6 +509,177 @@ __global__ void __launch_bounds__(kGWarps * 32)
   }
 }
 
+// v2: metadata flattened per unit (one level of independent loads) and the
+// scratch window moved global -> shared with cp.async (LDGSTS, no register
+// staging), so a warp has its whole contiguous range in flight at once.
+constexpr int kG2Warps = 4;
+constexpr int kG2Win = 1152;  // doubles per warp (128 blocks, 9.2 KB; 37 KB per CTA)
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+__global__ void __launch_bounds__(kG2Warps * 32)
+    k_gather_units_v2(int64_t n_units, const int32_t* __restrict__ unit_ptr, const int32_t* __restrict__ u_off,
+                      const int32_t* __restrict__ u_offT, const int32_t* __restrict__ u_deg,
+                      const double* __restrict__ u_m, const double* __restrict__ Kscr, double h,
+                      double* __restrict__ H) {
+  __shared__ double s_win[kG2Warps][kG2Win];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t u0 = ((int64_t)blockIdx.x * kG2Warps + wib) * 32;
+  if (u0 >= n_units) return;
+  const int64_t u = u0 + lane;
+  const bool valid = u < n_units;
+  const int64_t uend = min(u0 + 32, n_units);
+  const int64_t P0 = unit_ptr[u0], P1 = unit_ptr[uend];
+  // independent metadata loads, issued before the data is needed
+  int32_t my0 = 0, my1 = 0, off = 0, offT = -1, dg = 0;
+  double m = 0.0;
+  if (valid) {
+    my0 = unit_ptr[u];
+    my1 = unit_ptr[u + 1];
+    off = u_off[u];
+    offT = u_offT[u];
+    dg = u_deg[u];
+    m = u_m[u];
+  }
+  double acc[9];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) acc[r] = 0.0;
+  constexpr int WB = kG2Win / 9;
+  for (int64_t w0 = P0; w0 < P1; w0 += WB) {
+    const int64_t w1 = min(w0 + (int64_t)WB, P1);
+    const int nd = (int)((w1 - w0) * 9);
+    const double* src = Kscr + w0 * 9;
+    for (int t = lane; t < nd; t += 32) cp_async8(&s_win[wib][t], src + t);
+    cp_async_wait_all();
+    __syncwarp();
+    const int64_t a0 = max((int64_t)my0, w0), a1 = min((int64_t)my1, w1);
+    for (int64_t t = a0; t < a1; ++t) {
+      const double* sb = &s_win[wib][(t - w0) * 9];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) acc[r] += sb[r];
+    }
+    __syncwarp();
+  }
+  if (!valid) return;
+  const double mh = m / h;
+  const int deg = dg & 0xffff, degT = dg >> 16;
+  double* out = H + off;
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int f = 0; f < 3; ++f) out[3 * d * deg + f] = fma(h, acc[3 * d + f], d == f ? mh : 0.0);
+  if (offT >= 0) {
+    double* o2 = H + offT;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int f = 0; f < 3; ++f) o2[3 * d * degT + f] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
+  }
+}
+
+// v3: TMA bulk copies (cp.async.bulk global->shared, mbarrier completion),
+// double-buffered per warp: one elected lane moves the next window of the
+// contiguous scratch range while the warp sums the current one.
+constexpr int kG3Warps = 4;
+constexpr int kG3WB = 64;                    // blocks per window
+constexpr int kG3Buf = kG3WB * 9 + 2;        // doubles per buffer (+16 B alignment slack)
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kG3Warps * 32)
+    k_gather_units_v3(int64_t n_units, const int32_t* __restrict__ unit_ptr, const int32_t* __restrict__ u_off,
+                      const int32_t* __restrict__ u_offT, const int32_t* __restrict__ u_deg,
+                      const double* __restrict__ u_m, const double* __restrict__ Kscr, double h,
+                      double* __restrict__ H) {
+  __shared__ __align__(16) double s_buf[kG3Warps][2][kG3Buf];
+  __shared__ __align__(8) uint64_t s_bar[kG3Warps][2];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (lane == 0) {
+    mbar_init(&s_bar[wib][0], 1);
+    mbar_init(&s_bar[wib][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  const int64_t u0 = ((int64_t)blockIdx.x * kG3Warps + wib) * 32;
+  if (u0 >= n_units) return;
+  const int64_t u = u0 + lane;
+  const bool valid = u < n_units;
+  const int64_t uend = min(u0 + 32, n_units);
+  const int64_t P0 = unit_ptr[u0], P1 = unit_ptr[uend];
+  int32_t my0 = 0, my1 = 0, off = 0, offT = -1, dg = 0;
+  double m = 0.0;
+  if (valid) {
+    my0 = unit_ptr[u];
+    my1 = unit_ptr[u + 1];
+    off = u_off[u];
+    offT = u_offT[u];
+    dg = u_deg[u];
+    m = u_m[u];
+  }
+  const int nwin = (int)((P1 - P0 + kG3WB - 1) / kG3WB);
+  auto issue = [&](int k) {
+    const int64_t w0 = P0 + (int64_t)k * kG3WB, w1 = min(w0 + (int64_t)kG3WB, P1);
+    const uintptr_t a = (uintptr_t)(Kscr + w0 * 9) & ~(uintptr_t)15;
+    const uintptr_t b = ((uintptr_t)(Kscr + w1 * 9) + 15) & ~(uintptr_t)15;
+    bulk_load(&s_buf[wib][k & 1][0], (const void*)a, (unsigned)(b - a), &s_bar[wib][k & 1]);
+  };
+  if (lane == 0 && nwin > 0) issue(0);
+  double acc[9];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) acc[r] = 0.0;
+  for (int k = 0; k < nwin; ++k) {
+    if (lane == 0 && k + 1 < nwin) issue(k + 1);
+    mbar_wait(&s_bar[wib][k & 1], (unsigned)((k >> 1) & 1));
+    const int64_t w0 = P0 + (int64_t)k * kG3WB, w1 = min(w0 + (int64_t)kG3WB, P1);
+    const int delta = (int)(((uintptr_t)(Kscr + w0 * 9) & 15) >> 3);  // 0 or 1 double
+    const double* buf = &s_buf[wib][k & 1][delta];
+    const int64_t a0 = max((int64_t)my0, w0), a1 = min((int64_t)my1, w1);
+    for (int64_t t = a0; t < a1; ++t) {
+      const double* sb = buf + (t - w0) * 9;
+#pragma unroll
+      for (int r = 0; r < 9; ++r) acc[r] += sb[r];
+    }
+    __syncwarp();
+  }
+  if (!valid) return;
+  const double mh = m / h;
+  const int deg = dg & 0xffff, degT = dg >> 16;
+  double* out = H + off;
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int f = 0; f < 3; ++f) out[3 * d * deg + f] = fma(h, acc[3 * d + f], d == f ? mh : 0.0);
+  if (offT >= 0) {
+    double* o2 = H + offT;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int f = 0; f < 3; ++f) o2[3 * d * degT + f] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
+  }
+}
+
 // ------------------------------------------------------------- launchers
 
 template <int ELEM, int NQ, int MODEL, bool KV, bool TAN>
@@ -484,15 +692,15 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
     const size_t smem = sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
     static size_t smem_set = 0;  // per template instantiation
     if (smem > smem_set) {
-      TL_CUDA(cudaFuncSetAttribute(k_element<ELEM, NQ, MODEL, KV, TAN, true>,
+      TL_CUDA(cudaFuncSetAttribute(k_element<ELEM, NQ, MODEL, KV, TAN, true, TLFEA_NPASS>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       smem_set = smem;
     }
-    k_element<ELEM, NQ, MODEL, KV, TAN, true><<<grid, kWarps * 32, smem, s>>>(
+    k_element<ELEM, NQ, MODEL, KV, TAN, true, TLFEA_NPASS><<<grid, kWarps * 32, smem, s>>>(
         c->n_el, c->conn, c->gradN, c->J0w, c->cls, c->cls_tab, c->n_cls, x, v, c->mat, c->fscr, c->Kscr,
         c->dest, c->fdest, c->err_flag);
   } else {
-    k_element<ELEM, NQ, MODEL, KV, TAN, false><<<grid, kWarps * 32, 0, s>>>(
+    k_element<ELEM, NQ, MODEL, KV, TAN, false, TLFEA_NPASS><<<grid, kWarps * 32, 0, s>>>(
         c->n_el, c->conn, c->gradN, c->J0w, c->cls, c->cls_tab, 0, x, v, c->mat, c->fscr, c->Kscr, c->dest,
         c->fdest, c->err_flag);
   }
@@ -524,6 +732,13 @@ tlfea_status launch_element_kernel(Context* c, const double* x, const double* v,
 
 tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
   if (c->n_units == 0) return TLFEA_OK;
+  if (c->u_off) {
+    const int64_t per = (int64_t)kG3Warps * 32;
+    k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(
+        c->n_units, c->unit_ptr, c->u_off, c->u_offT, c->u_deg, c->u_m, c->Kscr, h, H);
+    TL_CHECK_LAUNCH();
+    return TLFEA_OK;
+  }
   if (c->unit_ptr) {
     const int64_t per = (int64_t)kGWarps * 32;
     k_gather_units_sorted<<<(unsigned)((c->n_units + per - 1) / per), kGWarps * 32, 0, s>>>(

@@ -44,6 +44,7 @@ __global__ void k_gather_f(int64_t n_own, int nen, const int32_t* __restrict__ n
     f1 = fpart_in[3 * i + 1];
     f2 = fpart_in[3 * i + 2];
   } else {
+#pragma unroll 4
     for (int32_t t = node_ptr[i]; t < node_ptr[i + 1]; ++t) {
       const double* s;
       if (sorted) {
@@ -64,6 +65,7 @@ __global__ void k_gather_f(int64_t n_own, int nen, const int32_t* __restrict__ n
   }
   if (mode == 1 || !g) return;
   double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+#pragma unroll 4
   for (int32_t p = rowptr_c[i]; p < rowptr_c[i + 1]; ++p) {
     const int64_t J = cols_c[p];
     const double mm = M[p];

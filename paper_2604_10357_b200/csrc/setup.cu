@@ -469,6 +469,26 @@ __global__ void k_unit_dest(int64_t n_units, int nen, int nub, const int32_t* __
   }
 }
 
+__global__ void k_unit_meta(int64_t n_units, const int32_t* __restrict__ unit_p, const int32_t* __restrict__ unit_pT,
+                            const int32_t* __restrict__ blk_row, const int32_t* __restrict__ rowptr_c,
+                            const double* __restrict__ M, int32_t* __restrict__ u_off, int32_t* __restrict__ u_offT,
+                            int32_t* __restrict__ u_deg, double* __restrict__ u_m) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n_units) return;
+  const int32_t p = unit_p[u], pT = unit_pT[u];
+  const int32_t i = blk_row[p], b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0;
+  u_off[u] = 9 * b0 + 3 * (p - b0);
+  int32_t degT = 0, offT = -1;
+  if (pT >= 0) {
+    const int32_t j = blk_row[pT], c0 = rowptr_c[j];
+    degT = rowptr_c[j + 1] - c0;
+    offT = 9 * c0 + 3 * (pT - c0);
+  }
+  u_offT[u] = offT;
+  u_deg[u] = deg | (degT << 16);
+  u_m[u] = M[p];
+}
+
 __global__ void k_force_dest(int64_t n, int nen, const uint32_t* __restrict__ node_ent, int32_t* __restrict__ fdest) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n) return;
@@ -650,6 +670,18 @@ static tlfea_status build_sorted_scratch(Context* c) {
     k_force_dest<<<grid_for(nf, 256), 256>>>(nf, nen, c->node_ent, c->fdest);
     TL_CHECK_LAUNCH();
   }
+  return TLFEA_OK;
+}
+
+static tlfea_status build_unit_meta(Context* c) {
+  if (c->n_units == 0 || !c->unit_ptr) return TLFEA_OK;
+  TL_TRY(c->alloc(&c->u_off, (size_t)c->n_units));
+  TL_TRY(c->alloc(&c->u_offT, (size_t)c->n_units));
+  TL_TRY(c->alloc(&c->u_deg, (size_t)c->n_units));
+  TL_TRY(c->alloc(&c->u_m, (size_t)c->n_units));
+  k_unit_meta<<<grid_for(c->n_units, 256), 256>>>(c->n_units, c->unit_p, c->unit_pT, c->blk_row, c->rowptr_c, c->M,
+                                                  c->u_off, c->u_offT, c->u_deg, c->u_m);
+  TL_CHECK_LAUNCH();
   return TLFEA_OK;
 }
 
@@ -996,8 +1028,11 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     }
   }
 
+  TL_TRY(build_unit_meta(c));
+
   // ---- eval scratch
-  TL_TRY(c->alloc(&c->Kscr, (size_t)c->n_el * n_ublk_of(nen) * 9));
+  // +4 doubles: the bulk-copy gather rounds its windows out to 16-byte bounds
+  TL_TRY(c->alloc(&c->Kscr, (size_t)c->n_el * n_ublk_of(nen) * 9 + 4));
   TL_TRY(c->alloc(&c->fscr, (size_t)c->n_el * nen * 3));
   TL_TRY(c->alloc(&c->fpart, (size_t)3 * std::max<int64_t>(c->n_own, 1)));
 
