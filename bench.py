@@ -41,7 +41,15 @@ import synth  # noqa: E402
 
 METRIC = "T10 force+tangent assembly elements/s (fp64) and % of B200 HBM roofline"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz
+FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz
+FP64_PEAK_PATH = os.path.join(ROOT, "profiles", "fp64_peak.json")   # tools/fp64_peak on a B200
+
+
+def fp64_peak():
+    try:
+        return float(json.load(open(FP64_PEAK_PATH))["fp64_tflops"]), "measured (tools/fp64_peak, profiles/fp64_peak.json)"
+    except Exception:
+        return FP64_NOMINAL_TFLOPS, "nominal 148 SM x 64 FMA x 2 x 1.965 GHz (DESIGN.md)"
 
 # Exact structured-SVK operation counts: flops per
 # quadrature point for force only / force + symmetric tangent.
@@ -131,9 +139,12 @@ def bytes_per_element(mesh, info, tangent: bool, kv: bool):
     nen, nq = info["n_en"], info["n_qp"]
     nub = nen * (nen + 1) // 2
     coords = 24.0 * mesh.n_coef / mesh.n_el * (2 if kv else 1)
-    b = 4 * nen + 8 * nq * (3 * nen + 1) + coords + 24 * nen
+    # reference data: per-(e,q) tables (paper layout) or, with geometry
+    # classes, one class id per element (tables staged in shared memory)
+    ref = 1 if info.get("n_geometry_classes", 0) > 0 else 8 * nq * (3 * nen + 1)
+    b = 4 * nen + ref + coords + 24 * nen
     if tangent:
-        b += 72 * nub
+        b += 72 * nub + 4 * nub   # upper blocks + their gather-sorted destinations
     return b
 
 
@@ -321,7 +332,8 @@ def run_ours(args):
         flops_launch = 3 * info["n_elements"] * info["n_en"]
     gbs = bytes_launch / (avg_ms / 1e3) / 1e9
     tfl = flops_launch / (avg_ms / 1e3) / 1e12
-    f_hbm, f_fp64 = gbs / hbm_peak, tfl / FP64_PEAK_TFLOPS
+    fp64_pk, fp64_src = fp64_peak()
+    f_hbm, f_fp64 = gbs / hbm_peak, tfl / fp64_pk
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -333,8 +345,8 @@ def run_ours(args):
         roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": f_hbm,
                 "traffic": traffic, "peak_source": hbm_src}
     else:
-        roof = {"bound": "alu", "achieved": tfl, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": f_fp64,
-                "traffic": traffic, "peak_source": "fp64 nominal 148 SM x 64 FMA x 2 x 1.965 GHz (DESIGN.md)"}
+        roof = {"bound": "alu", "achieved": tfl, "peak": fp64_pk, "unit": "TFLOP/s", "frac": f_fp64,
+                "traffic": traffic, "peak_source": fp64_src}
     roof.update({"kernel": dom, "kernel_ms": avg_ms, "hbm_frac": f_hbm, "fp64_frac": f_fp64,
                  "alg_bytes_per_launch": bytes_launch, "alg_flops_per_launch": flops_launch})
     path_b = path_bytes_per_element(mesh, info, not force_only, kv) * mesh.n_el
