@@ -58,6 +58,7 @@ struct MatDev {
   double C10, C01, kappa;
   double eta, lamd;
   double rho0;
+  int dbg_nowrite;  // diagnostics only: skip the tangent scratch stores (TLFEA_DBG_NOKWRITE=1)
 };
 
 // Device buffer helper (raw cudaMalloc, owned by the context)

@@ -335,36 +335,316 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>())
     fo[1] = fa[1];
     fo[2] = fa[2];
   }
-  if (TAN && valid) {
+  // Tangent blocks -> scratch. Each lane's blocks go to scattered 72-byte
+  // slots; storing them lane-by-lane would issue one 8-byte sector request per
+  // value (measured: half of the kernel time). Instead each round stages one
+  // block per lane (already in the orientation its receiver needs) in shared
+  // memory and the warp writes the round's blocks as consecutive doubles, so a
+  // warp store covers 3-4 whole blocks.
+  if (TAN && !mat.dbg_nowrite) {
+    __shared__ int64_t s_pos[kWarps][32];
 #pragma unroll
     for (int jj = 0; jj < NBP; ++jj) {
       const int j = pass * NBP + jj;
-      const int b = j < NB ? partner<ELEM>(a, half, j) : -1;
-      if (b < 0) continue;
-      const double* Kj = K[jj];
-      const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
-      // element-major: store the upper block K_{min,max}; gather-sorted: the
-      // orientation the receiving unit needs (dest low bit)
-      bool tr = a > b;
-      int64_t pos = e * NUB + ub;
-      if (dest) {
-        const int32_t d = dest[e * NUB + ub];
-        pos = d >> 1;
-        tr = tr != ((d & 1) != 0);
-      }
-      double* o = Kscr + pos * 9;
-      if (!tr) {
-#pragma unroll
-        for (int r = 0; r < 9; ++r) o[r] = Kj[r];
-      } else {
+      const int b = (valid && j < NB) ? partner<ELEM>(a, half, j) : -1;
+      int64_t pos = -1;
+      if (b >= 0) {
+        const double* Kj = K[jj];
+        const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
+        // element-major: store the upper block K_{min,max}; gather-sorted: the
+        // orientation the receiving unit needs (dest low bit)
+        bool tr = a > b;
+        pos = e * NUB + ub;
+        if (dest) {
+          const int32_t d = dest[e * NUB + ub];
+          pos = d >> 1;
+          tr = tr != ((d & 1) != 0);
+        }
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-          for (int k = 0; k < 3; ++k) o[3 * k + i] = Kj[3 * i + k];
+          for (int k = 0; k < 3; ++k) s_part[wib][tr ? 3 * k + i : 3 * i + k][lane] = Kj[3 * i + k];
       }
+      s_pos[wib][lane] = pos;
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < 9; ++it) {
+        const int t = lane + 32 * it;  // value t of the round: block t / 9, entry t % 9
+        const int blk = t / 9, r = t - 9 * (t / 9);
+        const int64_t p = s_pos[wib][blk];
+        if (p >= 0) Kscr[p * 9 + r] = s_part[wib][r][blk];
+      }
+      __syncwarp();
     }
   }
   }  // pass
+}
+
+// ------------------------------------------------ FP64 tensor-core variant
+// T10 + SVK + congruent-element classes. The element tangent is split as
+//   K_ab = lam G_ab + mu G_ab^T + D_ab + sigma_ab I,
+//   G = sum_q w_q g(q) g(q)^T          (30x30 Gram of g_(a,i) = (F grad N_a)_i)
+//   D_ab = sum_q mu w_q d_ab(q) F F^T,  sigma_ab = sum_q w_q grad N_a . S grad N_b
+// (Eq. tangent_block P:527-534 for A = dP/dF of SVK, reading Q5). G — 55 % of
+// the flops — is a dense GEMM per element (M = N = 30 -> 32, K = n_qp -> 8):
+// 10 upper 8x8 tiles x 2 k-steps of mma.sync.m8n8k4.f64 (DMMA) per element.
+// D and sigma accumulate per q in the owner-lane layout of k_element; the
+// Gram blocks meet them through a compact shared-memory block store.
+constexpr int kTCWarps = 4;
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int NQ, bool KV>
+__global__ void __launch_bounds__(kTCWarps * 32, 2)
+    k_t10_tc(int64_t n_el, const int32_t* __restrict__ conn, const uint8_t* __restrict__ cls,
+             const double* __restrict__ cls_tab, int n_cls, const double* __restrict__ x,
+             const double* __restrict__ v, MatDev mat, double* __restrict__ fscr, double* __restrict__ Kscr,
+             const int32_t* __restrict__ dest, const int32_t* __restrict__ fdest) {
+  constexpr int NEN = 10, GROUP = 10, EPW = 3, NUB = 55, NB = 6;
+  constexpr int NC = KV ? 18 : 9;
+  constexpr int TABW = NEN * 3 + 1;
+  static_assert(NQ <= 8, "k-dimension holds at most 8 quadrature points");
+  __shared__ double s_part[kTCWarps][NC][kLD];
+  __shared__ double s_F[kTCWarps][EPW][NC];
+  // dynamic shared memory: [class tables][G operand][compact Gram blocks]
+  extern __shared__ __align__(16) double s_dyn[];
+  double* s_tab = s_dyn;
+  const int tab_len = (n_cls * NQ * TABW + 1) & ~1;
+  typedef double GOp[EPW][2][32][4];                 // [element][k-half][row (a,i)][q % 4]
+  typedef double GamBlk[EPW][NUB * 9];
+  GOp* s_G = reinterpret_cast<GOp*>(s_dyn + tab_len);
+  GamBlk* s_Gam = reinterpret_cast<GamBlk*>(s_dyn + tab_len + kTCWarps * EPW * 256);
+
+  {
+    const int tot = n_cls * NQ * TABW;
+    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_tab[t] = cls_tab[t];
+    double* z = &s_G[0][0][0][0][0];
+    for (int t = threadIdx.x; t < kTCWarps * EPW * 256; t += blockDim.x) z[t] = 0.0;
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const bool lane_active = lane < EPW * GROUP;
+  const int g = lane_active ? lane / GROUP : 0;
+  const int a = lane_active ? lane % GROUP : 0;
+  const int64_t ebase = ((int64_t)blockIdx.x * kTCWarps + wib) * EPW;
+  const int64_t e = ebase + g;
+  const bool valid = lane_active && e < n_el;
+  const int gbase = g * GROUP;
+
+  double xa[3] = {0, 0, 0}, va[3] = {0, 0, 0};
+  int ce = 0;
+  if (valid) {
+    const int64_t I = conn[e * NEN + a];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) xa[i] = x[3 * I + i];
+    if (KV) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) va[i] = v[3 * I + i];
+    }
+    ce = cls[e];
+  }
+  double fa[3] = {0, 0, 0};
+  double Dm[NB][6], sg[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    sg[j] = 0.0;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) Dm[j][r] = 0.0;
+  }
+
+  // ---------------- phase A: per quadrature point (3 elements per warp)
+#pragma unroll 1
+  for (int q = 0; q < NQ; ++q) {
+    const double* tq = s_tab + (ce * NQ + q) * TABW;
+    double gN[3] = {0, 0, 0}, w = 0.0;
+    if (valid) {
+      gN[0] = tq[3 * a];
+      gN[1] = tq[3 * a + 1];
+      gN[2] = tq[3 * a + 2];
+      w = tq[3 * NEN];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int J = 0; J < 3; ++J) {
+        s_part[wib][3 * i + J][lane] = xa[i] * gN[J];
+        if (KV) s_part[wib][9 + 3 * i + J][lane] = va[i] * gN[J];
+      }
+    __syncwarp();
+    if (lane_active && a < 9) {
+      const double* p = &s_part[wib][a][gbase];
+      s_F[wib][g][a] = (((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]))) + (p[8] + p[9]);
+      if (KV) {
+        const double* pd = &s_part[wib][9 + a][gbase];
+        s_F[wib][g][9 + a] =
+            (((pd[0] + pd[1]) + (pd[2] + pd[3])) + ((pd[4] + pd[5]) + (pd[6] + pd[7]))) + (pd[8] + pd[9]);
+      }
+    }
+    __syncwarp();
+    double F[9], Fd[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      F[r] = s_F[wib][g][r];
+      if (KV) Fd[r] = s_F[wib][g][9 + r];
+    }
+    double S[6], St[6];
+    svk_S(F, mat.lam, mat.mu, S);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) St[r] = S[r];
+    if (KV) {
+      double Sv[6];
+      kv_S(F, Fd, mat.eta, mat.lamd, Sv);
+#pragma unroll
+      for (int r = 0; r < 6; ++r) St[r] += Sv[r];
+    }
+    {  // Stage 2 force
+      double t[3];
+#pragma unroll
+      for (int I = 0; I < 3; ++I)
+        t[I] = w * (sget(St, I, 0) * gN[0] + sget(St, I, 1) * gN[1] + sget(St, I, 2) * gN[2]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) fa[i] = fma(F[3 * i], t[0], fma(F[3 * i + 1], t[1], fma(F[3 * i + 2], t[2], fa[i])));
+    }
+    // Gram operand: g_a = F grad N_a into G[(a,i)][q]
+    if (valid) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        s_G[wib][g][q >> 2][3 * a + i][q & 3] = F[3 * i] * gN[0] + F[3 * i + 1] * gN[1] + F[3 * i + 2] * gN[2];
+    }
+    double B[6];
+#pragma unroll
+    for (int vv = 0; vv < 6; ++vv) {
+      int i, k;
+      voigt_pair(vv, i, k);
+      B[vv] = F[3 * i] * F[3 * k] + F[3 * i + 1] * F[3 * k + 1] + F[3 * i + 2] * F[3 * k + 2];
+    }
+    double tw[3], gNm[3];
+    const double mw = mat.mu * w;
+#pragma unroll
+    for (int I = 0; I < 3; ++I) {
+      tw[I] = w * (sget(S, I, 0) * gN[0] + sget(S, I, 1) * gN[1] + sget(S, I, 2) * gN[2]);
+      gNm[I] = mw * gN[I];
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int b = partner<0>(a, 0, j);
+      if (b < 0) continue;
+      const double nb0 = tq[3 * b], nb1 = tq[3 * b + 1], nb2 = tq[3 * b + 2];
+      sg[j] += fma(tw[0], nb0, fma(tw[1], nb1, tw[2] * nb2));
+      const double d = fma(gNm[0], nb0, fma(gNm[1], nb1, gNm[2] * nb2));
+#pragma unroll
+      for (int r = 0; r < 6; ++r) Dm[j][r] = fma(d, B[r], Dm[j][r]);
+    }
+    __syncwarp();
+  }
+
+  // ---------------- phase B: Gram G = sum_q w g g^T on the FP64 tensor cores
+  const int fr = lane >> 2, fc = lane & 3;
+  // per-lane destinations of the 20 accumulator entries in the compact block
+  // store (primary | mirror << 16, 0xffff = none), constant across elements
+  int gmap[20];
+  {
+    int n = 0;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = mi; ni < 4; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h, ++n) {
+          const int r = 8 * mi + fr, c = 8 * ni + 2 * fc + h;
+          int prim = 0xffff, mir = 0xffff;
+          if (r < 30 && c < 30 && r <= c) {
+            const int A = r / 3, Bn = c / 3, ri = r % 3, ci = c % 3;
+            prim = ublk(NEN, A, Bn) * 9 + 3 * ri + ci;
+            if (A == Bn && ri != ci) mir = ublk(NEN, A, Bn) * 9 + 3 * ci + ri;
+          }
+          gmap[n] = prim | (mir << 16);
+        }
+  }
+#pragma unroll 1
+  for (int gg = 0; gg < EPW; ++gg) {
+    if (ebase + gg >= n_el) break;
+    const int cg = cls[ebase + gg];
+    double bf[2][4], af[2][4];
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const int q = 4 * kk + fc;
+      const double wq = q < NQ ? s_tab[(cg * NQ + q) * TABW + 3 * NEN] : 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        bf[kk][t] = s_G[wib][gg][kk][8 * t + fr][fc];
+        af[kk][t] = wq * bf[kk][t];
+      }
+    }
+    double* gam = s_Gam[wib][gg];
+    int n = 0;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = mi; ni < 4; ++ni) {
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) dmma884(c0, c1, af[kk][mi], bf[kk][ni]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h, ++n) {
+          const double val = h ? c1 : c0;
+          const int prim = gmap[n] & 0xffff, mir = gmap[n] >> 16;
+          if (prim != 0xffff) gam[prim] = val;
+          if (mir != 0xffff) gam[mir] = val;
+        }
+      }
+  }
+  __syncwarp();
+
+  // ---------------- phase C: K_ab = lam G_ab + mu G_ab^T + D_ab + sigma_ab I
+  if (!valid) return;
+  {
+    double* fo = fscr + (fdest ? (int64_t)fdest[e * NEN + a] : e * NEN + a) * 3;
+    fo[0] = fa[0];
+    fo[1] = fa[1];
+    fo[2] = fa[2];
+  }
+  const double* gam = s_Gam[wib][g];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const int b = partner<0>(a, 0, j);
+    if (b < 0) continue;
+    const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
+    const double* gb = gam + ub * 9;
+    double Gab[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) Gab[3 * i + k] = a <= b ? gb[3 * i + k] : gb[3 * k + i];
+    double K[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        K[3 * i + k] = fma(mat.lam, Gab[3 * i + k], fma(mat.mu, Gab[3 * k + i], Dm[j][vidx(i, k)])) +
+                       (i == k ? sg[j] : 0.0);
+    bool tr = a > b;
+    int64_t pos = e * NUB + ub;
+    if (dest) {
+      const int32_t dd = dest[e * NUB + ub];
+      pos = dd >> 1;
+      tr = tr != ((dd & 1) != 0);
+    }
+    double* o = Kscr + pos * 9;
+    if (!tr) {
+#pragma unroll
+      for (int r = 0; r < 9; ++r) o[r] = K[r];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) o[3 * k + i] = K[3 * i + k];
+    }
+  }
 }
 
 // ------------------------------------------------------------------ gather
@@ -682,12 +962,53 @@ __global__ void __launch_bounds__(kG3Warps * 32)
 
 // ------------------------------------------------------------- launchers
 
+// FP64 tensor-core tangent (k_t10_tc) on by default; TLFEA_TC=0 selects the
+// all-DFMA k_element (A/B measurements).
+static bool use_tc() {
+  // measured slower than the all-DFMA kernel on B200 (DMMA shares the FP64
+  // throughput and the fragment->block exchange adds shared-memory traffic):
+  // off by default, TLFEA_TC=1 enables it.
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TLFEA_TC");
+    v = (s && s[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+static int dbg_nowrite() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TLFEA_DBG_NOKWRITE");
+    v = (s && s[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
+
 template <int ELEM, int NQ, int MODEL, bool KV, bool TAN>
 static tlfea_status launch_el(Context* c, const double* x, const double* v, cudaStream_t s) {
   using G = Geo<ELEM>;
+  if constexpr (ELEM == 0 && MODEL == 0 && TAN) {
+    if (c->n_cls > 0 && use_tc()) {
+      const int tab_len = (c->n_cls * NQ * 31 + 1) & ~1;
+      const size_t smem = sizeof(double) * ((size_t)tab_len + kTCWarps * 3 * 256 + kTCWarps * 3 * 55 * 9);
+      static size_t smem_set = 0;
+      if (smem > smem_set) {
+        TL_CUDA(cudaFuncSetAttribute(k_t10_tc<NQ, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set = smem;
+      }
+      const int64_t per = (int64_t)kTCWarps * 3;
+      const unsigned grid = (unsigned)((c->n_el + per - 1) / per);
+      if (grid == 0) return TLFEA_OK;
+      k_t10_tc<NQ, KV><<<grid, kTCWarps * 32, smem, s>>>(c->n_el, c->conn, c->cls, c->cls_tab, c->n_cls, x, v,
+                                                         c->mat, c->fscr, c->Kscr, c->dest, c->fdest);
+      TL_CHECK_LAUNCH();
+      return TLFEA_OK;
+    }
+  }
   const int64_t per_cta = (int64_t)kWarps * G::EPW;
   const unsigned grid = (unsigned)((c->n_el + per_cta - 1) / per_cta);
   if (grid == 0) return TLFEA_OK;
+  c->mat.dbg_nowrite = dbg_nowrite();
   if (c->n_cls > 0) {
     const size_t smem = sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
     static size_t smem_set = 0;  // per template instantiation
