@@ -148,6 +148,24 @@ def bytes_per_element(mesh, info, tangent: bool, kv: bool):
     return b
 
 
+def fused_bytes_per_element(mesh, info, kv: bool):
+    """Algorithmic bytes per element of the fused persistent eval (the whole
+    tangent path in one kernel): what must cross
+    HBM with no intermediate at all — connectivity, one class id, the unique
+    gathers of x (v) and of v, v_n, f_ext for the residual, the unique g and
+    f_int writes, the H values, and the mass row (values + columns) the
+    residual reads. The element scratch round trip is NOT counted: it is the
+    implementation's cost and shows up as `traffic` above these bytes."""
+    nen = info["n_en"]
+    per_node = mesh.n_coef / mesh.n_el
+    b = 4 * nen + 1
+    b += per_node * 24 * 4                 # x, v (also Fdot when KV), v_n, f_ext
+    b += per_node * 24 * 2                 # g, f_int
+    b += 8 * info["nnz"] / mesh.n_el       # H
+    b += 12 * info["nnz_coef"] / mesh.n_el  # M values + column ids
+    return b
+
+
 def path_bytes_per_element(mesh, info, tangent: bool, kv: bool):
     """Algorithmic bytes per element of the whole path (SURVEY §8(d) 'paper
     layout' accounting): unique gathers of x, v, v_n, f_ext, the unique f/g
@@ -322,6 +340,10 @@ def run_ours(args):
         bpe = bytes_per_element(mesh, info, not force_only, kv)
         bytes_launch = bpe * info["n_elements"]
         flops_launch = FLOP_PER_QP[(elem, not force_only)] * info["n_qp"] * info["n_elements"]
+    elif dom == "fused":
+        bytes_launch = fused_bytes_per_element(mesh, info, kv) * info["n_elements"]
+        flops_launch = (FLOP_PER_QP[(elem, True)] * info["n_qp"] * info["n_elements"]
+                        + 9 * info["n_elements"] * info["n_en"] ** 2)
     elif dom == "gather_H":
         nnz_c = info["nnz_coef"]
         contrib = info["n_elements"] * info["n_en"] ** 2

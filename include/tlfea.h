@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define TLFEA_ABI_VERSION 1
+#define TLFEA_ABI_VERSION 2
 
 typedef struct tlfea_ctx_s* tlfea_ctx;
 
@@ -149,7 +149,12 @@ typedef struct {
   int32_t n_geometry_classes; /* > 0: congruent elements share reference
                                  tables (staged in shared memory); 0: the
                                  per-(e,q) tables of §4.1 are read from HBM */
-  int32_t reserved;
+  int32_t fused_eval;      /* 1: tlfea_eval runs as ONE persistent kernel
+                              (element tiles + dependency-ordered H and f/g
+                              gather items, results bitwise equal to the
+                              three-kernel path); 0: three kernels. Opt-in
+                              (TLFEA_FUSED=1 in the environment at setup) for
+                              single-rank contexts with geometry classes. */
 } tlfea_info_t;
 
 /* ---------------------------------------------------------------- setup -- */
@@ -343,8 +348,10 @@ tlfea_status tlfea_test_constitutive(const tlfea_material* mat, int64_t n,
  * kernel of this context is bracketed by CUDA events recorded on its launch
  * stream. tlfea_timing_report synchronizes and returns, per kernel class
  * (0 element kernel, 1 H gather, 2 force gather / residual, 3 partition
- * pack/unpack), the number of launches and their summed duration in ms, and
- * resets the record. counts/ms are HOST arrays of length 4. */
+ * pack/unpack, 4 fused persistent eval), the number of launches and their
+ * summed duration in ms, and resets the record. counts/ms are HOST arrays of
+ * length TLFEA_N_TIMING. */
+#define TLFEA_N_TIMING 5
 tlfea_status tlfea_set_timing(tlfea_ctx ctx, int32_t enable);
 tlfea_status tlfea_timing_report(tlfea_ctx ctx, int64_t* counts, double* ms);
 

@@ -60,7 +60,10 @@ class Info(C.Structure):
                 ("n_elements", C.c_int64), ("n_elements_global", C.c_int64), ("n_coef", C.c_int64),
                 ("n_dof", C.c_int64), ("nnz_coef", C.c_int64), ("nnz", C.c_int64), ("n_owned_nodes", C.c_int64),
                 ("affine", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32), ("device_bytes", C.c_int64),
-                ("n_geometry_classes", C.c_int32), ("reserved", C.c_int32)]
+                ("n_geometry_classes", C.c_int32), ("fused_eval", C.c_int32)]
+
+N_TIMING = 5
+TIMING_KINDS = ("element", "gather_H", "gather_f", "exchange", "fused")
 
 
 _vp, _i64, _i32, _d = C.c_void_p, C.c_int64, C.c_int32, C.c_double
@@ -352,11 +355,11 @@ class Context:
         _check(lib().tlfea_set_timing(self.handle, int(enable)))
 
     def timing_report(self):
-        """{kind: (launches, total_ms)} for kinds element / gather_H / gather_f / exchange."""
-        cnt = np.zeros(4, np.int64)
-        ms = np.zeros(4, np.float64)
+        """{kind: (launches, total_ms)} for kinds element / gather_H / gather_f / exchange / fused."""
+        cnt = np.zeros(N_TIMING, np.int64)
+        ms = np.zeros(N_TIMING, np.float64)
         _check(lib().tlfea_timing_report(self.handle, _ptr(cnt), _ptr(ms)))
-        return {k: (int(cnt[i]), float(ms[i])) for i, k in enumerate(("element", "gather_H", "gather_f", "exchange"))}
+        return {k: (int(cnt[i]), float(ms[i])) for i, k in enumerate(TIMING_KINDS)}
 
     def sync_status(self):
         e, q = C.c_int64(0), C.c_int32(0)

@@ -114,7 +114,7 @@ tlfea_status tlfea_info(tlfea_ctx ctx, tlfea_info_t* o) {
   o->nranks = c.nranks;
   o->device_bytes = c.device_bytes;
   o->n_geometry_classes = c.n_cls;
-  o->reserved = 0;
+  o->fused_eval = fused_available(&c) ? 1 : 0;
   return TLFEA_OK;
 }
 
@@ -226,6 +226,10 @@ tlfea_status tlfea_eval(tlfea_ctx ctx, const double* x, const double* v, const d
   TRY(use_device(c));
   const cudaStream_t s = as_stream(stream);
   c.last_stream = s;
+  if (fused_available(&c)) {
+    TIMED(4, launch_fused_eval(&c, x, v, v_n, f_ext, h, g_out, H_out, f_int_out, s));
+    return TLFEA_OK;
+  }
   TIMED(0, launch_element_kernel(&c, x, v, true, s));
   TIMED(1, launch_gather_H(&c, h, H_out, s));
   TIMED(2, launch_gather_f(&c, v, v_n, f_ext, h, g_out, f_int_out, false, s));
@@ -430,7 +434,7 @@ tlfea_status tlfea_timing_report(tlfea_ctx ctx, int64_t* counts, double* ms) {
   CTX_OR_FAIL(ctx);
   Context& c = ctx->c;
   TRY(use_device(c));
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < TLFEA_N_TIMING; ++k) {
     if (counts) counts[k] = 0;
     if (ms) ms[k] = 0.0;
   }
@@ -438,7 +442,7 @@ tlfea_status tlfea_timing_report(tlfea_ctx ctx, int64_t* counts, double* ms) {
     TL_CUDA(cudaEventSynchronize(t.stop));
     float el = 0.f;
     TL_CUDA(cudaEventElapsedTime(&el, t.start, t.stop));
-    if (t.kind >= 0 && t.kind < 4) {
+    if (t.kind >= 0 && t.kind < TLFEA_N_TIMING) {
       if (counts) counts[t.kind] += 1;
       if (ms) ms[t.kind] += el;
     }

@@ -44,6 +44,11 @@ inline int n_qp_of(int quadrature) {
 }
 // number of upper-triangular 3x3 blocks (a <= b) of the element matrix
 inline int n_ublk_of(int nen) { return nen * (nen + 1) / 2; }
+// element-kernel CTA tile: kElWarps warps, 3 T10 elements or 1 ANCF element per warp
+constexpr int kElWarps = 4;
+inline int el_per_tile(int element) { return kElWarps * (element == TLFEA_T10 ? 3 : 1); }
+// gather CTA: 4 warps of 32 units (H) / 128 threads (f)
+constexpr int kGatherThreads = 128;
 
 // Packed contribution entry of the H gather: element (local id) << 8 | a << 4 | b
 __host__ __device__ inline uint32_t pack_eab(uint32_t e, uint32_t a, uint32_t b) {
@@ -120,6 +125,16 @@ struct Context {
   int32_t* u_offT = nullptr;      // [n_units] H offset of (J,I) or -1
   int32_t* u_deg = nullptr;       // [n_units] deg(I) | deg(J) << 16
   double* u_m = nullptr;          // [n_units] M_IJ
+  // fused persistent eval (single rank, class tables, gather-sorted scratch):
+  // one launch works through a list of element items (kElTile elements x
+  // fz_etiles) and H / f gather items, each gather item waiting on per-chunk
+  // completion counters of the element chunks it reads (setup.cu build_fused_plan)
+  int64_t fz_items = 0, fz_nE = 0, fz_nG = 0, fz_nF = 0;
+  int fz_chunks = 0, fz_etiles = 0, fz_chunk_items = 0, fz_gunits = 0, fz_fdofs = 0;
+  uint32_t* fz_list = nullptr;    // [fz_items] type << 30 | index (0 element, 1 H gather, 2 f gather)
+  int32_t* fz_lo = nullptr;       // [fz_nG + fz_nF] first element chunk read by a gather item
+  int32_t* fz_hi = nullptr;       // [fz_nG + fz_nF] last element chunk read
+  uint32_t* fz_sync = nullptr;    // [1 + fz_chunks]: work ticket, completed element items per chunk
   double* Kscr = nullptr;         // [n_el][n_ublk][9]
   double* fscr = nullptr;         // [n_el][nen][3]
   unsigned long long* err_flag = nullptr;  // min over (e*64+q) with det F <= 0 (MR)
@@ -184,6 +199,11 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
 tlfea_status launch_element_kernel(Context* c, const double* x, const double* v,
                                    bool tangent, cudaStream_t s);
 tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s);
+// fused element + H + f/g eval (one persistent launch); returns TLFEA_E_INVALID
+// without launching when the context has no fused plan
+bool fused_available(const Context* c);
+tlfea_status launch_fused_eval(Context* c, const double* x, const double* v, const double* vn, const double* fext,
+                               double h, double* g, double* H, double* fint, cudaStream_t s);
 tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, const double* fext,
                              double h, double* g, double* fint, bool partial_only,
                              cudaStream_t s);

@@ -22,6 +22,7 @@
 //   writes h K + M/h to (I,J) and its transpose to (J,I); every H value is
 //   written exactly once and every scratch block is read exactly once.
 #include "common.cuh"
+#include "fgather.cuh"
 #include "material.cuh"
 
 namespace tlfea {
@@ -45,7 +46,7 @@ __host__ __device__ __forceinline__ int ublk(int n, int a, int b) {  // a <= b
   return a * n - (a * (a - 1)) / 2 + (b - a);
 }
 
-constexpr int kWarps = 4;  // warps per CTA
+constexpr int kWarps = kElWarps;  // warps per CTA
 constexpr int kLD = 33;    // padded lane stride of the per-warp shared tables
 
 // Blocks owned by a lane: index j -> partner b (-1 when none).
@@ -61,29 +62,87 @@ __device__ __forceinline__ int partner(int a, int half, int j) {
   }
 }
 
-#ifndef TLFEA_T10_MINB
-#define TLFEA_T10_MINB 3  // T10 SVK: 3 CTAs of 4 warps per SM (<= 168 registers)
+// Block passes per lane. One pass keeps all of a lane's upper blocks live
+// (T10: 6 x 9 fp64 = 108 registers) and caps occupancy at 3 CTAs with
+// spills at the 168-register bound; two passes redo the per-q kinematics but
+// halve the accumulators, so T10 SVK fits 4 CTAs (128 registers) without
+// spills — measured faster (config 3: 11.2 vs 11.4-12.8 ms). Mooney-Rivlin
+// and ANCF measured slower with two passes (their per-q work is larger).
+#ifndef TLFEA_T10_SVK_NPASS
+#define TLFEA_T10_SVK_NPASS 2
 #endif
-
-#ifndef TLFEA_NPASS
-#define TLFEA_NPASS 1  // block passes per lane (2 halves the live accumulators)
+#ifndef TLFEA_T10_MINB
+#define TLFEA_T10_MINB 3  // T10 SVK, one pass: 3 CTAs of 4 warps per SM (<= 168 registers)
 #endif
 #ifndef TLFEA_T10_MINB2P
-#define TLFEA_T10_MINB2P 4
+#define TLFEA_T10_MINB2P 4  // T10 SVK, two passes: 4 CTAs (<= 128 registers)
 #endif
+
+template <int ELEM, int MODEL>
+__host__ __device__ constexpr int el_npass() {
+  return (ELEM == 0 && MODEL == 0) ? TLFEA_T10_SVK_NPASS : 1;
+}
 
 template <int ELEM, int MODEL, int NPASS>
 __host__ __device__ constexpr int el_minb() {
   return (ELEM == 0 && MODEL == 0) ? (NPASS == 1 ? TLFEA_T10_MINB : TLFEA_T10_MINB2P) : (NPASS == 1 ? 2 : 3);
 }
 
-template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS>
-__global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>())
-    k_element(int64_t n_el, const int32_t* __restrict__ conn, const double* __restrict__ gradN,
-              const double* __restrict__ J0w, const uint8_t* __restrict__ cls, const double* __restrict__ cls_tab,
-              int n_cls, const double* __restrict__ x, const double* __restrict__ v, MatDev mat,
-              double* __restrict__ fscr, double* __restrict__ Kscr, const int32_t* __restrict__ dest,
-              const int32_t* __restrict__ fdest, unsigned long long* __restrict__ err) {
+// Element arguments shared by k_element and the fused persistent kernel.
+struct ElArgs {
+  int64_t n_el;
+  const int32_t* conn;
+  const double* gradN;
+  const double* J0w;
+  const uint8_t* cls;
+  const double* cls_tab;
+  int n_cls;
+  const double* x;
+  const double* v;
+  MatDev mat;
+  double* fscr;
+  double* Kscr;
+  const int32_t* dest;
+  const int32_t* fdest;
+  unsigned long long* err;
+  int cta_tiles;  // k_element_pf: consecutive tiles per CTA
+};
+
+__device__ __forceinline__ void pf_cp4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void pf_cp8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void pf_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+#ifndef TLFEA_DEST_ASYNC
+#define TLFEA_DEST_ASYNC 1  // k_element: gather-sorted destinations via cp.async at group start
+#endif
+
+// Per-warp prefetch buffer of one element group (EPW elements): the inputs
+// k_element_pf moves into shared memory with cp.async one group ahead.
+template <int ELEM, bool KV>
+struct WarpIn {
+  static constexpr int NEN = Geo<ELEM>::NEN, EPW = Geo<ELEM>::EPW, NUB = Geo<ELEM>::NUB;
+  double x[EPW * NEN * 3];
+  double v[KV ? EPW * NEN * 3 : 1];
+  int32_t conn[EPW * NEN];
+  int32_t dest[EPW * NUB];
+  int32_t fdest[EPW * NEN];
+};
+
+// One warp group (EPW elements of warp `grp`) of Stage 1 + Stage 2. PF: the
+// element's coordinates, destinations and class come from the prefetched
+// shared-memory buffer `in` (class id `ce_in`) instead of global memory.
+// DA: the group's gather-sorted destinations are copied to shared memory with
+// cp.async when the group starts and consumed by the store phase, so the
+// scattered index loads never stall the warp.
+template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS, bool PF = false, bool DA = false>
+__device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab,
+                                              const WarpIn<ELEM, KV>* in = nullptr, int ce_in = 0) {
   using G = Geo<ELEM>;
   constexpr int NEN = G::NEN, GROUP = G::GROUP, EPW = G::EPW, NUB = G::NUB, NB = G::NB;
   constexpr int NC = KV ? 18 : 9;            // reduced components (F, Fdot)
@@ -93,34 +152,58 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>())
   __shared__ double s_F[kWarps][EPW][NC];
   __shared__ double s_node[kWarps][TAN ? ND : 1][kLD];
   __shared__ double s_C[kWarps][EPW][MODEL == 1 && TAN ? 36 : 1];
-  extern __shared__ double s_tab[];          // CLS: [n_cls][NQ][TABW]
-
-  if (CLS) {
-    const int tot = n_cls * NQ * TABW;
-    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_tab[t] = cls_tab[t];
-    __syncthreads();
-  }
+  const int64_t n_el = A.n_el;
+  const int32_t* __restrict__ conn = A.conn;
+  const double* __restrict__ gradN = A.gradN;
+  const double* __restrict__ J0w = A.J0w;
+  const uint8_t* __restrict__ cls = A.cls;
+  const double* __restrict__ x = A.x;
+  const double* __restrict__ v = A.v;
+  const MatDev& mat = A.mat;
+  double* __restrict__ fscr = A.fscr;
+  double* __restrict__ Kscr = A.Kscr;
+  const int32_t* __restrict__ dest = A.dest;
+  const int32_t* __restrict__ fdest = A.fdest;
+  unsigned long long* __restrict__ err = A.err;
 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const bool lane_active = ELEM == 0 ? (lane < EPW * GROUP) : true;
   const int g = (ELEM == 0 && lane_active) ? lane / GROUP : 0;
   const int a = ELEM == 0 ? (lane_active ? lane % GROUP : 0) : (lane & 15);
   const int half = ELEM == 0 ? 0 : (lane >> 4);
-  const int64_t e = ((int64_t)blockIdx.x * kWarps + wib) * EPW + g;
+  const int64_t e = grp * EPW + g;
   const bool valid = lane_active && e < n_el;
   const int gbase = g * GROUP;
+  // (SVK only: the Mooney-Rivlin tables already fill the 48 KB of static shared memory)
+  constexpr bool DAX = DA && TAN && !PF && MODEL == 0;
+  __shared__ int32_t s_dst[kWarps][DAX ? EPW * NUB : 1];
+  if (DAX && dest && !mat.dbg_nowrite) {
+    const int64_t e0 = grp * EPW, lim = (n_el - e0) * NUB;
+    for (int t = lane; t < EPW * NUB; t += 32)
+      if (t < lim) pf_cp4(&s_dst[wib][t], dest + e0 * NUB + t);
+  }
 
   double xa[3] = {0, 0, 0}, va[3] = {0, 0, 0};
   int ce = 0;
   if (valid) {
-    const int64_t I = conn[e * NEN + a];
+    if (PF) {
 #pragma unroll
-    for (int i = 0; i < 3; ++i) xa[i] = x[3 * I + i];
-    if (KV) {
+      for (int i = 0; i < 3; ++i) xa[i] = in->x[(g * NEN + a) * 3 + i];
+      if (KV) {
 #pragma unroll
-      for (int i = 0; i < 3; ++i) va[i] = v[3 * I + i];
+        for (int i = 0; i < 3; ++i) va[i] = in->v[(g * NEN + a) * 3 + i];
+      }
+      ce = (ce_in >> (8 * g)) & 0xff;
+    } else {
+      const int64_t I = conn[e * NEN + a];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) xa[i] = x[3 * I + i];
+      if (KV) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) va[i] = v[3 * I + i];
+      }
+      if (CLS) ce = cls[e];
     }
-    if (CLS) ce = cls[e];
   }
   double fa[3] = {0, 0, 0};
   // NPASS > 1 splits each lane's blocks over sequential passes that redo the
@@ -330,7 +413,8 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>())
   }
 
   if (valid && pass == 0 && (ELEM == 0 || half == 0)) {
-    double* fo = fscr + (fdest ? (int64_t)fdest[e * NEN + a] : e * NEN + a) * 3;
+    const int64_t fp = fdest ? (int64_t)(PF ? in->fdest[g * NEN + a] : fdest[e * NEN + a]) : e * NEN + a;
+    double* fo = fscr + fp * 3;
     fo[0] = fa[0];
     fo[1] = fa[1];
     fo[2] = fa[2];
@@ -342,21 +426,29 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>())
   // memory and the warp writes the round's blocks as consecutive doubles, so a
   // warp store covers 3-4 whole blocks.
   if (TAN && !mat.dbg_nowrite) {
-    __shared__ int64_t s_pos[kWarps][32];
+    __shared__ int32_t s_pos[kWarps][32];  // block position (< 2^31, checked at setup)
+    // store mapping: lane = 9 bi + r writes entry r of block 3 it + bi
+    constexpr int NLB = ELEM == 0 ? EPW * GROUP : 32;  // lanes holding blocks
+    constexpr int NIT = (NLB + 2) / 3;
+    const int bi = lane / 9, rr = lane - 9 * (lane / 9);
+    if (DAX && dest) {
+      pf_wait();
+      __syncwarp();
+    }
 #pragma unroll
     for (int jj = 0; jj < NBP; ++jj) {
       const int j = pass * NBP + jj;
       const int b = (valid && j < NB) ? partner<ELEM>(a, half, j) : -1;
-      int64_t pos = -1;
+      int32_t pos = -1;
       if (b >= 0) {
         const double* Kj = K[jj];
         const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
         // element-major: store the upper block K_{min,max}; gather-sorted: the
         // orientation the receiving unit needs (dest low bit)
         bool tr = a > b;
-        pos = e * NUB + ub;
+        pos = (int32_t)(e * NUB + ub);
         if (dest) {
-          const int32_t d = dest[e * NUB + ub];
+          const int32_t d = PF ? in->dest[g * NUB + ub] : DAX ? s_dst[wib][g * NUB + ub] : dest[e * NUB + ub];
           pos = d >> 1;
           tr = tr != ((d & 1) != 0);
         }
@@ -368,16 +460,131 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>())
       s_pos[wib][lane] = pos;
       __syncwarp();
 #pragma unroll
-      for (int it = 0; it < 9; ++it) {
-        const int t = lane + 32 * it;  // value t of the round: block t / 9, entry t % 9
-        const int blk = t / 9, r = t - 9 * (t / 9);
-        const int64_t p = s_pos[wib][blk];
-        if (p >= 0) Kscr[p * 9 + r] = s_part[wib][r][blk];
+      for (int it = 0; it < NIT; ++it) {
+        const int blk = 3 * it + bi;
+        if (lane < 27 && blk < NLB) {
+          const int32_t p = s_pos[wib][blk];
+          if (p >= 0) Kscr[(int64_t)p * 9 + rr] = s_part[wib][rr][blk];
+        }
       }
       __syncwarp();
     }
   }
   }  // pass
+}
+
+template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS>
+__global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>()) k_element(ElArgs A) {
+  extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
+  if (CLS) {
+    const int tot = A.n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1);
+    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_tab[t] = A.cls_tab[t];
+    __syncthreads();
+  }
+  // A.cta_tiles consecutive tiles per CTA (class tables staged once)
+  const int64_t t0 = (int64_t)blockIdx.x * A.cta_tiles;
+#pragma unroll 1
+  for (int k = 0; k < A.cta_tiles; ++k)
+    element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, false, TLFEA_DEST_ASYNC != 0>(
+        (t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
+}
+
+// prefetch stage 1: the connectivity of group grp
+template <int ELEM, bool KV>
+__device__ __forceinline__ void pf_conn(WarpIn<ELEM, KV>& B, int64_t grp, const ElArgs& A) {
+  using W = WarpIn<ELEM, KV>;
+  const int lane = threadIdx.x & 31;
+  const int64_t base = grp * W::EPW * W::NEN, lim = A.n_el * W::NEN;
+  for (int t = lane; t < W::EPW * W::NEN; t += 32)
+    if (base + t < lim) pf_cp4(&B.conn[t], A.conn + base + t);
+}
+// prefetch stage 2 (conn of grp already in B): coordinates (velocities) of
+// its nodes, the gather-sorted destinations of its blocks and forces
+template <int ELEM, bool KV, bool TAN>
+__device__ __forceinline__ void pf_rest(WarpIn<ELEM, KV>& B, int64_t grp, const ElArgs& A) {
+  using W = WarpIn<ELEM, KV>;
+  const int lane = threadIdx.x & 31;
+  const int64_t e0 = grp * W::EPW;
+  for (int t = lane; t < W::EPW * W::NEN; t += 32) {
+    if (e0 + t / W::NEN >= A.n_el) continue;
+    const int64_t I = B.conn[t];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) pf_cp8(&B.x[3 * t + i], A.x + 3 * I + i);
+    if (KV) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) pf_cp8(&B.v[3 * t + i], A.v + 3 * I + i);
+    }
+    if (A.fdest) pf_cp4(&B.fdest[t], A.fdest + e0 * W::NEN + t);
+  }
+  if (TAN && A.dest) {
+    const int64_t lim = (A.n_el - e0) * W::NUB;
+    for (int t = lane; t < W::EPW * W::NUB; t += 32)
+      if (t < lim) pf_cp4(&B.dest[t], A.dest + e0 * W::NUB + t);
+  }
+}
+// class ids of the group's elements packed one byte each (plain load, one group ahead)
+template <int ELEM>
+__device__ __forceinline__ int pf_cls(int64_t grp, const ElArgs& A) {
+  constexpr int EPW = Geo<ELEM>::EPW;
+  int r = 0;
+#pragma unroll
+  for (int g = 0; g < EPW; ++g) {
+    const int64_t e = grp * EPW + g;
+    if (e < A.n_el) r |= (int)A.cls[e] << (8 * g);
+  }
+  return r;
+}
+
+// Persistent element kernel (geometry classes): one CTA per resident slot,
+// the class tables staged once per CTA, and each warp walks its element
+// groups with a two-deep cp.async pipeline — while group i is computed, the
+// coordinates / destinations of group i+1 and the connectivity of group i+2
+// are in flight, so the dependent conn -> x and dest loads never stall it.
+template <int ELEM, int NQ, int MODEL, bool KV, bool TAN>
+__global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, 1>()) k_element_pf(ElArgs A) {
+  using W = WarpIn<ELEM, KV>;
+  // dynamic shared memory: [prefetch buffers kWarps x 2][class tables [n_cls][NQ][3 NEN + 1]]
+  extern __shared__ __align__(16) double s_dyn[];
+  W(*s_in)[2] = reinterpret_cast<W(*)[2]>(s_dyn);
+  double* s_tab = s_dyn + kWarps * 2 * sizeof(W) / sizeof(double);
+  static_assert(sizeof(W) % sizeof(double) == 0, "class tables stay 8-byte aligned");
+  {
+    const int tot = A.n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1);
+    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_tab[t] = A.cls_tab[t];
+    __syncthreads();
+  }
+  const int wib = threadIdx.x >> 5;
+  // CTA b covers the A.cta_tiles consecutive tiles starting at b * cta_tiles;
+  // CTAs are dispatched in order, so the elements in flight stay a compact
+  // window (the gather-sorted scratch stores of neighbouring elements then
+  // merge into full sectors in L2 instead of forcing DRAM fills)
+  const int64_t n_grp = min((A.n_el + W::EPW - 1) / W::EPW, ((int64_t)blockIdx.x + 1) * A.cta_tiles * kWarps);
+  const int64_t stride = kWarps;
+  int64_t grp = (int64_t)blockIdx.x * A.cta_tiles * kWarps + wib;
+  W* B = s_in[wib];
+  int ce_cur = 0, ce_next = 0;
+  if (grp < n_grp) {
+    pf_conn<ELEM, KV>(B[0], grp, A);
+    pf_wait();
+    __syncwarp();
+    pf_rest<ELEM, KV, TAN>(B[0], grp, A);
+    ce_cur = pf_cls<ELEM>(grp, A);
+  }
+  if (grp + stride < n_grp) pf_conn<ELEM, KV>(B[1], grp + stride, A);
+#pragma unroll 1
+  for (int i = 0; grp < n_grp; ++i, grp += stride) {
+    pf_wait();
+    __syncwarp();
+    const int cur = i & 1, nxt = cur ^ 1;
+    if (grp + stride < n_grp) {
+      pf_rest<ELEM, KV, TAN>(B[nxt], grp + stride, A);
+      ce_next = pf_cls<ELEM>(grp + stride, A);
+    }
+    if (grp + 2 * stride < n_grp) pf_conn<ELEM, KV>(B[cur], grp + 2 * stride, A);
+    element_group<ELEM, NQ, MODEL, KV, TAN, true, 1, true>(grp, A, s_tab, &B[cur], ce_cur);
+    ce_cur = ce_next;
+  }
+  pf_wait();
 }
 
 // ------------------------------------------------ FP64 tensor-core variant
@@ -888,21 +1095,35 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
-__global__ void __launch_bounds__(kG3Warps * 32)
-    k_gather_units_v3(int64_t n_units, const int32_t* __restrict__ unit_ptr, const int32_t* __restrict__ u_off,
-                      const int32_t* __restrict__ u_offT, const int32_t* __restrict__ u_deg,
-                      const double* __restrict__ u_m, const double* __restrict__ Kscr, double h,
-                      double* __restrict__ H) {
-  __shared__ __align__(16) double s_buf[kG3Warps][2][kG3Buf];
-  __shared__ __align__(8) uint64_t s_bar[kG3Warps][2];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  if (lane == 0) {
-    mbar_init(&s_bar[wib][0], 1);
-    mbar_init(&s_bar[wib][1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncwarp();
-  const int64_t u0 = ((int64_t)blockIdx.x * kG3Warps + wib) * 32;
+struct GatherArgs {
+  int64_t n_units;
+  const int32_t* unit_ptr;
+  const int32_t* u_off;
+  const int32_t* u_offT;
+  const int32_t* u_deg;
+  const double* u_m;
+  const double* Kscr;
+  double h;
+  double* H;
+};
+
+// Per-warp TMA staging: two windows and their mbarriers. `wk` counts the
+// windows this warp has consumed so far (buffer wk & 1, phase (wk >> 1) & 1),
+// so the barriers can be reused across work items of a persistent kernel.
+struct G3Warp {
+  double* buf[2];
+  uint64_t* bar;
+  uint32_t wk;
+};
+
+// The 32 consecutive units u0 .. u0+31 on one warp.
+__device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& A, G3Warp& W) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_units = A.n_units;
+  const int32_t* __restrict__ unit_ptr = A.unit_ptr;
+  const double* __restrict__ Kscr = A.Kscr;
+  const double h = A.h;
+  double* __restrict__ H = A.H;
   if (u0 >= n_units) return;
   const int64_t u = u0 + lane;
   const bool valid = u < n_units;
@@ -913,17 +1134,19 @@ __global__ void __launch_bounds__(kG3Warps * 32)
   if (valid) {
     my0 = unit_ptr[u];
     my1 = unit_ptr[u + 1];
-    off = u_off[u];
-    offT = u_offT[u];
-    dg = u_deg[u];
-    m = u_m[u];
+    off = A.u_off[u];
+    offT = A.u_offT[u];
+    dg = A.u_deg[u];
+    m = A.u_m[u];
   }
   const int nwin = (int)((P1 - P0 + kG3WB - 1) / kG3WB);
+  const uint32_t wk0 = W.wk;
   auto issue = [&](int k) {
     const int64_t w0 = P0 + (int64_t)k * kG3WB, w1 = min(w0 + (int64_t)kG3WB, P1);
     const uintptr_t a = (uintptr_t)(Kscr + w0 * 9) & ~(uintptr_t)15;
     const uintptr_t b = ((uintptr_t)(Kscr + w1 * 9) + 15) & ~(uintptr_t)15;
-    bulk_load(&s_buf[wib][k & 1][0], (const void*)a, (unsigned)(b - a), &s_bar[wib][k & 1]);
+    const uint32_t wi = wk0 + k;
+    bulk_load(W.buf[wi & 1], (const void*)a, (unsigned)(b - a), &W.bar[wi & 1]);
   };
   if (lane == 0 && nwin > 0) issue(0);
   double acc[9];
@@ -931,10 +1154,11 @@ __global__ void __launch_bounds__(kG3Warps * 32)
   for (int r = 0; r < 9; ++r) acc[r] = 0.0;
   for (int k = 0; k < nwin; ++k) {
     if (lane == 0 && k + 1 < nwin) issue(k + 1);
-    mbar_wait(&s_bar[wib][k & 1], (unsigned)((k >> 1) & 1));
+    const uint32_t wi = wk0 + k;
+    mbar_wait(&W.bar[wi & 1], (wi >> 1) & 1);
     const int64_t w0 = P0 + (int64_t)k * kG3WB, w1 = min(w0 + (int64_t)kG3WB, P1);
     const int delta = (int)(((uintptr_t)(Kscr + w0 * 9) & 15) >> 3);  // 0 or 1 double
-    const double* buf = &s_buf[wib][k & 1][delta];
+    const double* buf = W.buf[wi & 1] + delta;
     const int64_t a0 = max((int64_t)my0, w0), a1 = min((int64_t)my1, w1);
     for (int64_t t = a0; t < a1; ++t) {
       const double* sb = buf + (t - w0) * 9;
@@ -943,6 +1167,7 @@ __global__ void __launch_bounds__(kG3Warps * 32)
     }
     __syncwarp();
   }
+  W.wk = wk0 + nwin;
   if (!valid) return;
   const double mh = m / h;
   const int deg = dg & 0xffff, degT = dg >> 16;
@@ -957,6 +1182,132 @@ __global__ void __launch_bounds__(kG3Warps * 32)
     for (int d = 0; d < 3; ++d)
 #pragma unroll
       for (int f = 0; f < 3; ++f) o2[3 * d * degT + f] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
+  }
+}
+
+__device__ __forceinline__ void g3_init(double (*s_buf)[2][kG3Buf], uint64_t (*s_bar)[2], G3Warp& W) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (lane == 0) {
+    mbar_init(&s_bar[wib][0], 1);
+    mbar_init(&s_bar[wib][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  W.buf[0] = s_buf[wib][0];
+  W.buf[1] = s_buf[wib][1];
+  W.bar = s_bar[wib];
+  W.wk = 0;
+}
+
+__global__ void __launch_bounds__(kG3Warps * 32) k_gather_units_v3(GatherArgs A) {
+  __shared__ __align__(16) double s_buf[kG3Warps][2][kG3Buf];
+  __shared__ __align__(8) uint64_t s_bar[kG3Warps][2];
+  G3Warp W;
+  g3_init(s_buf, s_bar, W);
+  gather_units_warp(((int64_t)blockIdx.x * kG3Warps + (threadIdx.x >> 5)) * 32, A, W);
+}
+
+// ------------------------------------------------- fused persistent eval
+// One launch for the whole tangent eval (Stage 1 + 2, H gather, f / g):
+// CTAs take work items from a global ticket in list order. Element items
+// (fz_etiles CTA tiles) never wait; when one finishes it publishes its
+// chunk's completion counter (release). A gather item (512 units of H or
+// 1024 owned DOFs of f / g) first waits (acquire) until every element chunk
+// it reads is complete — the list places it a chunk after the last of them,
+// so the wait is normally already satisfied — and then reads the scratch
+// while it is still in L2. Items are handed out in list order and element
+// items never block, so every wait ends (no deadlock for any grid size).
+// Each H / f value is still summed by one thread in ascending element order:
+// the result is bitwise identical to the three-kernel path.
+struct FusedArgs {
+  ElArgs el;
+  GatherArgs ga;
+  FArgs fa;
+  const uint32_t* list;
+  int64_t n_items, nE, nG;
+  const int32_t* lo;
+  const int32_t* hi;
+  uint32_t* sync;  // [0] ticket, [1 + c] completed element items of chunk c
+  int etiles, chunk_items, gunits, fdofs;
+  int dbg;  // diagnostics (TLFEA_FZ_DBG): 1 skip gather items, 2 skip element work
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int ELEM, int NQ, int MODEL, bool KV>
+__global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, 1>()) k_fused(FusedArgs P) {
+  static_assert(kG3Warps == kWarps, "the fused CTA runs both item kinds");
+  // dynamic shared memory: [TMA windows kG3Warps x 2 x kG3Buf][class tables]
+  extern __shared__ __align__(16) double s_dyn[];
+  double(*s_buf)[2][kG3Buf] = reinterpret_cast<double(*)[2][kG3Buf]>(s_dyn);
+  double* s_tab = s_dyn + kG3Warps * 2 * kG3Buf;  // [n_cls][NQ][3 NEN + 1]
+  __shared__ __align__(8) uint64_t s_bar[kG3Warps][2];
+  __shared__ uint32_t s_item[2];
+  {
+    const int tot = P.el.n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1);
+    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_tab[t] = P.el.cls_tab[t];
+  }
+  G3Warp W;
+  g3_init(s_buf, s_bar, W);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint32_t* ticket = P.sync;
+  uint32_t* done = P.sync + 1;
+#pragma unroll 1
+  for (int it = 0;; ++it) {
+    if (threadIdx.x == 0) s_item[it & 1] = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t idx = s_item[it & 1];
+    if (idx >= P.n_items) break;
+    const uint32_t item = __ldg(P.list + idx);
+    const uint32_t type = item >> 30, k = item & 0x3fffffffu;
+    if (type == 0) {
+      const int64_t t0 = (int64_t)k * P.etiles;
+      if (!(P.dbg & 2)) {
+#pragma unroll 1
+        for (int j = 0; j < P.etiles; ++j)
+          element_group<ELEM, NQ, MODEL, KV, true, true, 1>((t0 + j) * kWarps + wib, P.el, s_tab);
+      }
+      // publish: the CTA's stores -> barrier -> one gpu-scope release by thread 0
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        red_release_add(done + k / P.chunk_items, 1u);
+      }
+    } else if (!(P.dbg & 1)) {
+      const int64_t gi = type == 1 ? (int64_t)k : P.nG + k;
+      const int c0 = P.lo[gi], c1 = P.hi[gi];
+      if (wib == 0) {
+        for (int c = c0 + lane; c <= c1; c += 32) {
+          const uint32_t need = (uint32_t)min((int64_t)P.chunk_items, P.nE - (int64_t)c * P.chunk_items);
+          while (ld_acquire_u32(done + c) < need) __nanosleep(100);
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      if (type == 1) {
+        // scratch written by other SMs through the generic proxy, read here by TMA
+        if (lane == 0) asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        __syncwarp();
+        const int64_t ub = (int64_t)k * P.gunits;
+#pragma unroll 1
+        for (int r = 0; r < P.gunits / (32 * kWarps); ++r) gather_units_warp(ub + (r * kWarps + wib) * 32, P.ga, W);
+      } else {
+        const int64_t t0 = (int64_t)k * P.fdofs, nd = 3 * P.fa.n_own;
+#pragma unroll 1
+        for (int r = 0; r < P.fdofs / (32 * kWarps); ++r) {
+          const int64_t t = t0 + r * (32 * kWarps) + threadIdx.x;
+          if (t < nd) gather_f_dof_one(t, P.fa);
+        }
+      }
+    }
   }
 }
 
@@ -975,6 +1326,26 @@ static bool use_tc() {
   }
   return v == 1;
 }
+// persistent prefetching element kernel (k_element_pf) for class-table
+// contexts; TLFEA_PF=0 selects the one-tile-per-CTA k_element (A/B).
+// tiles per CTA of the prefetching kernel; TLFEA_PF=0 selects k_element
+static int pf_tiles() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TLFEA_PF");
+    v = (s && s[0]) ? std::max(0, atoi(s)) : 0;
+  }
+  return v;
+}
+// tiles per CTA of k_element with class tables (TLFEA_EL_TILES)
+static int el_cta_tiles() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("TLFEA_EL_TILES");
+    v = (s && s[0]) ? std::max(1, atoi(s)) : 1;
+  }
+  return v;
+}
 static int dbg_nowrite() {
   static int v = -1;
   if (v < 0) {
@@ -982,6 +1353,27 @@ static int dbg_nowrite() {
     v = (s && s[0] == '1') ? 1 : 0;
   }
   return v;
+}
+
+static ElArgs el_args(const Context* c, const double* x, const double* v) {
+  ElArgs A;
+  A.n_el = c->n_el;
+  A.conn = c->conn;
+  A.gradN = c->gradN;
+  A.J0w = c->J0w;
+  A.cls = c->cls;
+  A.cls_tab = c->cls_tab;
+  A.n_cls = c->n_cls;
+  A.x = x;
+  A.v = v;
+  A.mat = c->mat;
+  A.fscr = c->fscr;
+  A.Kscr = c->Kscr;
+  A.dest = c->dest;
+  A.fdest = c->fdest;
+  A.err = c->err_flag;
+  A.cta_tiles = 1;
+  return A;
 }
 
 template <int ELEM, int NQ, int MODEL, bool KV, bool TAN>
@@ -1009,21 +1401,36 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
   const unsigned grid = (unsigned)((c->n_el + per_cta - 1) / per_cta);
   if (grid == 0) return TLFEA_OK;
   c->mat.dbg_nowrite = dbg_nowrite();
+  ElArgs A = el_args(c, x, v);
+  if (c->n_cls > 0 && pf_tiles() > 0) {
+    auto kern = k_element_pf<ELEM, NQ, MODEL, KV, TAN>;
+    const size_t smem = kWarps * 2 * sizeof(WarpIn<ELEM, KV>) + sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+      TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      smem_set = smem;
+    }
+    A.cta_tiles = pf_tiles();
+    const unsigned g = (unsigned)((grid + A.cta_tiles - 1) / A.cta_tiles);
+    kern<<<g, kWarps * 32, smem, s>>>(A);
+    TL_CHECK_LAUNCH();
+    return TLFEA_OK;
+  }
   if (c->n_cls > 0) {
     const size_t smem = sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
     static size_t smem_set = 0;  // per template instantiation
     if (smem > smem_set) {
-      TL_CUDA(cudaFuncSetAttribute(k_element<ELEM, NQ, MODEL, KV, TAN, true, TLFEA_NPASS>,
+      TL_CUDA(cudaFuncSetAttribute(k_element<ELEM, NQ, MODEL, KV, TAN, true, el_npass<ELEM, MODEL>()>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       smem_set = smem;
     }
-    k_element<ELEM, NQ, MODEL, KV, TAN, true, TLFEA_NPASS><<<grid, kWarps * 32, smem, s>>>(
-        c->n_el, c->conn, c->gradN, c->J0w, c->cls, c->cls_tab, c->n_cls, x, v, c->mat, c->fscr, c->Kscr,
-        c->dest, c->fdest, c->err_flag);
+    // several tiles per CTA amortize the class-table staging; the grid is
+    // still dispatched in element order (compact in-flight window)
+    A.cta_tiles = el_cta_tiles();
+    const unsigned g = (unsigned)((grid + A.cta_tiles - 1) / A.cta_tiles);
+    k_element<ELEM, NQ, MODEL, KV, TAN, true, el_npass<ELEM, MODEL>()><<<g, kWarps * 32, smem, s>>>(A);
   } else {
-    k_element<ELEM, NQ, MODEL, KV, TAN, false, TLFEA_NPASS><<<grid, kWarps * 32, 0, s>>>(
-        c->n_el, c->conn, c->gradN, c->J0w, c->cls, c->cls_tab, 0, x, v, c->mat, c->fscr, c->Kscr, c->dest,
-        c->fdest, c->err_flag);
+    k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>()><<<grid, kWarps * 32, 0, s>>>(A);
   }
   TL_CHECK_LAUNCH();
   return TLFEA_OK;
@@ -1051,12 +1458,107 @@ tlfea_status launch_element_kernel(Context* c, const double* x, const double* v,
   return launch_el_model<1, 48>(c, x, v, tangent, s);
 }
 
+static GatherArgs gather_args(const Context* c, double h, double* H) {
+  GatherArgs A;
+  A.n_units = c->n_units;
+  A.unit_ptr = c->unit_ptr;
+  A.u_off = c->u_off;
+  A.u_offT = c->u_offT;
+  A.u_deg = c->u_deg;
+  A.u_m = c->u_m;
+  A.Kscr = c->Kscr;
+  A.h = h;
+  A.H = H;
+  return A;
+}
+
+bool fused_available(const Context* c) { return c->fz_items > 0 && c->fz_list != nullptr; }
+
+template <int ELEM, int NQ, int MODEL, bool KV>
+static tlfea_status launch_fused_t(Context* c, const FusedArgs& P, cudaStream_t s) {
+  auto kern = k_fused<ELEM, NQ, MODEL, KV>;
+  static_assert((kG3Buf * sizeof(double)) % 16 == 0, "TMA windows stay 16-byte aligned");
+  const size_t smem =
+      sizeof(double) * ((size_t)kG3Warps * 2 * kG3Buf + (size_t)c->n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1));
+  static size_t smem_set = 0;
+  static int grid = 0;
+  if (smem > smem_set || grid == 0) {
+    TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
+    smem_set = std::max(smem, smem_set);
+    int per_sm = 0, n_sm = 0, dev = 0;
+    TL_CUDA(cudaGetDevice(&dev));
+    TL_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem_set));
+    grid = std::max(1, per_sm) * n_sm;
+  }
+  TL_CUDA(cudaMemsetAsync(c->fz_sync, 0, sizeof(uint32_t) * (1 + (size_t)c->fz_chunks), s));
+  kern<<<(unsigned)std::min<int64_t>(grid, c->fz_items), kWarps * 32, smem, s>>>(P);
+  TL_CHECK_LAUNCH();
+  return TLFEA_OK;
+}
+
+tlfea_status launch_fused_eval(Context* c, const double* x, const double* v, const double* vn, const double* fext,
+                               double h, double* g, double* H, double* fint, cudaStream_t s) {
+  if (!fused_available(c)) return fail(TLFEA_E_INVALID, "internal: no fused plan");
+  c->mat.dbg_nowrite = 0;
+  FusedArgs P;
+  P.el = el_args(c, x, v);
+  P.ga = gather_args(c, h, H);
+  P.fa.n_own = c->n_own;
+  P.fa.node_ptr = c->node_ptr;
+  P.fa.fscr = c->fscr;
+  P.fa.fpart_in = nullptr;
+  P.fa.own_nodes = c->own_nodes;
+  P.fa.rowptr_c = c->rowptr_c;
+  P.fa.cols_c = c->cols_c;
+  P.fa.M = c->M;
+  P.fa.fff = c->fff;
+  P.fa.v = v;
+  P.fa.vn = vn;
+  P.fa.fext = fext;
+  P.fa.h = h;
+  P.fa.mode = 0;
+  P.fa.g = g;
+  P.fa.fint = fint;
+  P.list = c->fz_list;
+  P.n_items = c->fz_items;
+  P.nE = c->fz_nE;
+  P.nG = c->fz_nG;
+  P.lo = c->fz_lo;
+  P.hi = c->fz_hi;
+  P.sync = c->fz_sync;
+  P.etiles = c->fz_etiles;
+  P.chunk_items = c->fz_chunk_items;
+  P.gunits = c->fz_gunits;
+  P.fdofs = c->fz_fdofs;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("TLFEA_FZ_DBG");
+      dbg = e ? atoi(e) : 0;
+    }
+    P.dbg = dbg;
+  }
+  const bool kv = c->mat.kv && v != nullptr;
+  const int model = c->mat.model == TLFEA_SVK ? 0 : 1;
+#define TL_FUSED(E, Q)                                                                     \
+  do {                                                                                     \
+    if (model == 0) return kv ? launch_fused_t<E, Q, 0, true>(c, P, s) : launch_fused_t<E, Q, 0, false>(c, P, s); \
+    return kv ? launch_fused_t<E, Q, 1, true>(c, P, s) : launch_fused_t<E, Q, 1, false>(c, P, s);                 \
+  } while (0)
+  if (c->element == TLFEA_T10) {
+    if (c->nq == 4) TL_FUSED(0, 4);
+    TL_FUSED(0, 5);
+  }
+  TL_FUSED(1, 48);
+#undef TL_FUSED
+}
+
 tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
   if (c->n_units == 0) return TLFEA_OK;
   if (c->u_off) {
     const int64_t per = (int64_t)kG3Warps * 32;
-    k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(
-        c->n_units, c->unit_ptr, c->u_off, c->u_offT, c->u_deg, c->u_m, c->Kscr, h, H);
+    k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(gather_args(c, h, H));
     TL_CHECK_LAUNCH();
     return TLFEA_OK;
   }

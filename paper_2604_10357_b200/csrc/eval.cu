@@ -17,6 +17,7 @@
 //   order through the precomputed inverse slot map, adds M/h and
 //   writes every H value exactly once — no floating-point atomics.
 #include "common.cuh"
+#include "fgather.cuh"
 #include "material.cuh"
 
 namespace tlfea {
@@ -29,36 +30,31 @@ static inline unsigned grid_for(int64_t n, int block) {
 // dependent index -> value loads of the mass row have 3x the parallelism;
 // the three threads of a node share its row through L1.
 // mode: 0 full (f + residual), 1 f only, 2 residual from fpart_in.
-__global__ void k_gather_f_dof(int64_t n_own, const int32_t* __restrict__ node_ptr, const double* __restrict__ fscr,
-                               const double* __restrict__ fpart_in, const int32_t* __restrict__ own_nodes,
-                               const int32_t* __restrict__ rowptr_c, const int32_t* __restrict__ cols_c,
-                               const double* __restrict__ M, const double* __restrict__ fff,
-                               const double* __restrict__ v, const double* __restrict__ vn,
-                               const double* __restrict__ fext, double h, int mode, double* __restrict__ g,
-                               double* __restrict__ fint) {
+__global__ void k_gather_f_dof(FArgs A) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= 3 * n_own) return;
-  const int64_t i = t / 3;
-  const int d = (int)(t - 3 * i);
-  double f = 0.0;
-  if (mode == 2) {
-    f = fpart_in[t];
-  } else {
-    const int32_t t0 = node_ptr[i], t1 = node_ptr[i + 1];
-#pragma unroll 4
-    for (int32_t s = t0; s < t1; ++s) f += fscr[3 * (int64_t)s + d];
-  }
-  if (fint) fint[t] = f;
-  if (mode == 1 || !g) return;
-  double m = 0.0;
-  const int32_t p0 = rowptr_c[i], p1 = rowptr_c[i + 1];
-#pragma unroll 4
-  for (int32_t p = p0; p < p1; ++p) {
-    const int64_t J = cols_c[p];
-    m += M[p] * (v[3 * J + d] - (vn ? vn[3 * J + d] : 0.0));
-  }
-  const int64_t I = own_nodes[i];
-  g[t] = m / h + f - (fext ? fext[3 * I + d] : 0.0) - fff[t];
+  if (t < 3 * A.n_own) gather_f_dof_one(t, A);
+}
+
+static FArgs f_args(const Context* c, const double* fscr, const double* fpart_in, const double* v, const double* vn,
+                    const double* fext, double h, int mode, double* g, double* fint) {
+  FArgs A;
+  A.n_own = c->n_own;
+  A.node_ptr = c->node_ptr;
+  A.fscr = fscr;
+  A.fpart_in = fpart_in;
+  A.own_nodes = c->own_nodes;
+  A.rowptr_c = c->rowptr_c;
+  A.cols_c = c->cols_c;
+  A.M = c->M;
+  A.fff = c->fff;
+  A.v = v;
+  A.vn = vn;
+  A.fext = fext;
+  A.h = h;
+  A.mode = mode;
+  A.g = g;
+  A.fint = fint;
+  return A;
 }
 
 // f_int and the residual g = (1/h) M (v - v_n) + f_int - f_ext - f_ff
@@ -287,9 +283,8 @@ tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, cons
     return TLFEA_OK;
   }
   if (c->fdest) {
-    k_gather_f_dof<<<grid_for(3 * c->n_own, 256), 256, 0, s>>>(c->n_own, c->node_ptr, c->fscr, nullptr, c->own_nodes,
-                                                               c->rowptr_c, c->cols_c, c->M, c->fff, v, vn, fext, h,
-                                                               partial_only ? 1 : 0, g, fint);
+    k_gather_f_dof<<<grid_for(3 * c->n_own, 256), 256, 0, s>>>(
+        f_args(c, c->fscr, nullptr, v, vn, fext, h, partial_only ? 1 : 0, g, fint));
     TL_CHECK_LAUNCH();
     return TLFEA_OK;
   }
@@ -311,9 +306,8 @@ tlfea_status launch_residual(Context* c, const double* fint, const double* v, co
     return TLFEA_OK;
   }
   if (g) {
-    k_gather_f_dof<<<grid_for(3 * c->n_own, 256), 256, 0, s>>>(c->n_own, c->node_ptr, c->fscr, fint, c->own_nodes,
-                                                               c->rowptr_c, c->cols_c, c->M, c->fff, v, vn, fext, h, 2,
-                                                               g, nullptr);
+    k_gather_f_dof<<<grid_for(3 * c->n_own, 256), 256, 0, s>>>(
+        f_args(c, c->fscr, fint, v, vn, fext, h, 2, g, nullptr));
     TL_CHECK_LAUNCH();
     return TLFEA_OK;
   }
