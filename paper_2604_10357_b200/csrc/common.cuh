@@ -46,8 +46,7 @@ inline int n_qp_of(int quadrature) {
 inline int n_ublk_of(int nen) { return nen * (nen + 1) / 2; }
 // element-kernel CTA tile: kElWarps warps, 3 T10 elements or 1 ANCF element per warp
 constexpr int kElWarps = 4;
-inline int el_per_tile(int element) { return kElWarps * (element == TLFEA_T10 ? 3 : 1); }
-// gather CTA: 4 warps of 32 units (H) / 128 threads (f)
+inline int el_per_tile(int element) { return kElWarps * (element == TLFEA_T10 ? 3 : 1); }// gather CTA: 4 warps of 32 units (H) / 128 threads (f)
 constexpr int kGatherThreads = 128;
 
 // Packed contribution entry of the H gather: element (local id) << 8 | a << 4 | b

@@ -105,15 +105,11 @@ struct ElArgs {
   const int32_t* dest;
   const int32_t* fdest;
   unsigned long long* err;
-  int cta_tiles;  // k_element_pf: consecutive tiles per CTA
+  int cta_tiles;  // k_element: consecutive tiles per CTA
 };
 
 __device__ __forceinline__ void pf_cp4(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
-               : "memory");
-}
-__device__ __forceinline__ void pf_cp8(void* smem, const void* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
                : "memory");
 }
 __device__ __forceinline__ void pf_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
@@ -122,27 +118,12 @@ __device__ __forceinline__ void pf_wait() { asm volatile("cp.async.wait_all;\n" 
 #define TLFEA_DEST_ASYNC 1  // k_element: gather-sorted destinations via cp.async at group start
 #endif
 
-// Per-warp prefetch buffer of one element group (EPW elements): the inputs
-// k_element_pf moves into shared memory with cp.async one group ahead.
-template <int ELEM, bool KV>
-struct WarpIn {
-  static constexpr int NEN = Geo<ELEM>::NEN, EPW = Geo<ELEM>::EPW, NUB = Geo<ELEM>::NUB;
-  double x[EPW * NEN * 3];
-  double v[KV ? EPW * NEN * 3 : 1];
-  int32_t conn[EPW * NEN];
-  int32_t dest[EPW * NUB];
-  int32_t fdest[EPW * NEN];
-};
-
-// One warp group (EPW elements of warp `grp`) of Stage 1 + Stage 2. PF: the
-// element's coordinates, destinations and class come from the prefetched
-// shared-memory buffer `in` (class id `ce_in`) instead of global memory.
+// One warp group (EPW elements of warp group `grp`) of Stage 1 + Stage 2.
 // DA: the group's gather-sorted destinations are copied to shared memory with
 // cp.async when the group starts and consumed by the store phase, so the
 // scattered index loads never stall the warp.
-template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS, bool PF = false, bool DA = false>
-__device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab,
-                                              const WarpIn<ELEM, KV>* in = nullptr, int ce_in = 0) {
+template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS, bool DA = false>
+__device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab) {
   using G = Geo<ELEM>;
   constexpr int NEN = G::NEN, GROUP = G::GROUP, EPW = G::EPW, NUB = G::NUB, NB = G::NB;
   constexpr int NC = KV ? 18 : 9;            // reduced components (F, Fdot)
@@ -175,7 +156,7 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
   const bool valid = lane_active && e < n_el;
   const int gbase = g * GROUP;
   // (SVK only: the Mooney-Rivlin tables already fill the 48 KB of static shared memory)
-  constexpr bool DAX = DA && TAN && !PF && MODEL == 0;
+  constexpr bool DAX = DA && TAN && MODEL == 0;
   __shared__ int32_t s_dst[kWarps][DAX ? EPW * NUB : 1];
   if (DAX && dest && !mat.dbg_nowrite) {
     const int64_t e0 = grp * EPW, lim = (n_el - e0) * NUB;
@@ -186,24 +167,14 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
   double xa[3] = {0, 0, 0}, va[3] = {0, 0, 0};
   int ce = 0;
   if (valid) {
-    if (PF) {
+    const int64_t I = conn[e * NEN + a];
 #pragma unroll
-      for (int i = 0; i < 3; ++i) xa[i] = in->x[(g * NEN + a) * 3 + i];
-      if (KV) {
+    for (int i = 0; i < 3; ++i) xa[i] = x[3 * I + i];
+    if (KV) {
 #pragma unroll
-        for (int i = 0; i < 3; ++i) va[i] = in->v[(g * NEN + a) * 3 + i];
-      }
-      ce = (ce_in >> (8 * g)) & 0xff;
-    } else {
-      const int64_t I = conn[e * NEN + a];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) xa[i] = x[3 * I + i];
-      if (KV) {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) va[i] = v[3 * I + i];
-      }
-      if (CLS) ce = cls[e];
+      for (int i = 0; i < 3; ++i) va[i] = v[3 * I + i];
     }
+    if (CLS) ce = cls[e];
   }
   double fa[3] = {0, 0, 0};
   // NPASS > 1 splits each lane's blocks over sequential passes that redo the
@@ -413,7 +384,7 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
   }
 
   if (valid && pass == 0 && (ELEM == 0 || half == 0)) {
-    const int64_t fp = fdest ? (int64_t)(PF ? in->fdest[g * NEN + a] : fdest[e * NEN + a]) : e * NEN + a;
+    const int64_t fp = fdest ? (int64_t)fdest[e * NEN + a] : e * NEN + a;
     double* fo = fscr + fp * 3;
     fo[0] = fa[0];
     fo[1] = fa[1];
@@ -448,7 +419,7 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
         bool tr = a > b;
         pos = (int32_t)(e * NUB + ub);
         if (dest) {
-          const int32_t d = PF ? in->dest[g * NUB + ub] : DAX ? s_dst[wib][g * NUB + ub] : dest[e * NUB + ub];
+          const int32_t d = DAX ? s_dst[wib][g * NUB + ub] : dest[e * NUB + ub];
           pos = d >> 1;
           tr = tr != ((d & 1) != 0);
         }
@@ -485,107 +456,10 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>()) k_
   const int64_t t0 = (int64_t)blockIdx.x * A.cta_tiles;
 #pragma unroll 1
   for (int k = 0; k < A.cta_tiles; ++k)
-    element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, false, TLFEA_DEST_ASYNC != 0>(
+    element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, TLFEA_DEST_ASYNC != 0>(
         (t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
 }
 
-// prefetch stage 1: the connectivity of group grp
-template <int ELEM, bool KV>
-__device__ __forceinline__ void pf_conn(WarpIn<ELEM, KV>& B, int64_t grp, const ElArgs& A) {
-  using W = WarpIn<ELEM, KV>;
-  const int lane = threadIdx.x & 31;
-  const int64_t base = grp * W::EPW * W::NEN, lim = A.n_el * W::NEN;
-  for (int t = lane; t < W::EPW * W::NEN; t += 32)
-    if (base + t < lim) pf_cp4(&B.conn[t], A.conn + base + t);
-}
-// prefetch stage 2 (conn of grp already in B): coordinates (velocities) of
-// its nodes, the gather-sorted destinations of its blocks and forces
-template <int ELEM, bool KV, bool TAN>
-__device__ __forceinline__ void pf_rest(WarpIn<ELEM, KV>& B, int64_t grp, const ElArgs& A) {
-  using W = WarpIn<ELEM, KV>;
-  const int lane = threadIdx.x & 31;
-  const int64_t e0 = grp * W::EPW;
-  for (int t = lane; t < W::EPW * W::NEN; t += 32) {
-    if (e0 + t / W::NEN >= A.n_el) continue;
-    const int64_t I = B.conn[t];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) pf_cp8(&B.x[3 * t + i], A.x + 3 * I + i);
-    if (KV) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i) pf_cp8(&B.v[3 * t + i], A.v + 3 * I + i);
-    }
-    if (A.fdest) pf_cp4(&B.fdest[t], A.fdest + e0 * W::NEN + t);
-  }
-  if (TAN && A.dest) {
-    const int64_t lim = (A.n_el - e0) * W::NUB;
-    for (int t = lane; t < W::EPW * W::NUB; t += 32)
-      if (t < lim) pf_cp4(&B.dest[t], A.dest + e0 * W::NUB + t);
-  }
-}
-// class ids of the group's elements packed one byte each (plain load, one group ahead)
-template <int ELEM>
-__device__ __forceinline__ int pf_cls(int64_t grp, const ElArgs& A) {
-  constexpr int EPW = Geo<ELEM>::EPW;
-  int r = 0;
-#pragma unroll
-  for (int g = 0; g < EPW; ++g) {
-    const int64_t e = grp * EPW + g;
-    if (e < A.n_el) r |= (int)A.cls[e] << (8 * g);
-  }
-  return r;
-}
-
-// Persistent element kernel (geometry classes): one CTA per resident slot,
-// the class tables staged once per CTA, and each warp walks its element
-// groups with a two-deep cp.async pipeline — while group i is computed, the
-// coordinates / destinations of group i+1 and the connectivity of group i+2
-// are in flight, so the dependent conn -> x and dest loads never stall it.
-template <int ELEM, int NQ, int MODEL, bool KV, bool TAN>
-__global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, 1>()) k_element_pf(ElArgs A) {
-  using W = WarpIn<ELEM, KV>;
-  // dynamic shared memory: [prefetch buffers kWarps x 2][class tables [n_cls][NQ][3 NEN + 1]]
-  extern __shared__ __align__(16) double s_dyn[];
-  W(*s_in)[2] = reinterpret_cast<W(*)[2]>(s_dyn);
-  double* s_tab = s_dyn + kWarps * 2 * sizeof(W) / sizeof(double);
-  static_assert(sizeof(W) % sizeof(double) == 0, "class tables stay 8-byte aligned");
-  {
-    const int tot = A.n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1);
-    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_tab[t] = A.cls_tab[t];
-    __syncthreads();
-  }
-  const int wib = threadIdx.x >> 5;
-  // CTA b covers the A.cta_tiles consecutive tiles starting at b * cta_tiles;
-  // CTAs are dispatched in order, so the elements in flight stay a compact
-  // window (the gather-sorted scratch stores of neighbouring elements then
-  // merge into full sectors in L2 instead of forcing DRAM fills)
-  const int64_t n_grp = min((A.n_el + W::EPW - 1) / W::EPW, ((int64_t)blockIdx.x + 1) * A.cta_tiles * kWarps);
-  const int64_t stride = kWarps;
-  int64_t grp = (int64_t)blockIdx.x * A.cta_tiles * kWarps + wib;
-  W* B = s_in[wib];
-  int ce_cur = 0, ce_next = 0;
-  if (grp < n_grp) {
-    pf_conn<ELEM, KV>(B[0], grp, A);
-    pf_wait();
-    __syncwarp();
-    pf_rest<ELEM, KV, TAN>(B[0], grp, A);
-    ce_cur = pf_cls<ELEM>(grp, A);
-  }
-  if (grp + stride < n_grp) pf_conn<ELEM, KV>(B[1], grp + stride, A);
-#pragma unroll 1
-  for (int i = 0; grp < n_grp; ++i, grp += stride) {
-    pf_wait();
-    __syncwarp();
-    const int cur = i & 1, nxt = cur ^ 1;
-    if (grp + stride < n_grp) {
-      pf_rest<ELEM, KV, TAN>(B[nxt], grp + stride, A);
-      ce_next = pf_cls<ELEM>(grp + stride, A);
-    }
-    if (grp + 2 * stride < n_grp) pf_conn<ELEM, KV>(B[cur], grp + 2 * stride, A);
-    element_group<ELEM, NQ, MODEL, KV, TAN, true, 1, true>(grp, A, s_tab, &B[cur], ce_cur);
-    ce_cur = ce_next;
-  }
-  pf_wait();
-}
 
 // ------------------------------------------------ FP64 tensor-core variant
 // T10 + SVK + congruent-element classes. The element tangent is split as
@@ -1326,17 +1200,6 @@ static bool use_tc() {
   }
   return v == 1;
 }
-// persistent prefetching element kernel (k_element_pf) for class-table
-// contexts; TLFEA_PF=0 selects the one-tile-per-CTA k_element (A/B).
-// tiles per CTA of the prefetching kernel; TLFEA_PF=0 selects k_element
-static int pf_tiles() {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("TLFEA_PF");
-    v = (s && s[0]) ? std::max(0, atoi(s)) : 0;
-  }
-  return v;
-}
 // tiles per CTA of k_element with class tables (TLFEA_EL_TILES)
 static int el_cta_tiles() {
   static int v = -1;
@@ -1402,20 +1265,6 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
   if (grid == 0) return TLFEA_OK;
   c->mat.dbg_nowrite = dbg_nowrite();
   ElArgs A = el_args(c, x, v);
-  if (c->n_cls > 0 && pf_tiles() > 0) {
-    auto kern = k_element_pf<ELEM, NQ, MODEL, KV, TAN>;
-    const size_t smem = kWarps * 2 * sizeof(WarpIn<ELEM, KV>) + sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-      TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      smem_set = smem;
-    }
-    A.cta_tiles = pf_tiles();
-    const unsigned g = (unsigned)((grid + A.cta_tiles - 1) / A.cta_tiles);
-    kern<<<g, kWarps * 32, smem, s>>>(A);
-    TL_CHECK_LAUNCH();
-    return TLFEA_OK;
-  }
   if (c->n_cls > 0) {
     const size_t smem = sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
     static size_t smem_set = 0;  // per template instantiation
