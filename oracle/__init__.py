@@ -90,6 +90,7 @@ def _declare(L):
     L.orc_eval_rows.argtypes = [i, i, i, i, _d, _i32, _d, _d, _d, _d, d, i64, _i64, _i64, _i64,
                                 i64, _i64, _d, _d, _d]
     L.orc_eval_rows.restype = i64
+    L.orc_adamw_update.argtypes = [i64, i, _d, _d, _d, _d, _d, _d, d, _d]
 
 
 def _p(a, kind=_d):
@@ -316,6 +317,30 @@ class Problem:
                        _p(self.cols, _i64), _p(_f64(x)), _p(_f64(v)), _p(_f64(vn)), _p(_f64(fext)),
                        float(h), _p(g), _p(H), _p(fint))
         return g, H, fint
+
+
+ADAMW_FIELDS = ("alpha", "beta1", "beta2", "eps", "weight_decay")
+
+
+def adamw_update(l: int, prm: dict, g, m, s, v, q_n, h):
+    """Alg. 2 lines 6-10 for inner iteration l >= 1: returns the
+    updated (m, s, v, q) (inputs are not modified)."""
+    m, s, v = _f64(m).copy(), _f64(s).copy(), _f64(v).copy()
+    q = np.zeros_like(v)
+    p = np.array([prm[k] for k in ADAMW_FIELDS], np.float64)
+    lib().orc_adamw_update(v.size, int(l), _p(p), _p(_f64(g)), _p(m), _p(s), _p(v), _p(_f64(q_n)), float(h), _p(q))
+    return m, s, v, q
+
+
+def adamw_iteration(problem: "Problem", l: int, prm: dict, q_n, v_n, fext, h, v, m, s, g):
+    """One AdamW inner iteration of Alg. 2 without constraints
+    (C_q empty, NEXT-3): the update above, then Stage 1 + Stage 2 at
+    q = q_n + h v (Kelvin-Voigt driven by the new v, reading Q9) and the
+    gradient g = M (v - v_n)/h + f_int - f_ext - f_ff (Eq. residual, reading
+    Q10). Returns (v, m, s, g, q, f_int, ||g||, ||v||)."""
+    m, s, v, q = adamw_update(l, prm, g, m, s, v, q_n, h)
+    g, _, f = problem.eval(q, v, v_n, fext, h, hessian=False)
+    return v, m, s, g, q, f, float(np.linalg.norm(g)), float(np.linalg.norm(v))
 
 
 def incidence(conn_coef: np.ndarray, nodes: np.ndarray):

@@ -901,4 +901,21 @@ int64_t orc_eval_rows(int elem, int rule, int mass_rule, int model, const double
   return need;
 }
 
+// AdamW velocity update of inner iteration l (Alg. 2), one DOF at a
+// time in the algorithm's order: first moment, second moment, bias correction,
+// velocity update with decoupled weight decay, backward-Euler step map.
+// prm = (alpha, beta1, beta2, eps, weight_decay). m, s, v updated in place.
+void orc_adamw_update(int64_t n, int l, const double* prm, const double* g, double* m, double* s, double* v,
+                      const double* q_n, double h, double* q) {
+  const double alpha = prm[0], b1 = prm[1], b2 = prm[2], eps = prm[3], wd = prm[4];
+  const double c1 = 1.0 - std::pow(b1, l), c2 = 1.0 - std::pow(b2, l);
+  for (int64_t i = 0; i < n; ++i) {
+    m[i] = b1 * m[i] + (1.0 - b1) * g[i];                   // first moment
+    s[i] = b2 * s[i] + (1.0 - b2) * g[i] * g[i];            // second moment
+    const double mh = m[i] / c1, sh = s[i] / c2;            // bias correction
+    v[i] = (1.0 - alpha * wd) * v[i] - alpha * mh / (std::sqrt(sh) + eps);  // velocity update
+    q[i] = q_n[i] + h * v[i];                               // q = q_n + h v
+  }
+}
+
 }  // extern "C"
