@@ -248,6 +248,34 @@ tlfea_status tlfea_eval(tlfea_ctx ctx, const double* x, const double* v,
 tlfea_status tlfea_force_only(tlfea_ctx ctx, const double* x, const double* v,
                               double* f_int_out, void* stream);
 
+/* AdamW hyper-parameters of Alg. 2: step alpha, moment decays
+ * beta1 / beta2, eps, decoupled weight decay lambda_wd. */
+typedef struct {
+  double alpha, beta1, beta2, eps, weight_decay;
+} tlfea_adamw_params;
+
+/* tlfea_adamw_iteration — one inner AdamW iteration l >= 1 of Alg. 2
+ * (SURVEY §8(f) NEXT-2), without constraint terms (C_q empty),
+ * single-rank contexts:
+ *   m <- b1 m + (1-b1) g;  s <- b2 s + (1-b2) g.g;
+ *   m^ = m/(1-b1^l);  s^ = s/(1-b2^l);
+ *   v <- (1 - alpha wd) v - alpha m^/(sqrt(s^) + eps);  q <- q_n + h v;
+ *   f_int(q, v) (Stage 1 + 2; Kelvin-Voigt driven by the new v, reading Q9);
+ *   g <- M (v - v_n)/h + f_int - f_ext - f_ff  (Eq. residual, reading Q10);
+ *   norms_out[0] = ||g||_2, norms_out[1] = ||v||_2 (the inner stopping test
+ *   ||g|| <= eps_in (1 + ||v||)), reduced on the device in a fixed
+ *   order (bitwise reproducible).
+ * All vectors are DEVICE [3 n_coef], DOF-major: q_n, v_n read; f_ext read
+ * (nullable = 0); v, m, s, g read AND overwritten (g on entry = the previous
+ * iteration's gradient, zeros for l = 1 after a reset); q_out written;
+ * f_int_out and norms_out (DEVICE [2]) nullable. Returns TLFEA_E_INVALID for
+ * l < 1, NULL required pointers or a partitioned context. */
+tlfea_status tlfea_adamw_iteration(tlfea_ctx ctx, const double* q_n, const double* v_n,
+                                   const double* f_ext, double h, int32_t l,
+                                   const tlfea_adamw_params* params, double* v, double* m,
+                                   double* s, double* g, double* q_out, double* f_int_out,
+                                   double* norms_out, void* stream);
+
 /* tlfea_eval_host — tlfea_eval with HOST buffers (end-to-end path): copies
  * x, v, v_n, f_ext host->device, evaluates, copies g, H (and f_int if
  * non-NULL) device->host, and synchronizes the stream before returning.

@@ -62,6 +62,11 @@ class Info(C.Structure):
                 ("affine", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32), ("device_bytes", C.c_int64),
                 ("n_geometry_classes", C.c_int32), ("fused_eval", C.c_int32)]
 
+class AdamWParams(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("weight_decay", C.c_double)]
+
+
 N_TIMING = 5
 TIMING_KINDS = ("element", "gather_H", "gather_f", "exchange", "fused")
 
@@ -80,6 +85,7 @@ _SIGS = {
     "tlfea_export_mass": [_vp, _vp, _vp, _vp],
     "tlfea_eval": [_vp, _vp, _vp, _vp, _vp, _d, _vp, _vp, _vp, _vp],
     "tlfea_force_only": [_vp, _vp, _vp, _vp, _vp],
+    "tlfea_adamw_iteration": [_vp, _vp, _vp, _vp, _d, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "tlfea_eval_host": [_vp, _vp, _vp, _vp, _vp, _d, _vp, _vp, _vp, _vp],
     "tlfea_compute_stress": [_vp, _vp, _vp, _vp, _vp],
     "tlfea_internal_force_from_stress": [_vp, _vp, _vp, _vp],
@@ -302,6 +308,23 @@ class Context:
             f_int = self.empty_outputs()[2]
         _check(lib().tlfea_force_only(self.handle, _ptr(x), _ptr(v), _ptr(f_int), _stream(stream)))
         return f_int
+
+    def adamw_iteration(self, q_n, v_n, f_ext, h, l, params, v, m, s, g, q=None, f_int=None, norms=None,
+                        stream=None):
+        """tlfea_adamw_iteration: one AdamW inner iteration l >= 1 (Alg. 2).
+        params: dict alpha, beta1, beta2, eps, weight_decay. v, m, s, g are
+        CUDA tensors updated in place; returns (q, norms) with norms =
+        [||g||, ||v||] on the device."""
+        import torch
+        if q is None:
+            q = torch.empty_like(v)
+        if norms is None:
+            norms = torch.empty(2, dtype=torch.float64, device=v.device)
+        p = AdamWParams(*(float(params[k]) for k in ("alpha", "beta1", "beta2", "eps", "weight_decay")))
+        _check(lib().tlfea_adamw_iteration(self.handle, _ptr(q_n), _ptr(v_n), _ptr(f_ext), float(h), int(l),
+                                           C.byref(p), _ptr(v), _ptr(m), _ptr(s), _ptr(g), _ptr(q), _ptr(f_int),
+                                           _ptr(norms), _stream(stream)))
+        return q, norms
 
     def eval_host(self, x, v, v_n=None, f_ext=None, h=1e-3, g=None, H=None, f_int=None, stream=None):
         """Host (numpy or pinned CPU tensors) in and out; synchronizes."""

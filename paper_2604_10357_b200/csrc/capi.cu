@@ -250,6 +250,30 @@ tlfea_status tlfea_force_only(tlfea_ctx ctx, const double* x, const double* v, d
   return TLFEA_OK;
 }
 
+tlfea_status tlfea_adamw_iteration(tlfea_ctx ctx, const double* q_n, const double* v_n, const double* f_ext,
+                                   double h, int32_t l, const tlfea_adamw_params* params, double* v, double* m,
+                                   double* s_mom, double* g, double* q_out, double* f_int_out, double* norms_out,
+                                   void* stream) {
+  CTX_OR_FAIL(ctx);
+  Context& c = ctx->c;
+  TRY(check_h(h));
+  if (c.nranks > 1) return fail(TLFEA_E_INVALID, "tlfea_adamw_iteration: single-rank contexts only");
+  if (l < 1) return fail(TLFEA_E_INVALID, "tlfea_adamw_iteration: iteration index l must be >= 1");
+  if (!q_n || !v_n || !params || !v || !m || !s_mom || !g || !q_out)
+    return fail(TLFEA_E_INVALID, "tlfea_adamw_iteration: NULL q_n, v_n, params, v, m, s, g or q_out");
+  TRY(use_device(c));
+  const cudaStream_t s = as_stream(stream);
+  c.last_stream = s;
+  // (i) velocity update and step map
+  TIMED(2, launch_adamw_update(&c, l, *params, g, m, s_mom, v, q_n, h, q_out, s));
+  // (iii)-(iv) Stage 1 + Stage 2 at q, (vi) gradient
+  TIMED(0, launch_element_kernel(&c, q_out, v, false, s));
+  TIMED(2, launch_gather_f(&c, v, v_n, f_ext, h, g, f_int_out, false, s));
+  // device ||g||, ||v|| for the inner stopping test
+  if (norms_out) TIMED(2, launch_norms2(&c, g, v, norms_out, s));
+  return TLFEA_OK;
+}
+
 tlfea_status tlfea_eval_host(tlfea_ctx ctx, const double* x, const double* v, const double* v_n,
                              const double* f_ext, double h, double* g_out, double* H_out, double* f_int_out,
                              void* stream) {

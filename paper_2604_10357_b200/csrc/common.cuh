@@ -153,6 +153,7 @@ struct Context {
   int64_t* recv_peer_blk_off = nullptr;  // host copies are enough
   std::vector<int64_t> recv_blk_count, recv_node_count, send_blk_count, send_node_count;
   double* fpart = nullptr;       // [3 n_own] local partial force (partitioned mode)
+  double* norm_part = nullptr;   // [2 x kNormBlocks] partial sums of the AdamW norms
 
   // live timing (tlfea_set_timing)
   bool timing = false;
@@ -211,6 +212,9 @@ tlfea_status launch_stress_only(Context* c, const double* x, const double* v, do
 tlfea_status launch_force_from_stress(Context* c, const double* P, cudaStream_t s);
 tlfea_status launch_residual(Context* c, const double* fint, const double* v, const double* vn,
                              const double* fext, double h, double* g, cudaStream_t s);
+tlfea_status launch_adamw_update(Context* c, int l, const tlfea_adamw_params& p, const double* g, double* m,
+                                 double* s, double* v, const double* q_n, double h, double* q, cudaStream_t st);
+tlfea_status launch_norms2(Context* c, const double* a, const double* b, double* out, cudaStream_t st);
 tlfea_status launch_pack_send(Context* c, double* send, bool force_only, cudaStream_t s);
 tlfea_status launch_unpack_recv(Context* c, const double* recv, double h, double* H,
                                 bool force_only, cudaStream_t s);

@@ -295,6 +295,98 @@ tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, cons
   return TLFEA_OK;
 }
 
+// ------------------------------------------------ AdamW (Alg. 2, NEXT-2)
+// One thread per DOF: moments, bias correction, velocity update with
+// decoupled weight decay, backward-Euler step map.
+__global__ void k_adamw_update(int64_t n, double c1, double c2, double alpha, double b1, double b2, double eps,
+                               double wd, const double* __restrict__ g, double* __restrict__ m,
+                               double* __restrict__ s, double* __restrict__ v, const double* __restrict__ q_n,
+                               double h, double* __restrict__ q) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double gi = g[i];
+  const double mi = b1 * m[i] + (1.0 - b1) * gi;
+  const double si = b2 * s[i] + (1.0 - b2) * gi * gi;
+  const double vi = (1.0 - alpha * wd) * v[i] - alpha * (mi / c1) / (sqrt(si / c2) + eps);
+  m[i] = mi;
+  s[i] = si;
+  v[i] = vi;
+  q[i] = q_n[i] + h * vi;
+}
+
+// ||a||^2 and ||b||^2 in a fixed reduction order: kNormBlocks blocks of
+// grid-stride partials, then one block sums the partials (bitwise reproducible)
+constexpr int kNormBlocks = 296, kNormThreads = 256;
+
+__device__ __forceinline__ void block_sum2(double& x, double& y) {
+  __shared__ double sx[kNormThreads], sy[kNormThreads];
+  sx[threadIdx.x] = x;
+  sy[threadIdx.x] = y;
+  __syncthreads();
+  for (int w = kNormThreads / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      sx[threadIdx.x] += sx[threadIdx.x + w];
+      sy[threadIdx.x] += sy[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  x = sx[0];
+  y = sy[0];
+}
+
+__global__ void __launch_bounds__(kNormThreads) k_sumsq_partial(int64_t n, const double* __restrict__ a,
+                                                                const double* __restrict__ b,
+                                                                double* __restrict__ part) {
+  double x = 0.0, y = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)kNormThreads + threadIdx.x; i < n; i += (int64_t)kNormBlocks * kNormThreads) {
+    x = fma(a[i], a[i], x);
+    y = fma(b[i], b[i], y);
+  }
+  block_sum2(x, y);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = x;
+    part[2 * blockIdx.x + 1] = y;
+  }
+}
+
+__global__ void __launch_bounds__(kNormThreads) k_sumsq_final(const double* __restrict__ part,
+                                                              double* __restrict__ out) {
+  double x = 0.0, y = 0.0;
+  for (int i = threadIdx.x; i < kNormBlocks; i += kNormThreads) {
+    x += part[2 * i];
+    y += part[2 * i + 1];
+  }
+  block_sum2(x, y);
+  if (threadIdx.x == 0) {
+    out[0] = sqrt(x);
+    out[1] = sqrt(y);
+  }
+}
+
+tlfea_status launch_adamw_update(Context* c, int l, const tlfea_adamw_params& p, const double* g, double* m,
+                                 double* s, double* v, const double* q_n, double h, double* q, cudaStream_t st) {
+  const int64_t n = 3 * c->n_coef;
+  if (n == 0) return TLFEA_OK;
+  const double c1 = 1.0 - std::pow(p.beta1, l), c2 = 1.0 - std::pow(p.beta2, l);
+  k_adamw_update<<<grid_for(n, 256), 256, 0, st>>>(n, c1, c2, p.alpha, p.beta1, p.beta2, p.eps, p.weight_decay, g,
+                                                     m, s, v, q_n, h, q);
+  TL_CHECK_LAUNCH();
+  return TLFEA_OK;
+}
+
+tlfea_status launch_norms2(Context* c, const double* a, const double* b, double* out, cudaStream_t st) {
+  const int64_t n = 3 * c->n_coef;
+  if (!c->norm_part) {
+    const tlfea_status st_alloc = c->alloc(&c->norm_part, (size_t)2 * kNormBlocks);
+    if (st_alloc != TLFEA_OK) return st_alloc;
+  }
+  k_sumsq_partial<<<kNormBlocks, kNormThreads, 0, st>>>(n, a, b, c->norm_part);
+  TL_CHECK_LAUNCH();
+  k_sumsq_final<<<1, kNormThreads, 0, st>>>(c->norm_part, out);
+  TL_CHECK_LAUNCH();
+  return TLFEA_OK;
+}
+
 tlfea_status launch_residual(Context* c, const double* fint, const double* v, const double* vn,
                              const double* fext, double h, double* g, cudaStream_t s) {
   if (c->n_own == 0) return TLFEA_OK;
