@@ -230,7 +230,19 @@ class Problem:
     slot map (on demand), consistent mass and f_ff."""
 
     def __init__(self, mesh, mat: dict, rule: int, mass_rule: int = 0, gravity=(0.0, 0.0, 0.0),
-                 with_precompute: bool = True, with_pattern: bool = True):
+                 with_precompute: bool = True, with_pattern: bool = True, constraints: dict | None = None):
+        """constraints (NEXT-3, reading Q22): linear bilateral constraints
+        c(q) = C q - b with a constant CSR Jacobian C (m x n_dof): dict
+        rowptr [m+1], cols (DOF ids), vals, b [m]. Clamp rows are the special
+        case C row = e_i, b = the clamped value. The H pattern is
+        the union of the element couplings and C^T C's."""
+        self.C = None
+        if constraints is not None:
+            self.C = {k: np.asarray(constraints[k]) for k in ("rowptr", "cols", "vals", "b")}
+            self.C["rowptr"] = self.C["rowptr"].astype(np.int64)
+            self.C["cols"] = self.C["cols"].astype(np.int64)
+            self.C["vals"] = self.C["vals"].astype(np.float64)
+            self.C["b"] = self.C["b"].astype(np.float64)
         self.mesh = mesh
         self.elem = int(mesh.element)
         self.rule = int(rule)
@@ -261,6 +273,17 @@ class Problem:
             self.cols_c = np.zeros(nnz, np.int64)
             L.orc_coef_pattern(self.elem, self.n_el, _p(self.conn, _i32), self.n_coef,
                                _p(self.rowptr_c, _i64), _p(self.cols_c, _i64))
+            if self.C is not None:
+                # union with the coefficient couplings of every constraint row
+                rows = [set(self.cols_c[self.rowptr_c[I]:self.rowptr_c[I + 1]].tolist())
+                        for I in range(self.n_coef)]
+                for k in range(self.C["b"].size):
+                    coefs = {int(j) // 3 for j in self.C["cols"][self.C["rowptr"][k]:self.C["rowptr"][k + 1]]}
+                    for I in coefs:
+                        rows[I] |= coefs
+                self.rowptr_c = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+                self.cols_c = np.array([j for r in rows for j in sorted(r)], np.int64)
+                nnz = self.cols_c.size
             self.rowptr = np.zeros(3 * self.n_coef + 1, np.int64)
             self.cols = np.zeros(9 * nnz, np.int64)
             L.orc_lift(self.n_coef, _p(self.rowptr_c, _i64), _p(self.cols_c, _i64),
@@ -304,8 +327,10 @@ class Problem:
                                     _p(self.dims), _p(_f64(P)), self.n_coef, _p(f))
         return f
 
-    def eval(self, x, v, vn=None, fext=None, h=1e-3, hessian=True, use_fff=True):
-        """Returns (g, H or None, f_int) on the full DOF pattern."""
+    def eval(self, x, v, vn=None, fext=None, h=1e-3, hessian=True, use_fff=True, lam=None, rho=0.0):
+        """Returns (g, H or None, f_int) on the full DOF pattern. With
+        constraints: g += h C^T (lam + rho c(x)) (Eq. residual P:101-113,
+        P:484-489) and H += h^2 rho C^T C (Eq. hessian)."""
         nd = 3 * self.n_coef
         g = np.zeros(nd)
         fint = np.zeros(nd)
@@ -316,7 +341,38 @@ class Problem:
                        _p(self.fff if use_fff else None), _p(self.rowptr, _i64),
                        _p(self.cols, _i64), _p(_f64(x)), _p(_f64(v)), _p(_f64(vn)), _p(_f64(fext)),
                        float(h), _p(g), _p(H), _p(fint))
+        if self.C is not None:
+            C = self.C
+            c = self.constraint_residual(x)
+            y = (np.zeros_like(c) if lam is None else _f64(lam)) + rho * c
+            for k in range(c.size):
+                for p in range(C["rowptr"][k], C["rowptr"][k + 1]):
+                    g[C["cols"][p]] += h * C["vals"][p] * y[k]
+            if hessian:
+                for k in range(c.size):
+                    r = range(C["rowptr"][k], C["rowptr"][k + 1])
+                    for p1 in r:
+                        for p2 in r:
+                            H[self.dof_slot(C["cols"][p1], C["cols"][p2])] += h * h * rho * C["vals"][p1] * C["vals"][p2]
         return g, H, fint
+
+    def dof_slot(self, i: int, j: int) -> int:
+        """CSR index of DOF entry (i, j) (binary search over the row's columns)."""
+        a, b = self.rowptr[i], self.rowptr[i + 1]
+        k = a + int(np.searchsorted(self.cols[a:b], j))
+        if k >= b or self.cols[k] != j:
+            raise KeyError((i, j))
+        return k
+
+    def constraint_residual(self, x):
+        """c(q) = C q - b (reading Q22)."""
+        C = self.C
+        xq = _f64(x)
+        c = -C["b"].copy()
+        for k in range(c.size):
+            for p in range(C["rowptr"][k], C["rowptr"][k + 1]):
+                c[k] += C["vals"][p] * xq[C["cols"][p]]
+        return c
 
 
 ADAMW_FIELDS = ("alpha", "beta1", "beta2", "eps", "weight_decay")

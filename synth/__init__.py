@@ -146,6 +146,39 @@ def clamped_dofs_ancf(mesh: Mesh, tol: float = 1e-12) -> int:
     return int(12 * np.count_nonzero(np.abs(pos[:, 0]) < tol))
 
 
+def constraint_set(mesh: Mesh, seed: int = SEED_BASE + 20, n_ties: int = 4, tol: float = 1e-12) -> dict:
+    """Linear bilateral constraints c(q) = C q - b (NEXT-3, reading Q22) as a
+    CSR over DOFs: clamp rows (C row = e_i, b = the reference coordinate)
+    for every DOF of the x = 0 face (T10 nodes; ANCF position coefficients),
+    then `n_ties` random linear ties between two DOFs of different nodes
+    elsewhere (coefficients N(0,1), b = 0). Inputs only — no method arithmetic."""
+    rng = np.random.default_rng(seed)
+    X = mesh.X
+    if mesh.element == 0:
+        face = np.nonzero(np.abs(X[:, 0]) < tol)[0]
+    else:
+        face = 4 * np.nonzero(np.abs(X.reshape(-1, 4, 3)[:, 0, 0]) < tol)[0]
+    rows, cols, vals, b = [0], [], [], []
+    for I in face:
+        for d in range(3):
+            cols.append(3 * int(I) + d)
+            vals.append(1.0)
+            b.append(float(X[I, d]))
+            rows.append(len(cols))
+    n_dof = 3 * mesh.n_coef
+    for _ in range(n_ties):
+        i, j = rng.choice(n_dof, 2, replace=False)
+        while i // 3 == j // 3:
+            j = int(rng.integers(n_dof))
+        lo, hi = sorted((int(i), int(j)))
+        cols += [lo, hi]
+        vals += list(rng.normal(size=2))
+        b.append(0.0)
+        rows.append(len(cols))
+    return dict(rowptr=np.array(rows, np.int64), cols=np.array(cols, np.int64),
+                vals=np.array(vals, np.float64), b=np.array(b, np.float64))
+
+
 # ------------------------------------------------------------------ fields --
 
 def t10_state(mesh: Mesh, seed: int = SEED_BASE, bend: float = 0.02,
