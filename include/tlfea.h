@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define TLFEA_ABI_VERSION 2
+#define TLFEA_ABI_VERSION 3
 
 typedef struct tlfea_ctx_s* tlfea_ctx;
 
@@ -119,7 +119,24 @@ typedef struct {
  *   rank, nranks, elem_part (host [n_elements] owning rank, or NULL for
  *   contiguous equal element blocks). A node is owned by the lowest rank
  *   among its incident elements (reading Q20).
- *  device   : CUDA device ordinal the context lives on. */
+ *  device   : CUDA device ordinal the context lives on.
+ *  constraints: linear bilateral constraints (below), or NULL. */
+
+/* Linear bilateral constraints c(q) = C q - b with a constant Jacobian C
+ * (m x n_dof), all HOST memory copied by tlfea_setup (SURVEY §8(f) NEXT-3,
+ * reading Q22; Eq. residual).
+ * Clamped Dirichlet DOFs are identity rows (C row = e_i, b = clamped value).
+ *  rowptr [m+1], cols [rowptr[m]] DOF ids (3 I + d) distinct within a row,
+ *  vals [rowptr[m]], b [m]. The H pattern becomes the union of the element
+ *  couplings and those of C^T C. Single-rank contexts only. */
+typedef struct {
+  int64_t m;
+  const int64_t* rowptr;
+  const int64_t* cols;
+  const double* vals;
+  const double* b;
+} tlfea_constraints;
+
 typedef struct {
   int32_t quadrature; /* tlfea_quadrature */
   int32_t mass_rule;
@@ -128,6 +145,7 @@ typedef struct {
   int32_t rank, nranks;
   const int32_t* elem_part;
   int32_t device;
+  const tlfea_constraints* constraints;
 } tlfea_options;
 
 /* Sizes of a context (tlfea_info). Rows/DOFs are GLOBAL indices; in a
@@ -155,6 +173,7 @@ typedef struct {
                               three-kernel path); 0: three kernels. Opt-in
                               (TLFEA_FUSED=1 in the environment at setup) for
                               single-rank contexts with geometry classes. */
+  int64_t n_constraints;   /* rows m of the context's constraint set (0: none) */
 } tlfea_info_t;
 
 /* ---------------------------------------------------------------- setup -- */
@@ -242,6 +261,29 @@ tlfea_status tlfea_eval(tlfea_ctx ctx, const double* x, const double* v,
                         double* g_out, double* H_out, double* f_int_out,
                         void* stream);
 
+/* tlfea_eval_constrained — tlfea_eval plus the constraint terms of the
+ * context's constraint set (NEXT-3; Eq. residual P:101-113, P:484-489 and
+ * Eq. hessian), with c = C x - b (x = q_n + h v):
+ *   g += h C^T (lambda + rho c),   H += h^2 rho C^T C.
+ * lambda DEVICE [m] (NULL = 0), rho >= 0. Each H value receives its C^T C
+ * sum once and each g entry its C^T row in ascending constraint order
+ * (deterministic). Without constraints it equals tlfea_eval. */
+tlfea_status tlfea_eval_constrained(tlfea_ctx ctx, const double* x, const double* v,
+                                    const double* v_n, const double* f_ext, double h,
+                                    const double* lambda, double rho, double* g_out,
+                                    double* H_out, double* f_int_out, void* stream);
+
+/* tlfea_constraint_residual — c_out DEVICE [m] = C q - b for DEVICE q [n_dof]. */
+tlfea_status tlfea_constraint_residual(tlfea_ctx ctx, const double* q, double* c_out,
+                                       void* stream);
+
+/* tlfea_update_multipliers — the dual ascent step of the ALM outer loop,
+ * lambda <- lambda + rho c(q) (Eq. lambda_update, Alg. 2):
+ * lambda DEVICE [m] read and overwritten; c_out DEVICE [m] or NULL receives
+ * c(q) (the outer stopping test ||c|| <= eps_out). */
+tlfea_status tlfea_update_multipliers(tlfea_ctx ctx, const double* q, double rho,
+                                      double* lambda, double* c_out, void* stream);
+
 /* tlfea_force_only — f_int only (the AdamW inner evaluation, Alg. 2
  * P:617-621): DEVICE x, v (v may be NULL when damping is off), f_int_out
  * [3*n_owned_nodes]. */
@@ -255,24 +297,26 @@ typedef struct {
 } tlfea_adamw_params;
 
 /* tlfea_adamw_iteration — one inner AdamW iteration l >= 1 of Alg. 2
- * (SURVEY §8(f) NEXT-2), without constraint terms (C_q empty),
- * single-rank contexts:
+ * (SURVEY §8(f) NEXT-2), single-rank contexts:
  *   m <- b1 m + (1-b1) g;  s <- b2 s + (1-b2) g.g;
  *   m^ = m/(1-b1^l);  s^ = s/(1-b2^l);
  *   v <- (1 - alpha wd) v - alpha m^/(sqrt(s^) + eps);  q <- q_n + h v;
  *   f_int(q, v) (Stage 1 + 2; Kelvin-Voigt driven by the new v, reading Q9);
- *   g <- M (v - v_n)/h + f_int - f_ext - f_ff  (Eq. residual, reading Q10);
+ *   g <- M (v - v_n)/h + f_int - f_ext - f_ff  (Eq. residual, reading Q10)
+ *        + h C^T (lambda + rho c(q))  (with the context's constraints, NEXT-3);
  *   norms_out[0] = ||g||_2, norms_out[1] = ||v||_2 (the inner stopping test
  *   ||g|| <= eps_in (1 + ||v||)), reduced on the device in a fixed
  *   order (bitwise reproducible).
  * All vectors are DEVICE [3 n_coef], DOF-major: q_n, v_n read; f_ext read
  * (nullable = 0); v, m, s, g read AND overwritten (g on entry = the previous
  * iteration's gradient, zeros for l = 1 after a reset); q_out written;
- * f_int_out and norms_out (DEVICE [2]) nullable. Returns TLFEA_E_INVALID for
- * l < 1, NULL required pointers or a partitioned context. */
+ * f_int_out and norms_out (DEVICE [2]) nullable; lambda DEVICE [m] (NULL = 0)
+ * and rho >= 0 enter only with constraints. Returns TLFEA_E_INVALID for
+ * l < 1, rho < 0, NULL required pointers or a partitioned context. */
 tlfea_status tlfea_adamw_iteration(tlfea_ctx ctx, const double* q_n, const double* v_n,
                                    const double* f_ext, double h, int32_t l,
-                                   const tlfea_adamw_params* params, double* v, double* m,
+                                   const tlfea_adamw_params* params, const double* lambda,
+                                   double rho, double* v, double* m,
                                    double* s, double* g, double* q_out, double* f_int_out,
                                    double* norms_out, void* stream);
 

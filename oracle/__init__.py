@@ -388,14 +388,14 @@ def adamw_update(l: int, prm: dict, g, m, s, v, q_n, h):
     return m, s, v, q
 
 
-def adamw_iteration(problem: "Problem", l: int, prm: dict, q_n, v_n, fext, h, v, m, s, g):
-    """One AdamW inner iteration of Alg. 2 without constraints
-    (C_q empty, NEXT-3): the update above, then Stage 1 + Stage 2 at
-    q = q_n + h v (Kelvin-Voigt driven by the new v, reading Q9) and the
-    gradient g = M (v - v_n)/h + f_int - f_ext - f_ff (Eq. residual, reading
-    Q10). Returns (v, m, s, g, q, f_int, ||g||, ||v||)."""
+def adamw_iteration(problem: "Problem", l: int, prm: dict, q_n, v_n, fext, h, v, m, s, g, lam=None, rho=0.0):
+    """One AdamW inner iteration of Alg. 2: the update above,
+    then Stage 1 + Stage 2 at q = q_n + h v (Kelvin-Voigt driven by the new
+    v, reading Q9) and the gradient g = M (v - v_n)/h + f_int - f_ext - f_ff
+    (Eq. residual, reading Q10) + h C^T (lam + rho c(q)) when the problem has
+    constraints. Returns (v, m, s, g, q, f_int, ||g||, ||v||)."""
     m, s, v, q = adamw_update(l, prm, g, m, s, v, q_n, h)
-    g, _, f = problem.eval(q, v, v_n, fext, h, hessian=False)
+    g, _, f = problem.eval(q, v, v_n, fext, h, hessian=False, lam=lam, rho=rho)
     return v, m, s, g, q, f, float(np.linalg.norm(g)), float(np.linalg.norm(v))
 
 

@@ -49,10 +49,16 @@ class Mesh(C.Structure):
                 ("ancf_dims", C.POINTER(C.c_double))]
 
 
+class Constraints(C.Structure):
+    _fields_ = [("m", C.c_int64), ("rowptr", C.POINTER(C.c_int64)), ("cols", C.POINTER(C.c_int64)),
+                ("vals", C.POINTER(C.c_double)), ("b", C.POINTER(C.c_double))]
+
+
 class Options(C.Structure):
     _fields_ = [("quadrature", C.c_int32), ("mass_rule", C.c_int32), ("gravity", C.c_double * 3),
                 ("ancf_dims", C.c_double * 3), ("rank", C.c_int32), ("nranks", C.c_int32),
-                ("elem_part", C.POINTER(C.c_int32)), ("device", C.c_int32)]
+                ("elem_part", C.POINTER(C.c_int32)), ("device", C.c_int32),
+                ("constraints", C.POINTER(Constraints))]
 
 
 class Info(C.Structure):
@@ -60,7 +66,7 @@ class Info(C.Structure):
                 ("n_elements", C.c_int64), ("n_elements_global", C.c_int64), ("n_coef", C.c_int64),
                 ("n_dof", C.c_int64), ("nnz_coef", C.c_int64), ("nnz", C.c_int64), ("n_owned_nodes", C.c_int64),
                 ("affine", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32), ("device_bytes", C.c_int64),
-                ("n_geometry_classes", C.c_int32), ("fused_eval", C.c_int32)]
+                ("n_geometry_classes", C.c_int32), ("fused_eval", C.c_int32), ("n_constraints", C.c_int64)]
 
 class AdamWParams(C.Structure):
     _fields_ = [("alpha", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
@@ -84,8 +90,11 @@ _SIGS = {
     "tlfea_export_precompute": [_vp, _vp, _vp, _vp],
     "tlfea_export_mass": [_vp, _vp, _vp, _vp],
     "tlfea_eval": [_vp, _vp, _vp, _vp, _vp, _d, _vp, _vp, _vp, _vp],
+    "tlfea_eval_constrained": [_vp, _vp, _vp, _vp, _vp, _d, _vp, _d, _vp, _vp, _vp, _vp],
+    "tlfea_constraint_residual": [_vp, _vp, _vp, _vp],
+    "tlfea_update_multipliers": [_vp, _vp, _d, _vp, _vp, _vp],
     "tlfea_force_only": [_vp, _vp, _vp, _vp, _vp],
-    "tlfea_adamw_iteration": [_vp, _vp, _vp, _vp, _d, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "tlfea_adamw_iteration": [_vp, _vp, _vp, _vp, _d, _i32, _vp, _vp, _d, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "tlfea_eval_host": [_vp, _vp, _vp, _vp, _vp, _d, _vp, _vp, _vp, _vp],
     "tlfea_compute_stress": [_vp, _vp, _vp, _vp, _vp],
     "tlfea_internal_force_from_stress": [_vp, _vp, _vp, _vp],
@@ -197,8 +206,18 @@ class Context:
 
     def __init__(self, element: int, conn: np.ndarray, X: np.ndarray, mat: dict, quadrature: int,
                  dims: np.ndarray | None = None, mass_rule: int = 0, gravity=(0.0, 0.0, 0.0),
-                 rank: int = 0, nranks: int = 1, elem_part=None, device: int = 0):
+                 rank: int = 0, nranks: int = 1, elem_part=None, device: int = 0, constraints: dict | None = None):
+        """constraints: dict rowptr, cols (DOF ids), vals, b of c(q) = C q - b
+        (tlfea_constraints; NEXT-3)."""
         L = lib()
+        con = None
+        if constraints is not None:
+            self._con = [np.ascontiguousarray(constraints[k], t) for k, t in
+                         (("rowptr", np.int64), ("cols", np.int64), ("vals", np.float64), ("b", np.float64))]
+            p64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64))
+            pd = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+            con = Constraints(self._con[3].size, p64(self._con[0]), p64(self._con[1]), pd(self._con[2]),
+                              pd(self._con[3]))
         self._conn = np.ascontiguousarray(conn, np.int32)
         self._X = np.ascontiguousarray(X, np.float64)
         self._dims = None if dims is None else np.ascontiguousarray(dims, np.float64)
@@ -207,7 +226,8 @@ class Context:
                     self._conn.ctypes.data_as(C.POINTER(C.c_int32)), self._X.ctypes.data_as(C.POINTER(C.c_double)),
                     None if self._dims is None else self._dims.ctypes.data_as(C.POINTER(C.c_double)))
         opts = Options(quadrature, mass_rule, (C.c_double * 3)(*gravity), (C.c_double * 3)(0, 0, 0), rank, nranks,
-                       None if self._part is None else self._part.ctypes.data_as(C.POINTER(C.c_int32)), device)
+                       None if self._part is None else self._part.ctypes.data_as(C.POINTER(C.c_int32)), device,
+                       None if con is None else C.pointer(con))
         self.material = dict(mat)
         m = make_material(mat)
         h = C.c_void_p()
@@ -294,14 +314,34 @@ class Context:
         return M, fff
 
     # -- evaluation
-    def eval(self, x, v, v_n=None, f_ext=None, h=1e-3, g=None, H=None, f_int=None, stream=None):
+    def eval(self, x, v, v_n=None, f_ext=None, h=1e-3, g=None, H=None, f_int=None, stream=None, lam=None,
+             rho=None):
+        """tlfea_eval, or tlfea_eval_constrained when lam / rho are given."""
         if g is None or H is None:
             g0, H0, _ = self.empty_outputs()
             g = g0 if g is None else g
             H = H0 if H is None else H
-        _check(lib().tlfea_eval(self.handle, _ptr(x), _ptr(v), _ptr(v_n), _ptr(f_ext), float(h), _ptr(g), _ptr(H),
-                                _ptr(f_int), _stream(stream)))
+        if lam is None and rho is None:
+            _check(lib().tlfea_eval(self.handle, _ptr(x), _ptr(v), _ptr(v_n), _ptr(f_ext), float(h), _ptr(g),
+                                    _ptr(H), _ptr(f_int), _stream(stream)))
+        else:
+            _check(lib().tlfea_eval_constrained(self.handle, _ptr(x), _ptr(v), _ptr(v_n), _ptr(f_ext), float(h),
+                                                _ptr(lam), float(rho or 0.0), _ptr(g), _ptr(H), _ptr(f_int),
+                                                _stream(stream)))
         return g, H, f_int
+
+    def constraint_residual(self, q, c=None, stream=None):
+        """c(q) = C q - b on the device (tlfea_constraint_residual)."""
+        torch = self._torch()
+        if c is None:
+            c = torch.empty(max(self.info["n_constraints"], 1), dtype=torch.float64, device=q.device)
+        _check(lib().tlfea_constraint_residual(self.handle, _ptr(q), _ptr(c), _stream(stream)))
+        return c
+
+    def update_multipliers(self, q, rho, lam, c=None, stream=None):
+        """lam += rho c(q) in place (tlfea_update_multipliers); returns c if given."""
+        _check(lib().tlfea_update_multipliers(self.handle, _ptr(q), float(rho), _ptr(lam), _ptr(c), _stream(stream)))
+        return c
 
     def force_only(self, x, v=None, f_int=None, stream=None):
         if f_int is None:
@@ -310,11 +350,12 @@ class Context:
         return f_int
 
     def adamw_iteration(self, q_n, v_n, f_ext, h, l, params, v, m, s, g, q=None, f_int=None, norms=None,
-                        stream=None):
+                        stream=None, lam=None, rho=0.0):
         """tlfea_adamw_iteration: one AdamW inner iteration l >= 1 (Alg. 2).
         params: dict alpha, beta1, beta2, eps, weight_decay. v, m, s, g are
         CUDA tensors updated in place; returns (q, norms) with norms =
-        [||g||, ||v||] on the device."""
+        [||g||, ||v||] on the device. lam / rho: constraint multipliers and
+        penalty (contexts with constraints)."""
         import torch
         if q is None:
             q = torch.empty_like(v)
@@ -322,8 +363,8 @@ class Context:
             norms = torch.empty(2, dtype=torch.float64, device=v.device)
         p = AdamWParams(*(float(params[k]) for k in ("alpha", "beta1", "beta2", "eps", "weight_decay")))
         _check(lib().tlfea_adamw_iteration(self.handle, _ptr(q_n), _ptr(v_n), _ptr(f_ext), float(h), int(l),
-                                           C.byref(p), _ptr(v), _ptr(m), _ptr(s), _ptr(g), _ptr(q), _ptr(f_int),
-                                           _ptr(norms), _stream(stream)))
+                                           C.byref(p), _ptr(lam), float(rho), _ptr(v), _ptr(m), _ptr(s), _ptr(g),
+                                           _ptr(q), _ptr(f_int), _ptr(norms), _stream(stream)))
         return q, norms
 
     def eval_host(self, x, v, v_n=None, f_ext=None, h=1e-3, g=None, H=None, f_int=None, stream=None):

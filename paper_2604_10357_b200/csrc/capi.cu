@@ -115,6 +115,7 @@ tlfea_status tlfea_info(tlfea_ctx ctx, tlfea_info_t* o) {
   o->device_bytes = c.device_bytes;
   o->n_geometry_classes = c.n_cls;
   o->fused_eval = fused_available(&c) ? 1 : 0;
+  o->n_constraints = c.n_con;
   return TLFEA_OK;
 }
 
@@ -236,6 +237,36 @@ tlfea_status tlfea_eval(tlfea_ctx ctx, const double* x, const double* v, const d
   return TLFEA_OK;
 }
 
+tlfea_status tlfea_eval_constrained(tlfea_ctx ctx, const double* x, const double* v, const double* v_n,
+                                    const double* f_ext, double h, const double* lambda, double rho, double* g_out,
+                                    double* H_out, double* f_int_out, void* stream) {
+  CTX_OR_FAIL(ctx);
+  Context& c = ctx->c;
+  if (!(rho >= 0.0)) return fail(TLFEA_E_INVALID, "tlfea_eval_constrained: rho must be >= 0");
+  TRY(tlfea_eval(ctx, x, v, v_n, f_ext, h, g_out, H_out, f_int_out, stream));
+  const cudaStream_t s = as_stream(stream);
+  TIMED(2, launch_constraint_terms(&c, x, lambda, rho, h, g_out, H_out, s));
+  return TLFEA_OK;
+}
+
+tlfea_status tlfea_constraint_residual(tlfea_ctx ctx, const double* q, double* c_out, void* stream) {
+  CTX_OR_FAIL(ctx);
+  Context& c = ctx->c;
+  if (c.n_con > 0 && (!q || !c_out)) return fail(TLFEA_E_INVALID, "tlfea_constraint_residual: NULL q or c_out");
+  TRY(use_device(c));
+  return launch_constraint_residual(&c, q, c_out, as_stream(stream));
+}
+
+tlfea_status tlfea_update_multipliers(tlfea_ctx ctx, const double* q, double rho, double* lambda, double* c_out,
+                                      void* stream) {
+  CTX_OR_FAIL(ctx);
+  Context& c = ctx->c;
+  if (!(rho >= 0.0)) return fail(TLFEA_E_INVALID, "tlfea_update_multipliers: rho must be >= 0");
+  if (c.n_con > 0 && (!q || !lambda)) return fail(TLFEA_E_INVALID, "tlfea_update_multipliers: NULL q or lambda");
+  TRY(use_device(c));
+  return launch_dual_update(&c, q, rho, lambda, c_out, as_stream(stream));
+}
+
 tlfea_status tlfea_force_only(tlfea_ctx ctx, const double* x, const double* v, double* f_int_out, void* stream) {
   CTX_OR_FAIL(ctx);
   Context& c = ctx->c;
@@ -251,12 +282,13 @@ tlfea_status tlfea_force_only(tlfea_ctx ctx, const double* x, const double* v, d
 }
 
 tlfea_status tlfea_adamw_iteration(tlfea_ctx ctx, const double* q_n, const double* v_n, const double* f_ext,
-                                   double h, int32_t l, const tlfea_adamw_params* params, double* v, double* m,
-                                   double* s_mom, double* g, double* q_out, double* f_int_out, double* norms_out,
-                                   void* stream) {
+                                   double h, int32_t l, const tlfea_adamw_params* params, const double* lambda,
+                                   double rho, double* v, double* m, double* s_mom, double* g, double* q_out,
+                                   double* f_int_out, double* norms_out, void* stream) {
   CTX_OR_FAIL(ctx);
   Context& c = ctx->c;
   TRY(check_h(h));
+  if (!(rho >= 0.0)) return fail(TLFEA_E_INVALID, "tlfea_adamw_iteration: rho must be >= 0");
   if (c.nranks > 1) return fail(TLFEA_E_INVALID, "tlfea_adamw_iteration: single-rank contexts only");
   if (l < 1) return fail(TLFEA_E_INVALID, "tlfea_adamw_iteration: iteration index l must be >= 1");
   if (!q_n || !v_n || !params || !v || !m || !s_mom || !g || !q_out)
@@ -269,6 +301,8 @@ tlfea_status tlfea_adamw_iteration(tlfea_ctx ctx, const double* q_n, const doubl
   // (iii)-(iv) Stage 1 + Stage 2 at q, (vi) gradient
   TIMED(0, launch_element_kernel(&c, q_out, v, false, s));
   TIMED(2, launch_gather_f(&c, v, v_n, f_ext, h, g, f_int_out, false, s));
+  // (v) constraint residual and its gradient term
+  TIMED(2, launch_constraint_terms(&c, q_out, lambda, rho, h, g, nullptr, s));
   // device ||g||, ||v|| for the inner stopping test
   if (norms_out) TIMED(2, launch_norms2(&c, g, v, norms_out, s));
   return TLFEA_OK;

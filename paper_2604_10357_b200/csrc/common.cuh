@@ -25,6 +25,12 @@ void count_launch(int n = 1);
                            std::string(#call) + ": " + cudaGetErrorString(err__)); \
   } while (0)
 
+#define TL_TRY_LAUNCH(expr)                    \
+  do {                                         \
+    const tlfea_status st_try__ = (expr);      \
+    if (st_try__ != TLFEA_OK) return st_try__; \
+  } while (0)
+
 #define TL_CHECK_LAUNCH()                                                      \
   do {                                                                         \
     ::tlfea::count_launch();                                                   \
@@ -155,6 +161,20 @@ struct Context {
   double* fpart = nullptr;       // [3 n_own] local partial force (partitioned mode)
   double* norm_part = nullptr;   // [2 x kNormBlocks] partial sums of the AdamW norms
 
+  // linear constraints c(q) = C q - b (NEXT-3, reading Q22; single rank)
+  int64_t n_con = 0;
+  int32_t* con_ptr = nullptr;    // [m+1] rows of C
+  int32_t* con_cols = nullptr;   // DOF columns
+  double* con_vals = nullptr;
+  double* con_b = nullptr;       // [m]
+  int32_t* conT_ptr = nullptr;   // [n_dof+1] rows of C^T (ascending constraint index)
+  int32_t* conT_rows = nullptr;
+  double* conT_vals = nullptr;
+  int64_t n_gram = 0;            // distinct (i, j) DOF pairs of C^T C
+  int64_t* gram_ij = nullptr;    // [n_gram] i << 32 | j (setup), then the H slot
+  double* gram_val = nullptr;    // [n_gram] sum_k C_ki C_kj (ascending k)
+  double* con_c = nullptr;       // [m] residual buffer
+
   // live timing (tlfea_set_timing)
   bool timing = false;
   struct TimedLaunch {
@@ -215,6 +235,11 @@ tlfea_status launch_residual(Context* c, const double* fint, const double* v, co
 tlfea_status launch_adamw_update(Context* c, int l, const tlfea_adamw_params& p, const double* g, double* m,
                                  double* s, double* v, const double* q_n, double h, double* q, cudaStream_t st);
 tlfea_status launch_norms2(Context* c, const double* a, const double* b, double* out, cudaStream_t st);
+tlfea_status launch_constraint_residual(Context* c, const double* q, double* c_out, cudaStream_t st);
+tlfea_status launch_constraint_terms(Context* c, const double* q, const double* lam, double rho, double h,
+                                     double* g, double* H, cudaStream_t st);
+tlfea_status launch_dual_update(Context* c, const double* q, double rho, double* lam, double* c_out,
+                                cudaStream_t st);
 tlfea_status launch_pack_send(Context* c, double* send, bool force_only, cudaStream_t s);
 tlfea_status launch_unpack_recv(Context* c, const double* recv, double h, double* H,
                                 bool force_only, cudaStream_t s);

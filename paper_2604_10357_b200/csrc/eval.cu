@@ -295,6 +295,83 @@ tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, cons
   return TLFEA_OK;
 }
 
+// ------------------------------------- linear constraints (NEXT-3, Q22)
+// c_k = C_k q - b_k, one thread per constraint (Alg. 2)
+__global__ void k_con_residual(int64_t m, const int32_t* __restrict__ ptr, const int32_t* __restrict__ cols,
+                               const double* __restrict__ vals, const double* __restrict__ b,
+                               const double* __restrict__ q, double* __restrict__ c) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  double s = -b[k];
+  for (int32_t p = ptr[k]; p < ptr[k + 1]; ++p) s += vals[p] * q[cols[p]];
+  c[k] = s;
+}
+
+// g_i += h sum_k C_ki (lambda_k + rho c_k) over the C^T row of DOF i, in
+// ascending k (one thread per DOF, no write conflicts)
+__global__ void k_con_grad(int64_t n_dof, const int32_t* __restrict__ tptr, const int32_t* __restrict__ trows,
+                           const double* __restrict__ tvals, const double* __restrict__ lam, double rho,
+                           const double* __restrict__ c, double h, double* __restrict__ g) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_dof) return;
+  const int32_t p0 = tptr[i], p1 = tptr[i + 1];
+  if (p0 == p1) return;
+  double gi = g[i];
+  for (int32_t p = p0; p < p1; ++p) {
+    const int32_t k = trows[p];
+    gi += h * tvals[p] * ((lam ? lam[k] : 0.0) + rho * c[k]);
+  }
+  g[i] = gi;
+}
+
+// H[slot] += h^2 rho (C^T C)_ij, one thread per distinct pair (P:541-543 without atomics)
+__global__ void k_con_hess(int64_t n, const int64_t* __restrict__ slot, const double* __restrict__ val,
+                           double h2rho, double* __restrict__ H) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) H[slot[t]] += h2rho * val[t];
+}
+
+// lambda_k += rho c_k (Eq. lambda_update)
+__global__ void k_con_dual(int64_t m, double rho, const double* __restrict__ c, double* __restrict__ lam) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < m) lam[k] += rho * c[k];
+}
+
+tlfea_status launch_constraint_residual(Context* c, const double* q, double* c_out, cudaStream_t st) {
+  if (c->n_con == 0) return TLFEA_OK;
+  k_con_residual<<<grid_for(c->n_con, 256), 256, 0, st>>>(c->n_con, c->con_ptr, c->con_cols, c->con_vals, c->con_b,
+                                                          q, c_out);
+  TL_CHECK_LAUNCH();
+  return TLFEA_OK;
+}
+
+tlfea_status launch_constraint_terms(Context* c, const double* q, const double* lam, double rho, double h,
+                                     double* g, double* H, cudaStream_t st) {
+  if (c->n_con == 0) return TLFEA_OK;
+  TL_TRY_LAUNCH(launch_constraint_residual(c, q, c->con_c, st));
+  if (g) {
+    const int64_t n_dof = 3 * c->n_coef;
+    k_con_grad<<<grid_for(n_dof, 256), 256, 0, st>>>(n_dof, c->conT_ptr, c->conT_rows, c->conT_vals, lam, rho,
+                                                     c->con_c, h, g);
+    TL_CHECK_LAUNCH();
+  }
+  if (H && c->n_gram > 0) {
+    k_con_hess<<<grid_for(c->n_gram, 256), 256, 0, st>>>(c->n_gram, c->gram_ij, c->gram_val, h * h * rho, H);
+    TL_CHECK_LAUNCH();
+  }
+  return TLFEA_OK;
+}
+
+tlfea_status launch_dual_update(Context* c, const double* q, double rho, double* lam, double* c_out,
+                                cudaStream_t st) {
+  if (c->n_con == 0) return TLFEA_OK;
+  double* cbuf = c_out ? c_out : c->con_c;
+  TL_TRY_LAUNCH(launch_constraint_residual(c, q, cbuf, st));
+  k_con_dual<<<grid_for(c->n_con, 256), 256, 0, st>>>(c->n_con, rho, cbuf, lam);
+  TL_CHECK_LAUNCH();
+  return TLFEA_OK;
+}
+
 // ------------------------------------------------ AdamW (Alg. 2, NEXT-2)
 // One thread per DOF: moments, bias correction, velocity update with
 // decoupled weight decay, backward-Euler step map.

@@ -830,6 +830,133 @@ static tlfea_status validate(const tlfea_mesh* mesh, const tlfea_material* mat,
     return fail(TLFEA_E_INVALID, "bad rank / nranks");
   if (mesh->n_elements >= (1ll << 24)) return fail(TLFEA_E_OVERFLOW, "n_elements >= 2^24 (packed gather entries)");
   if (3 * mesh->n_coef >= (1ll << 31)) return fail(TLFEA_E_OVERFLOW, "3 n_coef >= 2^31");
+  if (const tlfea_constraints* k = opts->constraints) {
+    if (k->m < 0) return fail(TLFEA_E_INVALID, "constraints: m < 0");
+    if (k->m > 0) {
+      if (opts->nranks != 1) return fail(TLFEA_E_UNSUPPORTED, "constraints: single-rank contexts only");
+      if (!k->rowptr || !k->b) return fail(TLFEA_E_INVALID, "constraints: NULL rowptr or b");
+      if (k->rowptr[0] != 0) return fail(TLFEA_E_INVALID, "constraints: rowptr[0] != 0");
+      for (int64_t r = 0; r < k->m; ++r)
+        if (k->rowptr[r + 1] < k->rowptr[r]) return fail(TLFEA_E_INVALID, "constraints: rowptr decreases");
+      const int64_t nz = k->rowptr[k->m];
+      if (nz >= (1ll << 31)) return fail(TLFEA_E_OVERFLOW, "constraints: nnz >= 2^31");
+      if (nz > 0 && (!k->cols || !k->vals)) return fail(TLFEA_E_INVALID, "constraints: NULL cols or vals");
+      for (int64_t r = 0; r < k->m; ++r)
+        for (int64_t p = k->rowptr[r]; p < k->rowptr[r + 1]; ++p) {
+          if (k->cols[p] < 0 || k->cols[p] >= 3 * mesh->n_coef)
+            return fail(TLFEA_E_INVALID, "constraints: DOF id out of range in row " + std::to_string(r));
+          for (int64_t p2 = k->rowptr[r]; p2 < p; ++p2)
+            if (k->cols[p2] == k->cols[p])
+              return fail(TLFEA_E_INVALID, "constraints: repeated DOF in row " + std::to_string(r));
+        }
+    }
+  }
+  return TLFEA_OK;
+}
+
+// Coefficient couplings (I, J) of every constraint row, as pattern keys
+// (single rank: owned row = I), ascending and unique.
+static std::vector<unsigned long long> constraint_keys(const tlfea_constraints* k) {
+  std::vector<unsigned long long> keys;
+  if (!k) return keys;
+  for (int64_t r = 0; r < k->m; ++r) {
+    std::vector<int64_t> coefs;
+    for (int64_t p = k->rowptr[r]; p < k->rowptr[r + 1]; ++p) coefs.push_back(k->cols[p] / 3);
+    for (int64_t I : coefs)
+      for (int64_t J : coefs) keys.push_back(((unsigned long long)I << 32) | (unsigned long long)J);
+  }
+  std::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  return keys;
+}
+
+// DOF slot of each C^T C pair (i << 32 | j) in the final pattern (binary
+// search over the coefficient row), written in place.
+__global__ void k_gram_slots(int64_t n, const int32_t* __restrict__ rowptr_c, const int32_t* __restrict__ cols_c,
+                             int64_t* __restrict__ ij) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t i = ij[t] >> 32, j = ij[t] & 0xffffffff;
+  const int32_t I = (int32_t)(i / 3), J = (int32_t)(j / 3);
+  int32_t lo = rowptr_c[I], hi = rowptr_c[I + 1];
+  const int32_t b0 = lo, deg = hi - lo;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (cols_c[mid] < J) lo = mid + 1;
+    else hi = mid;
+  }
+  ij[t] = 9 * (int64_t)b0 + 3 * (i % 3) * deg + 3 * (int64_t)(lo - b0) + (j % 3);
+}
+
+// C, C^T (entries of a DOF row in ascending constraint order) and the
+// distinct C^T C pairs with their sums over ascending constraint index.
+static tlfea_status setup_constraints(Context* c, const tlfea_constraints* k) {
+  if (!k || k->m == 0) return TLFEA_OK;
+  const int64_t m = k->m, nz = k->rowptr[m], n_dof = 3 * c->n_coef;
+  c->n_con = m;
+  std::vector<int32_t> ptr(m + 1), cols(nz), tptr(n_dof + 1, 0), trows(nz);
+  std::vector<double> tvals(nz);
+  for (int64_t r = 0; r <= m; ++r) ptr[r] = (int32_t)k->rowptr[r];
+  for (int64_t p = 0; p < nz; ++p) {
+    cols[p] = (int32_t)k->cols[p];
+    tptr[cols[p] + 1]++;
+  }
+  for (int64_t i = 0; i < n_dof; ++i) tptr[i + 1] += tptr[i];
+  {
+    std::vector<int32_t> fill(tptr.begin(), tptr.end() - 1);
+    for (int64_t r = 0; r < m; ++r)
+      for (int64_t p = k->rowptr[r]; p < k->rowptr[r + 1]; ++p) {
+        const int32_t q = fill[cols[p]]++;
+        trows[q] = (int32_t)r;
+        tvals[q] = k->vals[p];
+      }
+  }
+  std::vector<std::pair<int64_t, double>> gram;
+  {
+    std::vector<std::pair<int64_t, double>> terms;  // (i << 32 | j, C_ki C_kj) in ascending k
+    for (int64_t r = 0; r < m; ++r)
+      for (int64_t p1 = k->rowptr[r]; p1 < k->rowptr[r + 1]; ++p1)
+        for (int64_t p2 = k->rowptr[r]; p2 < k->rowptr[r + 1]; ++p2)
+          terms.push_back({(k->cols[p1] << 32) | k->cols[p2], k->vals[p1] * k->vals[p2]});
+    std::stable_sort(terms.begin(), terms.end(),
+                     [](const std::pair<int64_t, double>& a, const std::pair<int64_t, double>& b) {
+                       return a.first < b.first;
+                     });
+    for (auto& t : terms) {
+      if (!gram.empty() && gram.back().first == t.first) gram.back().second += t.second;
+      else gram.push_back(t);
+    }
+  }
+  c->n_gram = (int64_t)gram.size();
+  std::vector<int64_t> gij(c->n_gram);
+  std::vector<double> gval(c->n_gram);
+  for (int64_t t = 0; t < c->n_gram; ++t) {
+    gij[t] = gram[t].first;
+    gval[t] = gram[t].second;
+  }
+  TL_TRY(c->alloc(&c->con_ptr, (size_t)m + 1));
+  TL_TRY(c->alloc(&c->con_cols, (size_t)std::max<int64_t>(nz, 1)));
+  TL_TRY(c->alloc(&c->con_vals, (size_t)std::max<int64_t>(nz, 1)));
+  TL_TRY(c->alloc(&c->con_b, (size_t)m));
+  TL_TRY(c->alloc(&c->con_c, (size_t)m));
+  TL_TRY(c->alloc(&c->conT_ptr, (size_t)n_dof + 1));
+  TL_TRY(c->alloc(&c->conT_rows, (size_t)std::max<int64_t>(nz, 1)));
+  TL_TRY(c->alloc(&c->conT_vals, (size_t)std::max<int64_t>(nz, 1)));
+  TL_TRY(c->alloc(&c->gram_ij, (size_t)std::max<int64_t>(c->n_gram, 1)));
+  TL_TRY(c->alloc(&c->gram_val, (size_t)std::max<int64_t>(c->n_gram, 1)));
+  TL_CUDA(cudaMemcpy(c->con_ptr, ptr.data(), sizeof(int32_t) * (m + 1), cudaMemcpyHostToDevice));
+  TL_CUDA(cudaMemcpy(c->con_cols, cols.data(), sizeof(int32_t) * nz, cudaMemcpyHostToDevice));
+  TL_CUDA(cudaMemcpy(c->con_vals, k->vals, sizeof(double) * nz, cudaMemcpyHostToDevice));
+  TL_CUDA(cudaMemcpy(c->con_b, k->b, sizeof(double) * m, cudaMemcpyHostToDevice));
+  TL_CUDA(cudaMemcpy(c->conT_ptr, tptr.data(), sizeof(int32_t) * (n_dof + 1), cudaMemcpyHostToDevice));
+  TL_CUDA(cudaMemcpy(c->conT_rows, trows.data(), sizeof(int32_t) * nz, cudaMemcpyHostToDevice));
+  TL_CUDA(cudaMemcpy(c->conT_vals, tvals.data(), sizeof(double) * nz, cudaMemcpyHostToDevice));
+  TL_CUDA(cudaMemcpy(c->gram_ij, gij.data(), sizeof(int64_t) * c->n_gram, cudaMemcpyHostToDevice));
+  TL_CUDA(cudaMemcpy(c->gram_val, gval.data(), sizeof(double) * c->n_gram, cudaMemcpyHostToDevice));
+  if (c->n_gram > 0) {
+    k_gram_slots<<<grid_for(c->n_gram, 256), 256>>>(c->n_gram, c->rowptr_c, c->cols_c, c->gram_ij);
+    TL_CHECK_LAUNCH();
+  }
   return TLFEA_OK;
 }
 
@@ -1000,13 +1127,21 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   TL_TRY(build_geometry_classes(c));
 
   // ---- a-2 pattern over setup elements (64-bit keys, sort, unique)
-  const int64_t nkeys = NS * nen * nen;
+  // constraint couplings join the element keys (pattern union)
+  const std::vector<unsigned long long> ckeys = constraint_keys(opts->constraints);
+  const int64_t nekeys = NS * nen * nen;
+  const int64_t nkeys = nekeys + (int64_t)ckeys.size();
   {
     TmpArr<unsigned long long> keys, keys2;
     TL_TRY(keys.get(nkeys));
     TL_TRY(keys2.get(nkeys));
-    k_keys<<<grid_for(nkeys, 256), 256>>>(NS, nen, dsconn.p, c->own_idx, keys.p);
-    TL_CHECK_LAUNCH();
+    if (nekeys > 0) {
+      k_keys<<<grid_for(nekeys, 256), 256>>>(NS, nen, dsconn.p, c->own_idx, keys.p);
+      TL_CHECK_LAUNCH();
+    }
+    if (!ckeys.empty())
+      TL_CUDA(cudaMemcpy(keys.p + nekeys, ckeys.data(), sizeof(unsigned long long) * ckeys.size(),
+                         cudaMemcpyHostToDevice));
     Tmp tmp;
     size_t bytes = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys.p, keys2.p, (int64_t)nkeys);
@@ -1052,6 +1187,7 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   } else {
     TL_CUDA(cudaMemset(c->rowptr, 0, sizeof(int32_t)));
   }
+  TL_TRY(setup_constraints(c, opts->constraints));
 
   // ---- slot map of local elements + H gather lists (the slot map replaces the
   // paper's binary search at P:520)
