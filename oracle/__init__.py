@@ -63,6 +63,8 @@ def _declare(L):
     L.orc_t10_shape_csd.argtypes = [_d, i, _d]
     L.orc_ancf_shape.argtypes = [_d, _d, _d, _d]
     L.orc_ancf_shape_csd.argtypes = [_d, _d, i, _d]
+    L.orc_beam_shape.argtypes = [_d, _d, _d, _d]
+    L.orc_beam_shape_csd.argtypes = [_d, _d, i, _d]
     L.orc_precompute.argtypes = [i, i, i64, _i32, _d, _d, _d, _d]
     L.orc_precompute.restype = i64
     L.orc_coef_pattern.argtypes = [i, i64, _i32, i64, _i64, _i64]
@@ -112,7 +114,7 @@ def mat_array(mat: dict) -> np.ndarray:
 
 
 def n_en(elem: int) -> int:
-    return 10 if elem == 0 else 16
+    return {0: 10, 1: 16, 2: 8}[int(elem)]
 
 
 # ------------------------------------------------------------ primitives --
@@ -151,6 +153,22 @@ def ancf_shape_csd(xi, LWH, direction: int):
     xi, LWH = _f64(xi), _f64(LWH)
     out = np.zeros(16)
     lib().orc_ancf_shape_csd(_p(xi), _p(LWH), direction, _p(out))
+    return out
+
+
+def beam_shape(xi, LWH):
+    """ANCF3243 basis (reading Q23): S [8], dS/dxi [8][3]."""
+    xi, LWH = _f64(xi), _f64(LWH)
+    S = np.zeros(8)
+    dS = np.zeros((8, 3))
+    lib().orc_beam_shape(_p(xi), _p(LWH), _p(S), _p(dS))
+    return S, dS
+
+
+def beam_shape_csd(xi, LWH, direction: int):
+    xi, LWH = _f64(xi), _f64(LWH)
+    out = np.zeros(8)
+    lib().orc_beam_shape_csd(_p(xi), _p(LWH), direction, _p(out))
     return out
 
 

@@ -73,6 +73,20 @@ int quadrature(int rule, double pts[][3], double* w) {
         }
     return n;
   }
+  if (rule == 3) {  // Gauss-Legendre 3 x 2 x 2 on [-1,1]^3 (ANCF3243), xi-major
+    const double g3[3] = {-std::sqrt(3.0 / 5.0), 0.0, std::sqrt(3.0 / 5.0)};
+    const double w3[3] = {5.0 / 9.0, 8.0 / 9.0, 5.0 / 9.0};
+    const double g2[2] = {-1.0 / std::sqrt(3.0), 1.0 / std::sqrt(3.0)};
+    int n = 0;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 2; ++j)
+        for (int k = 0; k < 2; ++k) {
+          pts[n][0] = g3[i]; pts[n][1] = g2[j]; pts[n][2] = g2[k];
+          w[n] = w3[i];
+          ++n;
+        }
+    return n;
+  }
   return -1;
 }
 
@@ -131,15 +145,49 @@ void ancf_shape(const T xi3[3], const double LWH[3], T S[16], T dS[16][3]) {
   }
 }
 
-int n_en_of(int elem) { return elem == 0 ? 10 : 16; }
+// ANCF3243 beam (reading Q23): nodes A (xi = -1) and B (xi = +1), local
+// coefficient 4k+m, m = (r, r_x, r_y, r_z); xi, eta, zeta in [-1,1] span L,
+// W, H. Cubic Hermite along the axis for (r, r_x), linear for (r_y, r_z):
+//   S_r^A = (xi^3 - 3 xi + 2)/4,        S_r^B = (-xi^3 + 3 xi + 2)/4,
+//   S_x^A = L (xi^3 - xi^2 - xi + 1)/8,  S_x^B = L (xi^3 + xi^2 - xi - 1)/8,
+//   S_y^k = W eta (1 -+ xi)/4,          S_z^k = H zeta (1 -+ xi)/4.
+template <class T>
+void beam_shape(const T xi3[3], const double LWH[3], T S[8], T dS[8][3]) {
+  const T xi = xi3[0], eta = xi3[1], zeta = xi3[2];
+  const double L = LWH[0], W = LWH[1], H = LWH[2];
+  for (int k = 0; k < 2; ++k) {
+    const double s = k == 0 ? -1.0 : 1.0;  // node side
+    const T lin = 1.0 + s * xi;             // 1 - xi (A), 1 + xi (B)
+    S[4 * k + 0] = 0.25 * (s * (-xi * xi * xi + 3.0 * xi) + 2.0);
+    dS[4 * k + 0][0] = 0.25 * s * (-3.0 * xi * xi + 3.0);
+    dS[4 * k + 0][1] = T(0.0);
+    dS[4 * k + 0][2] = T(0.0);
+    S[4 * k + 1] = (L / 8.0) * (xi * xi * xi + s * xi * xi - xi - s);
+    dS[4 * k + 1][0] = (L / 8.0) * (3.0 * xi * xi + 2.0 * s * xi - 1.0);
+    dS[4 * k + 1][1] = T(0.0);
+    dS[4 * k + 1][2] = T(0.0);
+    S[4 * k + 2] = (W / 4.0) * eta * lin;
+    dS[4 * k + 2][0] = (W / 4.0) * eta * s;
+    dS[4 * k + 2][1] = (W / 4.0) * lin;
+    dS[4 * k + 2][2] = T(0.0);
+    S[4 * k + 3] = (H / 4.0) * zeta * lin;
+    dS[4 * k + 3][0] = (H / 4.0) * zeta * s;
+    dS[4 * k + 3][1] = T(0.0);
+    dS[4 * k + 3][2] = (H / 4.0) * lin;
+  }
+}
 
-// Coefficient ids of element e (ANCF: node k -> 4k .. 4k+3).
+int n_en_of(int elem) { return elem == 0 ? 10 : (elem == 1 ? 16 : 8); }
+
+// Coefficient ids of element e (ANCF: node k -> 4k .. 4k+3; 4 nodes for the
+// shell, 2 for the beam).
 void elem_coefs(int elem, const int32_t* conn, int64_t e, int64_t out[16]) {
   if (elem == 0) {
     for (int a = 0; a < 10; ++a) out[a] = conn[e * 10 + a];
   } else {
-    for (int k = 0; k < 4; ++k)
-      for (int m = 0; m < 4; ++m) out[4 * k + m] = 4 * (int64_t)conn[e * 4 + k] + m;
+    const int nn = elem == 1 ? 4 : 2;
+    for (int k = 0; k < nn; ++k)
+      for (int m = 0; m < 4; ++m) out[4 * k + m] = 4 * (int64_t)conn[e * nn + k] + m;
   }
 }
 
@@ -318,8 +366,10 @@ double geom_at(int elem, const double* X, const int64_t* cf, const double* LWH,
       N[a] = N10[a];
       for (int k = 0; k < 3; ++k) dN[a][k] = dN10[a][k];
     }
-  } else {
+  } else if (elem == 1) {
     ancf_shape(xi, LWH, N, dN);
+  } else {
+    beam_shape(xi, LWH, N, dN);
   }
   double J[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int a = 0; a < nen; ++a)
@@ -340,7 +390,7 @@ double geom_at(int elem, const double* X, const int64_t* cf, const double* LWH,
 }
 
 const double* dims_of(int elem, const double* dims, int64_t e) {
-  return elem == 1 ? dims + 3 * e : nullptr;
+  return elem != 0 ? dims + 3 * e : nullptr;
 }
 
 // ------------------------------------------------------- element routines --
@@ -507,7 +557,22 @@ void element_mass(int elem, int rule, int mass_rule, double rho, const double* X
     return;
   }
   double pts[48][3], w[48];
-  const int nq = quadrature(rule, pts, w);
+  int nq = quadrature(rule, pts, w);
+  if (elem == 2 && mass_rule == 0) {
+    // exact beam mass (reading Q4 / Q23): N_a N_b det J has degree <= 10 in
+    // xi and <= 3 in eta, zeta -> Gauss-Legendre 6 x 2 x 2
+    double g6[6], w6[6];
+    gauss_legendre(6, g6, w6);
+    const double g2 = 1.0 / std::sqrt(3.0);
+    nq = 0;
+    for (int i = 0; i < 6; ++i)
+      for (int j = 0; j < 2; ++j)
+        for (int k = 0; k < 2; ++k) {
+          pts[nq][0] = g6[i]; pts[nq][1] = j ? g2 : -g2; pts[nq][2] = k ? g2 : -g2;
+          w[nq] = w6[i];
+          ++nq;
+        }
+  }
   for (int r = 0; r < nen * nen; ++r) me[r] = 0.0;
   for (int q = 0; q < nq; ++q) {
     double gN[16][3], N[16];
@@ -563,6 +628,20 @@ void orc_ancf_shape_csd(const double* xi, const double* LWH, int dir, double* dS
   x[dir] += cplx(0.0, 1e-30);
   ancf_shape(x, LWH, S, d);
   for (int a = 0; a < 16; ++a) dSdir[a] = S[a].imag() / 1e-30;
+}
+
+void orc_beam_shape(const double* xi, const double* LWH, double* S, double* dS) {
+  double d[8][3];
+  beam_shape(xi, LWH, S, d);
+  for (int a = 0; a < 8; ++a)
+    for (int k = 0; k < 3; ++k) dS[3 * a + k] = d[a][k];
+}
+
+void orc_beam_shape_csd(const double* xi, const double* LWH, int dir, double* dSdir) {
+  cplx x[3] = {xi[0], xi[1], xi[2]}, S[8], d[8][3];
+  x[dir] += cplx(0.0, 1e-30);
+  beam_shape(x, LWH, S, d);
+  for (int a = 0; a < 8; ++a) dSdir[a] = S[a].imag() / 1e-30;
 }
 
 // a-1: gradN [n_el][nq][nen][3], J0w [n_el][nq]. Returns -1 on

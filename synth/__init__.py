@@ -62,7 +62,7 @@ class Mesh:
         if self.element == 0:
             return self.conn
         c = self.conn.astype(np.int64)
-        out = (4 * c[:, :, None] + np.arange(4)[None, None, :]).reshape(c.shape[0], 16)
+        out = (4 * c[:, :, None] + np.arange(4)[None, None, :]).reshape(c.shape[0], 4 * c.shape[1])
         return out.astype(np.int32)
 
 
@@ -136,6 +136,22 @@ def ancf_plate(n: int, Lx: float = 4.0, Ly: float = 2.0, H: float = 0.1) -> Mesh
     return Mesh(1, X.reshape(-1, 3), conn.astype(np.int32), dims, name=f"ancf{n}x{n}")
 
 
+def ancf_beam(n: int, L: float = 0.2, W: float = 0.1, H: float = 0.1) -> Mesh:
+    """Chain of n ANCF3243 beam elements along x (§5.3):
+    element e spans nodes e and e+1, uniform L, rectangular W x H section.
+    Coefficients per node: r = (x, 0, 0), r_x = e1, r_y = e2, r_z = e3
+    (straight reference, reading Q23)."""
+    nn = n + 1
+    X = np.zeros((nn, 4, 3))
+    X[:, 0, 0] = np.arange(nn) * L
+    X[:, 1, 0] = 1.0
+    X[:, 2, 1] = 1.0
+    X[:, 3, 2] = 1.0
+    conn = np.stack([np.arange(n), np.arange(1, nn)], axis=1).astype(np.int32)
+    dims = np.tile(np.array([L, W, H]), (n, 1))
+    return Mesh(2, X.reshape(-1, 3), conn, dims, name=f"beam{n}")
+
+
 def clamped_dofs_t10(mesh: Mesh, tol: float = 1e-12) -> int:
     """DOFs on the x = 0 face (the clamped end of the paper's beams)."""
     return int(3 * np.count_nonzero(np.abs(mesh.X[:, 0]) < tol))
@@ -201,14 +217,16 @@ def t10_state(mesh: Mesh, seed: int = SEED_BASE, bend: float = 0.02,
 
 
 def ancf_state(mesh: Mesh, seed: int = SEED_BASE, delta: float = 0.04,
-               noise: float = 1e-3, vel: float = 0.05):
-    """Coefficients = exact position and gradients of phi(X) = X + (0,0,delta (x/4)^2)
-    at the nodes, plus N(0, noise^2) relative noise."""
+               noise: float = 1e-3, vel: float = 0.05, length: float = 4.0):
+    """Coefficients = exact position and gradients of
+    phi(X) = X + (0, 0, delta (x/length)^2) at the nodes, plus N(0, noise^2)
+    relative noise (length = 4 for the 4 x 2 plate; the beam
+    chain uses its own length, delta scaled with it)."""
     Xc = mesh.X.reshape(-1, 4, 3)
     pos = Xc[:, 0, :]
     q = Xc.copy()
-    q[:, 0, 2] = pos[:, 2] + delta * (pos[:, 0] / 4.0) ** 2
-    q[:, 1, 2] = 2.0 * delta * pos[:, 0] / 16.0
+    q[:, 0, 2] = pos[:, 2] + delta * (pos[:, 0] / length) ** 2
+    q[:, 1, 2] = 2.0 * delta * pos[:, 0] / (length * length)
     L = float(mesh.dims[0, 0]) if mesh.dims is not None else 1.0
     rng = np.random.default_rng(seed + 0)
     q[:, 0, :] += rng.normal(0.0, noise * L, size=pos.shape)
