@@ -64,15 +64,17 @@ typedef enum {
   TLFEA_E_UNSUPPORTED = 7       /* valid request this build does not provide  */
 } tlfea_status;
 
-typedef enum { TLFEA_T10 = 0, TLFEA_ANCF3443 = 1 } tlfea_element;
+typedef enum { TLFEA_T10 = 0, TLFEA_ANCF3443 = 1, TLFEA_ANCF3243 = 2 } tlfea_element;
 
 /* Quadrature rules. T10: 4-point degree-2 rule (BASELINE config 1)
  * or the 5-point Keast rule (negative centroid weight); ANCF3443: 4x4x3
- * Gauss-Legendre, points ordered xi-major, eta, zeta-minor. */
+ * Gauss-Legendre; ANCF3243 beam: 3x2x2
+ * Gauss-Legendre; product rules ordered xi-major, eta, zeta-minor. */
 typedef enum {
   TLFEA_Q_T10_4PT = 0,
   TLFEA_Q_T10_KEAST5 = 1,
-  TLFEA_Q_GL_4x4x3 = 2
+  TLFEA_Q_GL_4x4x3 = 2,
+  TLFEA_Q_GL_3x2x2 = 3
 } tlfea_quadrature;
 
 typedef enum { TLFEA_SVK = 0, TLFEA_MOONEY_RIVLIN = 1 } tlfea_model;
@@ -100,7 +102,10 @@ typedef struct {
  *            (xi,eta)=(-1,-1); X_ref [n_coef][3] with n_coef = 4*n_nodes and
  *            coefficient 4*node+m = (r, r_x, r_y, r_z)[m] (reading Q11).
  *            ancf_dims [n_elements][3] = (L, W, H) per element, or NULL to
- *            use options.ancf_dims for every element. */
+ *            use options.ancf_dims for every element.
+ *  ANCF3243: conn [n_elements][2] physical node ids (A at xi = -1, B at
+ *            xi = +1); X_ref and ancf_dims as for ANCF3443 (reading Q23:
+ *            cubic Hermite (r, r_x) along the axis, linear (r_y, r_z)). */
 typedef struct {
   int32_t element; /* tlfea_element */
   int64_t n_elements;

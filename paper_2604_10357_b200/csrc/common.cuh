@@ -44,15 +44,23 @@ void count_launch(int n = 1);
 constexpr int kMaxQP = 48;
 constexpr int kMaxEN = 16;
 
-inline int n_en_of(int element) { return element == TLFEA_T10 ? 10 : 16; }
+inline int n_en_of(int element) { return element == TLFEA_T10 ? 10 : element == TLFEA_ANCF3443 ? 16 : 8; }
+// physical nodes per element in the caller's connectivity
+inline int n_nodes_of(int element) { return element == TLFEA_T10 ? 10 : element == TLFEA_ANCF3443 ? 4 : 2; }
 inline int n_qp_of(int quadrature) {
-  return quadrature == TLFEA_Q_T10_4PT ? 4 : quadrature == TLFEA_Q_T10_KEAST5 ? 5 : 48;
+  return quadrature == TLFEA_Q_T10_4PT ? 4
+         : quadrature == TLFEA_Q_T10_KEAST5 ? 5
+         : quadrature == TLFEA_Q_GL_3x2x2 ? 12
+                                          : 48;
 }
 // number of upper-triangular 3x3 blocks (a <= b) of the element matrix
 inline int n_ublk_of(int nen) { return nen * (nen + 1) / 2; }
-// element-kernel CTA tile: kElWarps warps, 3 T10 elements or 1 ANCF element per warp
+// element-kernel CTA tile: kElWarps warps of 3 T10 / 1 ANCF3443 / 4 ANCF3243 elements
 constexpr int kElWarps = 4;
-inline int el_per_tile(int element) { return kElWarps * (element == TLFEA_T10 ? 3 : 1); }// gather CTA: 4 warps of 32 units (H) / 128 threads (f)
+inline int el_per_tile(int element) {
+  return kElWarps * (element == TLFEA_T10 ? 3 : element == TLFEA_ANCF3443 ? 1 : 4);
+}
+// gather CTA: 4 warps of 32 units (H) / 128 threads (f)
 constexpr int kGatherThreads = 128;
 
 // Packed contribution entry of the H gather: element (local id) << 8 | a << 4 | b

@@ -41,6 +41,10 @@ template <>
 struct Geo<1> {  // ANCF3443
   static constexpr int NEN = 16, GROUP = 32, EPW = 1, NUB = 136, NB = 5;
 };
+template <>
+struct Geo<2> {  // ANCF3243 beam: 8 lanes per element, 4 elements per warp
+  static constexpr int NEN = 8, GROUP = 8, EPW = 4, NUB = 36, NB = 5;
+};
 
 __host__ __device__ __forceinline__ int ublk(int n, int a, int b) {  // a <= b
   return a * n - (a * (a - 1)) / 2 + (b - a);
@@ -55,6 +59,9 @@ __device__ __forceinline__ int partner(int a, int half, int j) {
   if (ELEM == 0) {
     if (j < 5) return (a + j) % 10;
     return a < 5 ? a + 5 : -1;
+  } else if (ELEM == 2) {
+    if (j < 4) return (a + j) & 7;
+    return a < 4 ? a + 4 : -1;
   } else {
     if (half == 0) return j < 4 ? (a + j) & 15 : -1;
     if (j < 4) return (a + 4 + j) & 15;
@@ -85,7 +92,9 @@ __host__ __device__ constexpr int el_npass() {
 
 template <int ELEM, int MODEL, int NPASS>
 __host__ __device__ constexpr int el_minb() {
-  return (ELEM == 0 && MODEL == 0) ? (NPASS == 1 ? TLFEA_T10_MINB : TLFEA_T10_MINB2P) : (NPASS == 1 ? 2 : 3);
+  return (ELEM == 0 && MODEL == 0)   ? (NPASS == 1 ? TLFEA_T10_MINB : TLFEA_T10_MINB2P)
+         : (ELEM == 2 && MODEL == 0) ? 3
+                                     : (NPASS == 1 ? 2 : 3);
 }
 
 // Element arguments shared by k_element and the fused persistent kernel.
@@ -147,11 +156,14 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
   const int32_t* __restrict__ fdest = A.fdest;
   unsigned long long* __restrict__ err = A.err;
 
+  // MULTI: several elements per warp, one lane per element node (T10, beam);
+  // otherwise one element per warp, two lanes per node (ANCF3443)
+  constexpr bool MULTI = ELEM != 1;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const bool lane_active = ELEM == 0 ? (lane < EPW * GROUP) : true;
-  const int g = (ELEM == 0 && lane_active) ? lane / GROUP : 0;
-  const int a = ELEM == 0 ? (lane_active ? lane % GROUP : 0) : (lane & 15);
-  const int half = ELEM == 0 ? 0 : (lane >> 4);
+  const bool lane_active = MULTI ? (lane < EPW * GROUP) : true;
+  const int g = (MULTI && lane_active) ? lane / GROUP : 0;
+  const int a = MULTI ? (lane_active ? lane % GROUP : 0) : (lane & 15);
+  const int half = MULTI ? 0 : (lane >> 4);
   const int64_t e = grp * EPW + g;
   const bool valid = lane_active && e < n_el;
   const int gbase = g * GROUP;
@@ -225,6 +237,16 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
           const double* pd = &s_part[wib][9 + a][gbase];
           s_F[wib][g][9 + a] =
               (((pd[0] + pd[1]) + (pd[2] + pd[3])) + ((pd[4] + pd[5]) + (pd[6] + pd[7]))) + (pd[8] + pd[9]);
+        }
+      }
+    } else if (ELEM == 2) {
+      // 8 lanes, 9 (18) components: lane a reduces components a, a + 8, ...
+#pragma unroll
+      for (int cc = 0; cc < (KV ? 3 : 2); ++cc) {
+        const int comp = a + 8 * cc;
+        if (comp < NC) {
+          const double* p = &s_part[wib][comp][gbase];
+          s_F[wib][g][comp] = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
         }
       }
     } else {
@@ -320,8 +342,8 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
         }
       } else {
         // MR: material tangent columns (6 lanes per element), B_a, w C B_a
-        if (lane_active && (ELEM == 0 || half == 0)) {
-          const int col = ELEM == 0 ? a : lane;
+        if (lane_active && (MULTI || half == 0)) {
+          const int col = MULTI ? a : lane;
           if (col < 6) {
             double cc[6];
             mr_Cv_column_dispatch(ms, mat.C10, mat.C01, mat.kappa, col, cc);
@@ -383,7 +405,7 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
     __syncwarp();
   }
 
-  if (valid && pass == 0 && (ELEM == 0 || half == 0)) {
+  if (valid && pass == 0 && (MULTI || half == 0)) {
     const int64_t fp = fdest ? (int64_t)fdest[e * NEN + a] : e * NEN + a;
     double* fo = fscr + fp * 3;
     fo[0] = fa[0];
@@ -399,7 +421,7 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
   if (TAN && !mat.dbg_nowrite) {
     __shared__ int32_t s_pos[kWarps][32];  // block position (< 2^31, checked at setup)
     // store mapping: lane = 9 bi + r writes entry r of block 3 it + bi
-    constexpr int NLB = ELEM == 0 ? EPW * GROUP : 32;  // lanes holding blocks
+    constexpr int NLB = MULTI ? EPW * GROUP : 32;  // lanes holding blocks
     constexpr int NIT = (NLB + 2) / 3;
     const int bi = lane / 9, rr = lane - 9 * (lane / 9);
     if (DAX && dest) {
@@ -1304,6 +1326,7 @@ tlfea_status launch_element_kernel(Context* c, const double* x, const double* v,
     if (c->nq == 4) return launch_el_model<0, 4>(c, x, v, tangent, s);
     return launch_el_model<0, 5>(c, x, v, tangent, s);
   }
+  if (c->element == TLFEA_ANCF3243) return launch_el_model<2, 12>(c, x, v, tangent, s);
   return launch_el_model<1, 48>(c, x, v, tangent, s);
 }
 

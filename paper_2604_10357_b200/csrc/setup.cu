@@ -117,8 +117,10 @@ __global__ void k_precompute(int element, int64_t n_el, int nq, int nen, const i
   const double xi[3] = {qxi[3 * q], qxi[3 * q + 1], qxi[3 * q + 2]};
   if (element == TLFEA_T10) {
     t10_shape(xi, nullptr, dN);
-  } else {
+  } else if (element == TLFEA_ANCF3443) {
     ancf_shape(xi, dims + 3 * e, nullptr, dN);
+  } else {
+    beam_shape(xi, dims + 3 * e, nullptr, dN);
   }
   // J = sum_a (X_a - X_o) (x) dN_a/dxi over position coefficients (sum_a dN_a = 0
   // for them), so the element's absolute placement does not enter the rounding:
@@ -288,8 +290,10 @@ __global__ void k_element_mass(int element, int64_t n_el, int nen, int nq, const
     const double xi[3] = {qxi[3 * q], qxi[3 * q + 1], qxi[3 * q + 2]};
     if (element == TLFEA_T10)
       t10_shape(xi, N, dN);
-    else
+    else if (element == TLFEA_ANCF3443)
       ancf_shape(xi, dims + 3 * e, N, dN);
+    else
+      beam_shape(xi, dims + 3 * e, N, dN);
     double J[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int a = 0; a < nen; ++a) {
       const int64_t I = conn[e * nen + a];
@@ -382,11 +386,21 @@ __global__ void k_run_flags(int64_t n, const unsigned long long* __restrict__ sk
   flag[t] = (t == 0 || skey[t] != skey[t - 1]) ? 1 : 0;
 }
 
+// An element joins its class when its own tables match the class tables to
+// 1e-12 relative, or to the rounding floor of its own table, ~ 16 eps
+// |X_o| / h_e (J is formed from coordinates of magnitude |X_o| over an element
+// of size h_e = V_e^(1/3); e.g. a 2 km beam chain of 0.2 m elements).
 __global__ void k_geom_validate(int64_t n_el, int len, const double* __restrict__ gradN,
                                 const double* __restrict__ J0w, int nq, const uint8_t* __restrict__ cls,
-                                const double* __restrict__ tab, unsigned int* __restrict__ bad) {
+                                const double* __restrict__ tab, const int32_t* __restrict__ conn, int nen,
+                                const double* __restrict__ X, unsigned int* __restrict__ bad) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n_el) return;
+  double vol = 0.0;
+  for (int q = 0; q < nq; ++q) vol += J0w[e * nq + q];
+  const int64_t Io = conn[e * nen];
+  const double xo = fmax(fabs(X[3 * Io]), fmax(fabs(X[3 * Io + 1]), fabs(X[3 * Io + 2])));
+  const double tol = fmax(1e-12, 16.0 * 2.220446049250313e-16 * xo / cbrt(fabs(vol)));
   const int lg = len - nq;
   const double* t = tab + (int64_t)cls[e] * len;  // len = nq * (per + 1) per class
   // table layout per class: [q][lg/nq gradN entries ..., J0w]
@@ -402,7 +416,7 @@ __global__ void k_geom_validate(int64_t n_el, int len, const double* __restrict_
     sw = fmax(sw, fabs(b));
     dw = fmax(dw, fabs(a - b));
   }
-  if (dg > 1e-12 * sg || dw > 1e-12 * sw) atomicOr(bad, 1u);
+  if (dg > tol * sg || dw > tol * sw) atomicOr(bad, 1u);
 }
 
 __global__ void k_geom_gather_rep(int n_cls, int nq, int per, const int64_t* __restrict__ rep,
@@ -531,7 +545,7 @@ static tlfea_status sort_and_ptr(int64_t n, int32_t* key, V* val, int64_t n_seg,
   return TLFEA_OK;
 }
 
-static tlfea_status build_geometry_classes(Context* c) {
+static tlfea_status build_geometry_classes(Context* c, const double* dX) {
   const int64_t n = c->n_el;
   const int nq = c->nq, per = c->nen * 3;
   const int max_cls = c->element == TLFEA_T10 ? 32 : 4;
@@ -589,7 +603,8 @@ static tlfea_status build_geometry_classes(Context* c) {
   unsigned int* dbad = nullptr;
   TL_TRY(c->alloc(&dbad, 1));
   TL_CUDA(cudaMemset(dbad, 0, sizeof(unsigned int)));
-  k_geom_validate<<<grid_for(n, 128), 128>>>(n, nq * (per + 1), c->gradN, c->J0w, nq, c->cls, c->cls_tab, dbad);
+  k_geom_validate<<<grid_for(n, 128), 128>>>(n, nq * (per + 1), c->gradN, c->J0w, nq, c->cls, c->cls_tab, c->conn,
+                                              c->nen, dX, dbad);
   TL_CHECK_LAUNCH();
   unsigned int hb = 0;
   TL_CUDA(cudaMemcpy(&hb, dbad, sizeof(hb), cudaMemcpyDeviceToHost));
@@ -739,7 +754,7 @@ static int env_int(const char* name, int dflt) {
 // TLFEA_FZ_{ETILES,CHUNK,LAG} tune it.
 static tlfea_status build_fused_plan(Context* c) {
   c->fz_items = 0;
-  if (env_int("TLFEA_FUSED", 0) == 0) return TLFEA_OK;
+  if (env_int("TLFEA_FUSED", 0) == 0 || c->element == TLFEA_ANCF3243) return TLFEA_OK;
   if (c->nranks != 1 || c->n_cls == 0 || !c->unit_ptr || !c->u_off || !c->fdest || c->n_el == 0 ||
       c->n_units == 0 || c->n_own == 0)
     return TLFEA_OK;
@@ -803,7 +818,7 @@ static tlfea_status build_fused_plan(Context* c) {
 static tlfea_status validate(const tlfea_mesh* mesh, const tlfea_material* mat,
                              const tlfea_options* opts) {
   if (!mesh || !mat || !opts) return fail(TLFEA_E_INVALID, "NULL mesh/material/options");
-  if (mesh->element != TLFEA_T10 && mesh->element != TLFEA_ANCF3443)
+  if (mesh->element != TLFEA_T10 && mesh->element != TLFEA_ANCF3443 && mesh->element != TLFEA_ANCF3243)
     return fail(TLFEA_E_INVALID, "unknown element type");
   if (mesh->n_elements <= 0 || mesh->n_coef <= 0 || !mesh->conn || !mesh->X_ref)
     return fail(TLFEA_E_INVALID, "empty mesh or NULL conn/X_ref");
@@ -812,8 +827,10 @@ static tlfea_status validate(const tlfea_mesh* mesh, const tlfea_material* mat,
     return fail(TLFEA_E_INVALID, "T10 needs quadrature TLFEA_Q_T10_4PT or TLFEA_Q_T10_KEAST5");
   if (mesh->element == TLFEA_ANCF3443 && opts->quadrature != TLFEA_Q_GL_4x4x3)
     return fail(TLFEA_E_INVALID, "ANCF3443 needs quadrature TLFEA_Q_GL_4x4x3");
-  if (mesh->element == TLFEA_ANCF3443 && (mesh->n_coef % 4) != 0)
-    return fail(TLFEA_E_INVALID, "ANCF3443 n_coef must be 4 * n_nodes");
+  if (mesh->element == TLFEA_ANCF3243 && opts->quadrature != TLFEA_Q_GL_3x2x2)
+    return fail(TLFEA_E_INVALID, "ANCF3243 needs quadrature TLFEA_Q_GL_3x2x2");
+  if (mesh->element != TLFEA_T10 && (mesh->n_coef % 4) != 0)
+    return fail(TLFEA_E_INVALID, "ANCF n_coef must be 4 * n_nodes");
   if (mat->model == TLFEA_SVK) {
     if (!(mat->E > 0.0) || !(mat->nu > -1.0 && mat->nu < 0.5))
       return fail(TLFEA_E_INVALID, "SVK needs E > 0 and -1 < nu < 0.5");
@@ -984,7 +1001,7 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   c->n_el_global = mesh->n_elements;
   c->n_coef = mesh->n_coef;
   const int nen = c->nen, nq = c->nq;
-  const int npe = mesh->element == TLFEA_T10 ? 10 : 4;
+  const int npe = n_nodes_of(mesh->element);
   const int64_t NE = mesh->n_elements;
 
   // ---- host: coefficient connectivity + validation (ids, distinct nodes)
@@ -1004,12 +1021,12 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     if (mesh->element == TLFEA_T10) {
       for (int a = 0; a < 10; ++a) cc[e * 10 + a] = row[a];
     } else {
-      for (int k = 0; k < 4; ++k)
-        for (int m = 0; m < 4; ++m) cc[e * 16 + 4 * k + m] = 4 * row[k] + m;
+      for (int k = 0; k < npe; ++k)
+        for (int m = 0; m < 4; ++m) cc[e * nen + 4 * k + m] = 4 * row[k] + m;
     }
   }
   std::vector<double> dims;
-  if (mesh->element == TLFEA_ANCF3443) {
+  if (mesh->element != TLFEA_T10) {
     dims.resize((size_t)NE * 3);
     for (int64_t e = 0; e < NE; ++e)
       for (int k = 0; k < 3; ++k) {
@@ -1124,7 +1141,7 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     TL_CUDA(cudaMemcpy(&na, dna, sizeof(na), cudaMemcpyDeviceToHost));
     c->affine = na ? 0 : 1;
   }
-  TL_TRY(build_geometry_classes(c));
+  TL_TRY(build_geometry_classes(c, dX));
 
   // ---- a-2 pattern over setup elements (64-bit keys, sort, unique)
   // constraint couplings join the element keys (pattern union)
@@ -1237,8 +1254,11 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   {
     double mq[kMassRuleT10 * 3], mw[kMassRuleT10];
     int nmq;
+    static_assert(kMassRuleBeam <= kMassRuleT10, "mass rule buffers");
     if (c->element == TLFEA_T10 && c->mass_rule == 0) {
       nmq = make_mass_rule_t10(mq, mw);
+    } else if (c->element == TLFEA_ANCF3243 && c->mass_rule == 0) {
+      nmq = make_mass_rule_beam(mq, mw);
     } else {
       nmq = make_rule(c->quadrature, mq, mw);
     }

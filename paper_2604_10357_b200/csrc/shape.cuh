@@ -40,6 +40,20 @@ inline int make_rule(int rule, double* xi /*[n][3]*/, double* w) {
     }
     return 5;
   }
+  if (rule == TLFEA_Q_GL_3x2x2) {  // beam: 3 points along the axis, 2 x 2 over the section
+    const double p3[3] = {-std::sqrt(0.6), 0.0, std::sqrt(0.6)}, q3[3] = {5.0 / 9.0, 8.0 / 9.0, 5.0 / 9.0};
+    const double p2 = 1.0 / std::sqrt(3.0);
+    int n = 0;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 2; ++j)
+        for (int k = 0; k < 2; ++k, ++n) {
+          xi[3 * n + 0] = p3[i];
+          xi[3 * n + 1] = j ? p2 : -p2;
+          xi[3 * n + 2] = k ? p2 : -p2;
+          w[n] = q3[i];
+        }
+    return n;
+  }
   // Gauss-Legendre: 4 points (roots of P4), 3 points (roots of P3)
   const double t = 2.0 * std::sqrt(1.2) / 7.0;
   const double x4o = std::sqrt(3.0 / 7.0 + t), x4i = std::sqrt(3.0 / 7.0 - t);
@@ -79,6 +93,65 @@ inline int make_mass_rule_t10(double* xi, double* w) {
         w[n] = gw[i] * gw[j] * gw[k] * 0.125 * (1.0 - u) * (1.0 - u) * (1.0 - s);
       }
   return n;
+}
+
+// Host: exact consistent-mass rule of the ANCF3243 beam (reading Q23):
+// N_a N_b det J has degree <= 10 along the axis and <= 3 across the section
+// -> Gauss-Legendre 6 x 2 x 2 (24 points).
+constexpr int kMassRuleBeam = 24;
+inline int make_mass_rule_beam(double* xi, double* w) {
+  const double g6[6] = {-0.9324695142031519, -0.6612093864662645, -0.2386191860831969,
+                        0.2386191860831969,  0.6612093864662645,  0.9324695142031519};
+  const double w6[6] = {0.17132449237917027, 0.3607615730481387, 0.46791393457269104,
+                        0.46791393457269104, 0.3607615730481387, 0.17132449237917027};
+  const double p2 = 1.0 / std::sqrt(3.0);
+  int n = 0;
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 2; ++j)
+      for (int k = 0; k < 2; ++k, ++n) {
+        xi[3 * n + 0] = g6[i];
+        xi[3 * n + 1] = j ? p2 : -p2;
+        xi[3 * n + 2] = k ? p2 : -p2;
+        w[n] = w6[i];
+      }
+  return n;
+}
+
+// Device/host: ANCF3243 beam values and parent gradients (reading Q23). With
+// s = (1 + xi)/2 along the axis: cubic Hermite h00, L h10 (node A) and h01,
+// L h11 (node B) for (r, r_x); (W/2) eta and (H/2) zeta times (1 - s) / s for
+// (r_y, r_z). Local coefficient 4k + m, k = A, B, m = (r, r_x, r_y, r_z).
+__host__ __device__ inline void beam_shape(const double* xi3, const double* LWH, double* S, double (*dS)[3]) {
+  const double s = 0.5 * (1.0 + xi3[0]), y = xi3[1], z = xi3[2];
+  const double L = LWH[0], W = LWH[1], H = LWH[2];
+  const double s2 = s * s, s3 = s2 * s;
+  // values and d/ds of the Hermite cubics
+  const double h[4] = {1.0 - 3.0 * s2 + 2.0 * s3, s - 2.0 * s2 + s3, 3.0 * s2 - 2.0 * s3, s3 - s2};
+  const double dh[4] = {6.0 * s2 - 6.0 * s, 1.0 - 4.0 * s + 3.0 * s2, 6.0 * s - 6.0 * s2, 3.0 * s2 - 2.0 * s};
+  const double lin[2] = {1.0 - s, s}, dlin[2] = {-1.0, 1.0};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double hr = h[2 * k], hx = L * h[2 * k + 1];
+    if (S) {
+      S[4 * k + 0] = hr;
+      S[4 * k + 1] = hx;
+      S[4 * k + 2] = 0.5 * W * y * lin[k];
+      S[4 * k + 3] = 0.5 * H * z * lin[k];
+    }
+    // d/dxi = 0.5 d/ds
+    dS[4 * k + 0][0] = 0.5 * dh[2 * k];
+    dS[4 * k + 0][1] = 0.0;
+    dS[4 * k + 0][2] = 0.0;
+    dS[4 * k + 1][0] = 0.5 * L * dh[2 * k + 1];
+    dS[4 * k + 1][1] = 0.0;
+    dS[4 * k + 1][2] = 0.0;
+    dS[4 * k + 2][0] = 0.25 * W * y * dlin[k];
+    dS[4 * k + 2][1] = 0.5 * W * lin[k];
+    dS[4 * k + 2][2] = 0.0;
+    dS[4 * k + 3][0] = 0.25 * H * z * dlin[k];
+    dS[4 * k + 3][1] = 0.0;
+    dS[4 * k + 3][2] = 0.5 * H * lin[k];
+  }
 }
 
 // Device/host: T10 values and parent-domain gradients.

@@ -303,8 +303,9 @@ KV_TIRE = dict(eta_damp=5.0e3, lambda_damp=5.0e3)
 TIRE_DROP = dict(model=0, E=5.0e6, nu=0.40, C10=0.0, C01=0.0, kappa=0.0, rho0=900.0,
                  eta_damp=0.0, lambda_damp=0.0)
 
-Q_T10_4PT, Q_T10_KEAST5, Q_GL_443 = 0, 1, 2
+Q_T10_4PT, Q_T10_KEAST5, Q_GL_443, Q_GL_322 = 0, 1, 2, 3
 H_T10, H_ANCF = 1.0e-3, 5.0e-4
+H_BEAM = 1.0e-3
 
 
 @dataclasses.dataclass
@@ -337,4 +338,8 @@ def config(idx: int, scale: str = "full") -> Config:
         m, _, _ = many_body()
         return Config("cfg5_manybody_2000x_t10_9x6x3_force_only", m, dict(TIRE_DROP),
                       Q_T10_KEAST5, H_T10, force_only=True)
+    if idx == 6:
+        # NEXT-1 measurement: the paper's largest ANCF3243 beam (RES32)
+        m = ancf_beam(500000)
+        return Config("cfg6_ancf3243_beam_res32_500k_svk_gl322", m, dict(SVK_PAPER), Q_GL_322, H_BEAM)
     raise ValueError(idx)

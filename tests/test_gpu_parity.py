@@ -66,6 +66,11 @@ CASES = {
                                            dict(synth.MR_PAPER), 0),
     "ancf_3x3_svk": lambda: (synth.ancf_plate(3), dict(synth.SVK_PAPER), 2),
     "ancf_5x5_mr_kv": lambda: (synth.ancf_plate(5), dict(synth.MR_PAPER, **synth.KV_TIRE), 2),
+    # ANCF3243 beam (NEXT-1): 16 elements = one CTA tile; 9 = ragged tile
+    "beam_16_svk": lambda: (synth.ancf_beam(16), dict(synth.SVK_PAPER), 3),
+    "beam_9_mr_kv": lambda: (synth.ancf_beam(9), dict(synth.MR_PAPER, **synth.KV_TIRE), 3),
+    "beam_5_perturbed_svk_kv": lambda: (synth.perturbed(synth.ancf_beam(5), amp=0.02),
+                                        dict(synth.SVK_PAPER, **synth.KV_TIRE), 3),
 }
 
 
@@ -106,7 +111,7 @@ def test_eval_parity(torch_cuda, case):
     assert np.array_equal(g, g2) and np.array_equal(H, H2) and np.array_equal(f, f2)
 
 
-@pytest.mark.parametrize("case", ["cfg1_svk_4pt", "t10_4x3x2_mr_kv_keast5", "ancf_5x5_mr_kv"])
+@pytest.mark.parametrize("case", ["cfg1_svk_4pt", "t10_4x3x2_mr_kv_keast5", "ancf_5x5_mr_kv", "beam_9_mr_kv"])
 def test_setup_exports(torch_cuda, case):
     mesh, mat, rule = CASES[case]()
     import paper_2604_10357_b200 as T
@@ -121,7 +126,7 @@ def test_setup_exports(torch_cuda, case):
     assert rel(fff.cpu().numpy(), pr.fff) <= 1e-13
 
 
-@pytest.mark.parametrize("case", ["cfg1_svk_4pt", "t10_4x3x2_mr_kv_keast5", "ancf_3x3_svk"])
+@pytest.mark.parametrize("case", ["cfg1_svk_4pt", "t10_4x3x2_mr_kv_keast5", "ancf_3x3_svk", "beam_16_svk"])
 def test_force_only_and_split_stages(torch_cuda, case):
     torch = torch_cuda
     mesh, mat, rule = CASES[case]()
