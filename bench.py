@@ -51,9 +51,12 @@ def fp64_peak():
     except Exception:
         return FP64_NOMINAL_TFLOPS, "nominal 148 SM x 64 FMA x 2 x 1.965 GHz (DESIGN.md)"
 
-# Exact structured-SVK operation counts: flops per
-# quadrature point for force only / force + symmetric tangent.
-FLOP_PER_QP = {("t10", False): 468, ("t10", True): 4420, ("ancf", False): 684, ("ancf", True): 10252}
+# Flops per quadrature point for force only / force + symmetric tangent:
+# exact structured-SVK counts for T10 / ANCF3443;
+# the ANCF3243 beam scaled from them (8-node kinematics + 36 blocks at the
+# T10 per-block count of 71.9 flop), a model figure (+-20 %).
+FLOP_PER_QP = {("t10", False): 468, ("t10", True): 4420, ("ancf", False): 684, ("ancf", True): 10252,
+               ("beam", False): 380, ("beam", True): 2970}
 
 
 def env_rank():
@@ -126,7 +129,9 @@ def workload(cfg_idx: int):
     elif mesh.element == 0:
         x, v, vn, fext = synth.t10_state(mesh, with_fext=True)
     else:
-        x, v, vn = synth.ancf_state(mesh)
+        # the beam chain bends over its own length (plate: 4 m)
+        length = 4.0 if mesh.element == 1 else float(mesh.X[:, 0].max())
+        x, v, vn = synth.ancf_state(mesh, length=length)
         fext = np.random.default_rng(synth.SEED_BASE + 3).normal(size=x.shape)
     return cfg, mesh, x, v, vn, fext
 
@@ -204,6 +209,12 @@ def oracle_slice(cfg_idx: int, target_el: int):
         nb = max(1, target_el // 972)
         sub, x, v = synth.many_body(n_bodies=nb)
         return cfg, sub, x, v, v.copy(), None, f"{nb} of 2000 bodies ({sub.n_el} elements)"
+    if cfg_idx == 6:
+        n = max(1, min(m.n_el, target_el))
+        sub = synth.ancf_beam(n)
+        x, v, vn = synth.ancf_state(sub, length=float(m.X[:, 0].max()))
+        fext = np.random.default_rng(synth.SEED_BASE + 3).normal(size=x.shape)
+        return cfg, sub, x, v, vn, fext, f"first {n} of {m.n_el} beam elements"
     x, v, vn, fext = synth.t10_state(m, with_fext=True)
     return cfg, m, x, v, vn, fext, f"whole mesh ({m.n_el} elements)"
 
@@ -231,7 +242,7 @@ def run_reference(args):
     if rank != 0:
         return
     cfg_idx = args.config
-    target = {1: 192, 2: 30000, 3: 40000, 4: 60, 5: 20000}[cfg_idx]
+    target = {1: 192, 2: 30000, 3: 40000, 4: 60, 5: 20000, 6: 30000}[cfg_idx]
     n_el, _, desc = time_oracle(cfg_idx, target, reps=0)
     _, ts, _ = time_oracle(cfg_idx, target, reps=args.warmup + args.steps)
     ts = ts[args.warmup:]
@@ -335,7 +346,7 @@ def run_ours(args):
     dom = max(kt, key=lambda k: kt[k][1])
     n_l, ms_l = kt[dom]
     avg_ms = ms_l / max(n_l, 1)
-    elem = "t10" if mesh.element == 0 else "ancf"
+    elem = {0: "t10", 1: "ancf", 2: "beam"}[int(mesh.element)]
     if dom == "element":
         bpe = bytes_per_element(mesh, info, not force_only, kv)
         bytes_launch = bpe * info["n_elements"]
@@ -395,7 +406,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        target = {1: 192, 2: 60000, 3: 110000, 4: 100, 5: 40000}[args.config]
+        target = {1: 192, 2: 60000, 3: 110000, 4: 100, 5: 40000, 6: 100000}[args.config]
         n_el_s, ts, desc = time_oracle(args.config, target)
         cpu = {"value": n_el_s / ts[0], "unit": "elements/s", "cores": cpu_cores_used(), "kind": "oracle",
                "sample": desc, "seconds": ts[0]}
@@ -407,7 +418,7 @@ def run_ours(args):
             "scaling": "strong" if args.config == 3 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": cfg.name, "n_elements": mesh.n_el, "nnz_H": int(9 * info["nnz_coef"]) if world == 1 else None,
-                       "quadrature": ["t10_4pt", "keast5", "gl443"][cfg.quadrature],
+                       "quadrature": ["t10_4pt", "keast5", "gl443", "gl322"][cfg.quadrature],
                        "material": ["svk", "mooney_rivlin"][cfg.material["model"]] + ("+kv" if kv else ""),
                        "path": "force_only" if force_only else "force+tangent+residual (tlfea_eval)",
                        "parallelism": f"element-partition x{world}" if world > 1 else "1 GPU",
