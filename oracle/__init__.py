@@ -374,6 +374,16 @@ class Problem:
                             H[self.dof_slot(C["cols"][p1], C["cols"][p2])] += h * h * rho * C["vals"][p1] * C["vals"][p2]
         return g, H, fint
 
+    def upper_view(self):
+        """UPPER storage of H (NEXT-4, reading Q14): the entries with
+        col >= row of the full DOF pattern, rows in order. Returns
+        (rowptr_u, cols_u, index into the full value array)."""
+        keep = self.cols >= np.repeat(np.arange(self.rowptr.size - 1), np.diff(self.rowptr))
+        counts = np.add.reduceat(keep.astype(np.int64), self.rowptr[:-1]) if keep.size else np.zeros(0, np.int64)
+        counts[np.diff(self.rowptr) == 0] = 0
+        rowptr_u = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        return rowptr_u, self.cols[keep], np.nonzero(keep)[0]
+
     def dof_slot(self, i: int, j: int) -> int:
         """CSR index of DOF entry (i, j) (binary search over the row's columns)."""
         a, b = self.rowptr[i], self.rowptr[i + 1]
