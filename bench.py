@@ -275,7 +275,8 @@ def run_ours(args):
     force_only = cfg.force_only
     kv = cfg.material.get("eta_damp", 0) > 0 or cfg.material.get("lambda_damp", 0) > 0
     t_setup = time.perf_counter()
-    ctx = T.Context.from_mesh(mesh, cfg.material, cfg.quadrature, rank=rank, nranks=world, device=local)
+    ctx = T.Context.from_mesh(mesh, cfg.material, cfg.quadrature, rank=rank, nranks=world, device=local,
+                              hessian=args.hessian)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
     info = ctx.info
@@ -417,10 +418,11 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if args.config == 3 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": cfg.name, "n_elements": mesh.n_el, "nnz_H": int(9 * info["nnz_coef"]) if world == 1 else None,
+            "config": {"workload": cfg.name, "n_elements": mesh.n_el, "nnz_H": int(info["nnz"]) if world == 1 else None,
                        "quadrature": ["t10_4pt", "keast5", "gl443", "gl322"][cfg.quadrature],
                        "material": ["svk", "mooney_rivlin"][cfg.material["model"]] + ("+kv" if kv else ""),
                        "path": "force_only" if force_only else "force+tangent+residual (tlfea_eval)",
+                       "hessian_storage": args.hessian,
                        "parallelism": f"element-partition x{world}" if world > 1 else "1 GPU",
                        "geometry_classes": info["n_geometry_classes"],
                        "l2": "inputs/outputs larger than L2 (no flush needed)",
@@ -449,6 +451,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--hessian", choices=["full", "upper"], default="full",
+                    help="H storage (full DOF CSR = the headline; upper = NEXT-4 variant)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define TLFEA_ABI_VERSION 3
+#define TLFEA_ABI_VERSION 4
 
 typedef struct tlfea_ctx_s* tlfea_ctx;
 
@@ -151,6 +151,10 @@ typedef struct {
   const int32_t* elem_part;
   int32_t device;
   const tlfea_constraints* constraints;
+  int32_t hessian_upper;  /* 0: full DOF CSR of H (default); 1: UPPER storage
+                             (entries with col >= row only, rows in order, the
+                             cuDSS-facing matrix view).
+                             UPPER: single rank, no constraints. */
 } tlfea_options;
 
 /* Sizes of a context (tlfea_info). Rows/DOFs are GLOBAL indices; in a
@@ -257,7 +261,8 @@ tlfea_status tlfea_export_mass(tlfea_ctx ctx, double* M_out, double* fff_out,
  *   f_ext external nodal forces, or NULL (= 0)
  *   h   time step (> 0, else TLFEA_E_INVALID)
  * Outputs (DEVICE, owned rows): g_out [3*n_owned_nodes] residual;
- *   H_out [nnz] values of M/h + h K_t on tlfea_pattern (elastic tangent only);
+ *   H_out [nnz] values of M/h + h K_t on tlfea_pattern (elastic tangent only;
+ *         full or UPPER storage per options.hessian_upper, info.nnz entries);
  *   f_int_out [3*n_owned_nodes] or NULL.
  * In a partitioned context (nranks > 1) use the begin/finish pair below.
  * Deterministic: bitwise identical results for identical inputs. */

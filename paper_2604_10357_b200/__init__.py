@@ -58,7 +58,7 @@ class Options(C.Structure):
     _fields_ = [("quadrature", C.c_int32), ("mass_rule", C.c_int32), ("gravity", C.c_double * 3),
                 ("ancf_dims", C.c_double * 3), ("rank", C.c_int32), ("nranks", C.c_int32),
                 ("elem_part", C.POINTER(C.c_int32)), ("device", C.c_int32),
-                ("constraints", C.POINTER(Constraints))]
+                ("constraints", C.POINTER(Constraints)), ("hessian_upper", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -206,9 +206,13 @@ class Context:
 
     def __init__(self, element: int, conn: np.ndarray, X: np.ndarray, mat: dict, quadrature: int,
                  dims: np.ndarray | None = None, mass_rule: int = 0, gravity=(0.0, 0.0, 0.0),
-                 rank: int = 0, nranks: int = 1, elem_part=None, device: int = 0, constraints: dict | None = None):
+                 rank: int = 0, nranks: int = 1, elem_part=None, device: int = 0, constraints: dict | None = None,
+                 hessian: str = "full"):
         """constraints: dict rowptr, cols (DOF ids), vals, b of c(q) = C q - b
-        (tlfea_constraints; NEXT-3)."""
+        (tlfea_constraints; NEXT-3). hessian: "full" or "upper" storage of H
+        (options.hessian_upper; NEXT-4)."""
+        if hessian not in ("full", "upper"):
+            raise ValueError("hessian must be 'full' or 'upper'")
         L = lib()
         con = None
         if constraints is not None:
@@ -227,7 +231,7 @@ class Context:
                     None if self._dims is None else self._dims.ctypes.data_as(C.POINTER(C.c_double)))
         opts = Options(quadrature, mass_rule, (C.c_double * 3)(*gravity), (C.c_double * 3)(0, 0, 0), rank, nranks,
                        None if self._part is None else self._part.ctypes.data_as(C.POINTER(C.c_int32)), device,
-                       None if con is None else C.pointer(con))
+                       None if con is None else C.pointer(con), 1 if hessian == "upper" else 0)
         self.material = dict(mat)
         m = make_material(mat)
         h = C.c_void_p()

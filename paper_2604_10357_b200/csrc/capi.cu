@@ -1,6 +1,7 @@
 // capi.cu — the extern "C" boundary of libtlfea (include/tlfea.h). Argument
 // checking and orchestration only; every step of the path runs in the kernels
 // of setup.cu / eval.cu / partition.cu.
+#include <algorithm>
 #include <new>
 
 #include "common.cuh"
@@ -107,7 +108,7 @@ tlfea_status tlfea_info(tlfea_ctx ctx, tlfea_info_t* o) {
   o->n_coef = c.n_coef;
   o->n_dof = 3 * c.n_coef;
   o->nnz_coef = c.nnz_c;
-  o->nnz = 9 * c.nnz_c;
+  o->nnz = c.nnz_H;
   o->n_owned_nodes = c.n_own;
   o->affine = c.affine;
   o->rank = c.rank;
@@ -147,7 +148,7 @@ tlfea_status tlfea_export_pattern(tlfea_ctx ctx, int32_t* rowptr_out, int32_t* c
   const cudaStream_t s = as_stream(stream);
   const cudaMemcpyKind k = cudaMemcpyDeviceToDevice;
   if (rowptr_out) TL_CUDA(cudaMemcpyAsync(rowptr_out, c.rowptr, sizeof(int32_t) * (3 * c.n_own + 1), k, s));
-  if (cols_out) TL_CUDA(cudaMemcpyAsync(cols_out, c.cols, sizeof(int32_t) * 9 * c.nnz_c, k, s));
+  if (cols_out) TL_CUDA(cudaMemcpyAsync(cols_out, c.cols, sizeof(int32_t) * c.nnz_H, k, s));
   if (rowptr_c_out) TL_CUDA(cudaMemcpyAsync(rowptr_c_out, c.rowptr_c, sizeof(int32_t) * (c.n_own + 1), k, s));
   if (cols_c_out) TL_CUDA(cudaMemcpyAsync(cols_c_out, c.cols_c, sizeof(int32_t) * c.nnz_c, k, s));
   if (owned_out) TL_CUDA(cudaMemcpyAsync(owned_out, c.own_nodes, sizeof(int32_t) * c.n_own, k, s));
@@ -171,6 +172,31 @@ tlfea_status tlfea_slot_map(tlfea_ctx ctx, int64_t e_begin, int64_t e_count, int
   if (e_count > 0)
     TL_CUDA(cudaMemcpy(conn.data(), c.conn + e_begin * nen, sizeof(int32_t) * conn.size(), cudaMemcpyDeviceToHost));
   TL_CUDA(cudaMemcpy(own_idx.data(), c.own_idx, sizeof(int32_t) * c.n_coef, cudaMemcpyDeviceToHost));
+  // UPPER storage: slot of (a,d; b,f) only when col >= row (common.cuh layout)
+  std::vector<int32_t> cols_c, ubase;
+  if (c.upper) {
+    cols_c.resize(c.nnz_c);
+    ubase.resize(c.n_own + 1);
+    TL_CUDA(cudaMemcpy(cols_c.data(), c.cols_c, sizeof(int32_t) * c.nnz_c, cudaMemcpyDeviceToHost));
+    TL_CUDA(cudaMemcpy(ubase.data(), c.ubase, sizeof(int32_t) * (c.n_own + 1), cudaMemcpyDeviceToHost));
+  }
+  if (c.upper) {
+    for (int64_t e = 0; e < e_count; ++e)
+      for (int a = 0; a < nen; ++a) {
+        const int32_t i = own_idx[conn[e * nen + a]];
+        const int32_t b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0;
+        const int32_t kd = (int32_t)(std::lower_bound(cols_c.begin() + b0, cols_c.begin() + b0 + deg,
+                                                      conn[e * nen + a]) - (cols_c.begin() + b0));
+        for (int b = 0; b < nen; ++b) {
+          const int32_t k = sc[(e * nen + a) * nen + b] - b0 - kd, L = deg - kd - 1;
+          for (int d = 0; d < 3; ++d)
+            for (int f = 0; f < 3; ++f)
+              out_host[(e * nd + 3 * a + d) * nd + 3 * b + f] =
+                  (k < 0 || (k == 0 && f < d)) ? -1 : ubase[i] + 3 * k + f + d * (2 + 3 * L) - d * (d - 1) / 2;
+        }
+      }
+    return TLFEA_OK;
+  }
   // DOF slot = 9 rowptr_c[i] + 3 d deg_i + 3 (s_c - rowptr_c[i]) + f  (DOF lift)
   for (int64_t e = 0; e < e_count; ++e)
     for (int a = 0; a < nen; ++a) {
@@ -318,7 +344,7 @@ tlfea_status tlfea_eval_host(tlfea_ctx ctx, const double* x, const double* v, co
   if (!x || !v || !g_out || !H_out) return fail(TLFEA_E_INVALID, "tlfea_eval_host: NULL x, v, g_out or H_out");
   TRY(use_device(c));
   const cudaStream_t s = as_stream(stream);
-  const int64_t nd = 3 * c.n_coef, nown = 3 * c.n_own, nnz = 9 * c.nnz_c;
+  const int64_t nd = 3 * c.n_coef, nown = 3 * c.n_own, nnz = c.nnz_H;
   if (!c.h_x) {  // persistent device staging, allocated on first use
     TRY(c.alloc(&c.h_x, nd));
     TRY(c.alloc(&c.h_v, nd));

@@ -98,6 +98,14 @@ struct Context {
   int64_t n_own = 0;           // owned coefficient rows
   int64_t nnz_c = 0;           // owned-row coefficient nnz
   int affine = 0;
+  // H storage: full DOF CSR (9 nnz_c values) or UPPER (col >= row). UPPER row
+  // 3I+d starts at ubase[I] + d (3 + 3 L_I) - d (d - 1) / 2, L_I = blocks
+  // J > I of coefficient row I; block (I, J) with rank k among J >= I (k = 0:
+  // the diagonal) has entry (d, f) at ubase[I] + 3 k + f + d (2 + 3 L_I)
+  // - d (d - 1) / 2 (f >= d when k = 0).
+  int upper = 0;
+  int64_t nnz_H = 0;           // values of H as stored
+  int32_t* ubase = nullptr;    // [n_own + 1] UPPER offsets of coefficient rows
 
   // device data
   int32_t* conn = nullptr;     // [n_el][nen] coefficient ids (local elements)

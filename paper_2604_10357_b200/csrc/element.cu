@@ -1001,6 +1001,7 @@ struct GatherArgs {
   const double* Kscr;
   double h;
   double* H;
+  int upper;  // UPPER H storage (u_deg = L | diagonal << 16, no transposed copy)
 };
 
 // Per-warp TMA staging: two windows and their mbarriers. `wk` counts the
@@ -1066,6 +1067,19 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
   W.wk = wk0 + nwin;
   if (!valid) return;
   const double mh = m / h;
+  if (A.upper) {
+    // UPPER storage (common.cuh): entry (d, f) at off + f + d (2 + 3 L) - d (d-1)/2,
+    // the diagonal block keeps f >= d only; no transposed copy
+    const int L = dg & 0xffff;
+    const bool diag = (dg >> 16) != 0;
+    double* out = H + off;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int f = 0; f < 3; ++f)
+        if (!diag || f >= d) out[f + d * (2 + 3 * L) - d * (d - 1) / 2] = fma(h, acc[3 * d + f], d == f ? mh : 0.0);
+    return;
+  }
   const int deg = dg & 0xffff, degT = dg >> 16;
   double* out = H + off;
 #pragma unroll
@@ -1341,6 +1355,7 @@ static GatherArgs gather_args(const Context* c, double h, double* H) {
   A.Kscr = c->Kscr;
   A.h = h;
   A.H = H;
+  A.upper = c->upper;
   return A;
 }
 

@@ -220,6 +220,55 @@ __global__ void k_lift(int64_t n_own, int64_t nnz_c, const int32_t* __restrict__
     for (int e = 0; e < 3; ++e) cols[9 * b + 3 * d * deg + 3 * k + e] = 3 * J + e;
 }
 
+// UPPER H storage (NEXT-4). Rank of the diagonal block in coefficient row i
+// (global coefficient I = own_nodes[i]) = number of columns J < I.
+__device__ __forceinline__ int32_t diag_rank(const int32_t* __restrict__ rowptr_c, const int32_t* __restrict__ cols_c,
+                                             int32_t i, int32_t I) {
+  int32_t lo = rowptr_c[i], hi = rowptr_c[i + 1];
+  const int32_t b = lo;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (cols_c[mid] < I) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo - b;
+}
+
+// values of coefficient row i in UPPER storage: 6 (diagonal block, f >= d) + 9 L
+__global__ void k_upper_count(int64_t n_own, const int32_t* __restrict__ rowptr_c, const int32_t* __restrict__ cols_c,
+                              const int32_t* __restrict__ own_nodes, int32_t* __restrict__ cnt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_own) return;
+  const int32_t deg = rowptr_c[i + 1] - rowptr_c[i];
+  const int32_t L = deg - diag_rank(rowptr_c, cols_c, (int32_t)i, own_nodes[i]) - 1;
+  cnt[i] = 6 + 9 * L;
+}
+
+__host__ __device__ __forceinline__ int64_t upper_pos(int32_t base, int32_t k, int32_t L, int d, int f) {
+  return (int64_t)base + 3 * k + f + d * (2 + 3 * L) - d * (d - 1) / 2;
+}
+
+__global__ void k_lift_upper(int64_t n_own, int64_t nnz_c, const int32_t* __restrict__ rowptr_c,
+                             const int32_t* __restrict__ cols_c, const int32_t* __restrict__ blk_row,
+                             const int32_t* __restrict__ own_nodes, const int32_t* __restrict__ ubase,
+                             int32_t* __restrict__ rowptr, int32_t* __restrict__ cols) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < n_own) {
+    const int32_t deg = rowptr_c[p + 1] - rowptr_c[p];
+    const int32_t L = deg - diag_rank(rowptr_c, cols_c, (int32_t)p, own_nodes[p]) - 1;
+    for (int d = 0; d < 3; ++d) rowptr[3 * p + d] = ubase[p] + d * (3 + 3 * L) - d * (d - 1) / 2;
+    if (p == n_own - 1) rowptr[3 * n_own] = ubase[n_own];
+  }
+  if (p >= nnz_c) return;
+  const int32_t i = blk_row[p], b = rowptr_c[i], deg = rowptr_c[i + 1] - b;
+  const int32_t kd = diag_rank(rowptr_c, cols_c, i, own_nodes[i]);
+  const int32_t k = (int32_t)p - b - kd;  // rank among J >= I
+  if (k < 0) return;                      // lower block: not stored
+  const int32_t L = deg - kd - 1, J = cols_c[p];
+  for (int d = 0; d < 3; ++d)
+    for (int f = (k == 0 ? d : 0); f < 3; ++f) cols[upper_pos(ubase[i], k, L, d, f)] = 3 * J + f;
+}
+
 __device__ __forceinline__ int32_t find_in_row(const int32_t* __restrict__ rowptr_c,
                                                const int32_t* __restrict__ cols_c, int32_t r,
                                                int32_t J) {
@@ -503,6 +552,25 @@ __global__ void k_unit_meta(int64_t n_units, const int32_t* __restrict__ unit_p,
   u_m[u] = M[p];
 }
 
+// UPPER storage: unit (I, J), J >= I, of row i writes block rank k at
+// ubase[i] + 3 k; u_deg = L_i | (k == 0) << 16; no transposed copy
+__global__ void k_unit_meta_upper(int64_t n_units, const int32_t* __restrict__ unit_p,
+                                  const int32_t* __restrict__ blk_row, const int32_t* __restrict__ rowptr_c,
+                                  const int32_t* __restrict__ cols_c, const int32_t* __restrict__ own_nodes,
+                                  const int32_t* __restrict__ ubase, const double* __restrict__ M,
+                                  int32_t* __restrict__ u_off, int32_t* __restrict__ u_offT,
+                                  int32_t* __restrict__ u_deg, double* __restrict__ u_m) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n_units) return;
+  const int32_t p = unit_p[u], i = blk_row[p], b = rowptr_c[i], deg = rowptr_c[i + 1] - b;
+  const int32_t kd = diag_rank(rowptr_c, cols_c, i, own_nodes[i]);
+  const int32_t k = p - b - kd, L = deg - kd - 1;
+  u_off[u] = ubase[i] + 3 * k;
+  u_offT[u] = -1;
+  u_deg[u] = L | ((k == 0 ? 1 : 0) << 16);
+  u_m[u] = M[p];
+}
+
 __global__ void k_force_dest(int64_t n, int nen, const uint32_t* __restrict__ node_ent, int32_t* __restrict__ fdest) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n) return;
@@ -694,8 +762,14 @@ static tlfea_status build_unit_meta(Context* c) {
   TL_TRY(c->alloc(&c->u_offT, (size_t)c->n_units));
   TL_TRY(c->alloc(&c->u_deg, (size_t)c->n_units));
   TL_TRY(c->alloc(&c->u_m, (size_t)c->n_units));
-  k_unit_meta<<<grid_for(c->n_units, 256), 256>>>(c->n_units, c->unit_p, c->unit_pT, c->blk_row, c->rowptr_c, c->M,
-                                                  c->u_off, c->u_offT, c->u_deg, c->u_m);
+  if (c->upper) {
+    k_unit_meta_upper<<<grid_for(c->n_units, 256), 256>>>(c->n_units, c->unit_p, c->blk_row, c->rowptr_c, c->cols_c,
+                                                          c->own_nodes, c->ubase, c->M, c->u_off, c->u_offT,
+                                                          c->u_deg, c->u_m);
+  } else {
+    k_unit_meta<<<grid_for(c->n_units, 256), 256>>>(c->n_units, c->unit_p, c->unit_pT, c->blk_row, c->rowptr_c, c->M,
+                                                    c->u_off, c->u_offT, c->u_deg, c->u_m);
+  }
   TL_CHECK_LAUNCH();
   return TLFEA_OK;
 }
@@ -845,6 +919,10 @@ static tlfea_status validate(const tlfea_mesh* mesh, const tlfea_material* mat,
   if (opts->mass_rule != 0 && opts->mass_rule != 1) return fail(TLFEA_E_INVALID, "mass_rule must be 0 or 1");
   if (opts->nranks < 1 || opts->rank < 0 || opts->rank >= opts->nranks)
     return fail(TLFEA_E_INVALID, "bad rank / nranks");
+  if (opts->hessian_upper != 0 && opts->hessian_upper != 1)
+    return fail(TLFEA_E_INVALID, "hessian_upper must be 0 or 1");
+  if (opts->hessian_upper && (opts->nranks != 1 || (opts->constraints && opts->constraints->m > 0)))
+    return fail(TLFEA_E_UNSUPPORTED, "UPPER H storage: single-rank contexts without constraints only");
   if (mesh->n_elements >= (1ll << 24)) return fail(TLFEA_E_OVERFLOW, "n_elements >= 2^24 (packed gather entries)");
   if (3 * mesh->n_coef >= (1ll << 31)) return fail(TLFEA_E_OVERFLOW, "3 n_coef >= 2^31");
   if (const tlfea_constraints* k = opts->constraints) {
@@ -1195,9 +1273,35 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     TL_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, c->rowptr_c, (int64_t)(c->n_own + 1)));
     count_launch();
   }
+  c->upper = opts->hessian_upper;
+  c->nnz_H = 9 * c->nnz_c;
+  if (c->upper) {
+    // UPPER: per-row counts 6 + 9 L_I -> offsets; then the lifted pattern
+    TmpArr<int32_t> ucnt;
+    TL_TRY(ucnt.get(c->n_own + 1));
+    TL_TRY(c->alloc(&c->ubase, (size_t)c->n_own + 1));
+    if (c->n_own > 0) {
+      k_upper_count<<<grid_for(c->n_own, 256), 256>>>(c->n_own, c->rowptr_c, c->cols_c, c->own_nodes, ucnt.p);
+      TL_CHECK_LAUNCH();
+    }
+    TL_CUDA(cudaMemset(ucnt.p + c->n_own, 0, sizeof(int32_t)));
+    Tmp tmp;
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, ucnt.p, c->ubase, (int64_t)(c->n_own + 1));
+    TL_TRY(tmp.get(bytes));
+    TL_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, ucnt.p, c->ubase, (int64_t)(c->n_own + 1)));
+    count_launch();
+    int32_t nu = 0;
+    TL_CUDA(cudaMemcpy(&nu, c->ubase + c->n_own, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    c->nnz_H = nu;
+  }
   TL_TRY(c->alloc(&c->rowptr, (size_t)3 * c->n_own + 1));
-  TL_TRY(c->alloc(&c->cols, (size_t)9 * c->nnz_c));
-  if (c->n_own > 0) {
+  TL_TRY(c->alloc(&c->cols, (size_t)std::max<int64_t>(c->nnz_H, 1)));
+  if (c->n_own > 0 && c->upper) {
+    k_lift_upper<<<grid_for(std::max(c->nnz_c, c->n_own), 256), 256>>>(
+        c->n_own, c->nnz_c, c->rowptr_c, c->cols_c, c->blk_row, c->own_nodes, c->ubase, c->rowptr, c->cols);
+    TL_CHECK_LAUNCH();
+  } else if (c->n_own > 0) {
     k_lift<<<grid_for(std::max(c->nnz_c, c->n_own), 256), 256>>>(c->n_own, c->nnz_c, c->rowptr_c, c->cols_c,
                                                                 c->blk_row, c->rowptr, c->cols);
     TL_CHECK_LAUNCH();
