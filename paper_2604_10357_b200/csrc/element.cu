@@ -818,152 +818,6 @@ __global__ void k_gather_units(int64_t n_units, int nen, int nub, const int32_t*
   }
 }
 
-// Warp-cooperative variant for the gather-sorted scratch: a warp owns 32
-// consecutive units whose scratch blocks form one contiguous range; the warp
-// streams that range with coalesced loads through a shared-memory window and
-// each lane then sums its own unit's blocks (fixed order = element order).
-constexpr int kGWarps = 8;
-constexpr int kGWin = 720;  // doubles of staging per warp (80 blocks, 5.6 KB; 45 KB per CTA)
-
-__global__ void __launch_bounds__(kGWarps * 32)
-    k_gather_units_sorted(int64_t n_units, const int32_t* __restrict__ unit_p, const int32_t* __restrict__ unit_pT,
-                          const int32_t* __restrict__ blk_row, const int32_t* __restrict__ rowptr_c,
-                          const int32_t* __restrict__ unit_ptr, const double* __restrict__ Kscr,
-                          const double* __restrict__ M, double h, double* __restrict__ H) {
-  __shared__ double s_win[kGWarps][kGWin];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t u0 = ((int64_t)blockIdx.x * kGWarps + wib) * 32;
-  if (u0 >= n_units) return;
-  const int64_t u = u0 + lane;
-  const bool valid = u < n_units;
-  const int64_t uend = min(u0 + 32, n_units);
-  const int64_t P0 = unit_ptr[u0], P1 = unit_ptr[uend];
-  const int32_t my0 = valid ? unit_ptr[u] : 0, my1 = valid ? unit_ptr[u + 1] : 0;
-  double acc[9];
-#pragma unroll
-  for (int r = 0; r < 9; ++r) acc[r] = 0.0;
-  // stream [P0, P1) blocks in windows of kGWin/9 blocks
-  constexpr int WB = kGWin / 9;
-  for (int64_t w0 = P0; w0 < P1; w0 += WB) {
-    const int64_t w1 = min(w0 + (int64_t)WB, P1);
-    const int64_t nd = (w1 - w0) * 9;
-    const double* src = Kscr + w0 * 9;
-    // batches of 8 independent loads per lane in flight before any store
-    for (int64_t t0 = lane; t0 < nd; t0 += 32 * 8) {
-      double r[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int64_t t = t0 + 32 * k;
-        r[k] = t < nd ? __ldcs(src + t) : 0.0;
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int64_t t = t0 + 32 * k;
-        if (t < nd) s_win[wib][t] = r[k];
-      }
-    }
-    __syncwarp();
-    const int64_t a0 = max((int64_t)my0, w0), a1 = min((int64_t)my1, w1);
-    for (int64_t t = a0; t < a1; ++t) {
-      const double* sb = &s_win[wib][(t - w0) * 9];
-#pragma unroll
-      for (int r = 0; r < 9; ++r) acc[r] += sb[r];
-    }
-    __syncwarp();
-  }
-  if (!valid) return;
-  const int32_t p = unit_p[u], pT = unit_pT[u];
-  const double mh = M[p] / h;
-  {
-    const int32_t i = blk_row[p], b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0, k = p - b0;
-    double* out = H + 9 * (int64_t)b0 + 3 * k;
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-#pragma unroll
-      for (int f = 0; f < 3; ++f) out[3 * d * deg + f] = fma(h, acc[3 * d + f], d == f ? mh : 0.0);
-  }
-  if (pT >= 0) {
-    const int32_t i = blk_row[pT], b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0, k = pT - b0;
-    double* out = H + 9 * (int64_t)b0 + 3 * k;
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-#pragma unroll
-      for (int f = 0; f < 3; ++f) out[3 * d * deg + f] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
-  }
-}
-
-// v2: metadata flattened per unit (one level of independent loads) and the
-// scratch window moved global -> shared with cp.async (LDGSTS, no register
-// staging), so a warp has its whole contiguous range in flight at once.
-constexpr int kG2Warps = 4;
-constexpr int kG2Win = 1152;  // doubles per warp (128 blocks, 9.2 KB; 37 KB per CTA)
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-__global__ void __launch_bounds__(kG2Warps * 32)
-    k_gather_units_v2(int64_t n_units, const int32_t* __restrict__ unit_ptr, const int32_t* __restrict__ u_off,
-                      const int32_t* __restrict__ u_offT, const int32_t* __restrict__ u_deg,
-                      const double* __restrict__ u_m, const double* __restrict__ Kscr, double h,
-                      double* __restrict__ H) {
-  __shared__ double s_win[kG2Warps][kG2Win];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t u0 = ((int64_t)blockIdx.x * kG2Warps + wib) * 32;
-  if (u0 >= n_units) return;
-  const int64_t u = u0 + lane;
-  const bool valid = u < n_units;
-  const int64_t uend = min(u0 + 32, n_units);
-  const int64_t P0 = unit_ptr[u0], P1 = unit_ptr[uend];
-  // independent metadata loads, issued before the data is needed
-  int32_t my0 = 0, my1 = 0, off = 0, offT = -1, dg = 0;
-  double m = 0.0;
-  if (valid) {
-    my0 = unit_ptr[u];
-    my1 = unit_ptr[u + 1];
-    off = u_off[u];
-    offT = u_offT[u];
-    dg = u_deg[u];
-    m = u_m[u];
-  }
-  double acc[9];
-#pragma unroll
-  for (int r = 0; r < 9; ++r) acc[r] = 0.0;
-  constexpr int WB = kG2Win / 9;
-  for (int64_t w0 = P0; w0 < P1; w0 += WB) {
-    const int64_t w1 = min(w0 + (int64_t)WB, P1);
-    const int nd = (int)((w1 - w0) * 9);
-    const double* src = Kscr + w0 * 9;
-    for (int t = lane; t < nd; t += 32) cp_async8(&s_win[wib][t], src + t);
-    cp_async_wait_all();
-    __syncwarp();
-    const int64_t a0 = max((int64_t)my0, w0), a1 = min((int64_t)my1, w1);
-    for (int64_t t = a0; t < a1; ++t) {
-      const double* sb = &s_win[wib][(t - w0) * 9];
-#pragma unroll
-      for (int r = 0; r < 9; ++r) acc[r] += sb[r];
-    }
-    __syncwarp();
-  }
-  if (!valid) return;
-  const double mh = m / h;
-  const int deg = dg & 0xffff, degT = dg >> 16;
-  double* out = H + off;
-#pragma unroll
-  for (int d = 0; d < 3; ++d)
-#pragma unroll
-    for (int f = 0; f < 3; ++f) out[3 * d * deg + f] = fma(h, acc[3 * d + f], d == f ? mh : 0.0);
-  if (offT >= 0) {
-    double* o2 = H + offT;
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-#pragma unroll
-      for (int f = 0; f < 3; ++f) o2[3 * d * degT + f] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
-  }
-}
-
 // v3: TMA bulk copies (cp.async.bulk global->shared, mbarrier completion),
 // double-buffered per warp: one elected lane moves the next window of the
 // contiguous scratch range while the warp sums the current one.
@@ -1446,13 +1300,6 @@ tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
   if (c->u_off) {
     const int64_t per = (int64_t)kG3Warps * 32;
     k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(gather_args(c, h, H));
-    TL_CHECK_LAUNCH();
-    return TLFEA_OK;
-  }
-  if (c->unit_ptr) {
-    const int64_t per = (int64_t)kGWarps * 32;
-    k_gather_units_sorted<<<(unsigned)((c->n_units + per - 1) / per), kGWarps * 32, 0, s>>>(
-        c->n_units, c->unit_p, c->unit_pT, c->blk_row, c->rowptr_c, c->unit_ptr, c->Kscr, c->M, h, H);
     TL_CHECK_LAUNCH();
     return TLFEA_OK;
   }

@@ -223,65 +223,9 @@ __global__ void k_constitutive(int64_t n, MatDev m, const double* __restrict__ F
 
 // ------------------------------------------------------------- launchers
 
-// Measured on B200 (cfg3): warp-per-node 4.2 ms vs thread-per-node 1.3 ms, so
-// the thread version is the default.
-constexpr bool kUseWarpGatherF = false;
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Warp per owned node (node-sorted force scratch): the lanes stream the node's
-// contiguous force contributions and its mass-CSR row (coalesced), then reduce
-// with a fixed butterfly (deterministic). mode as in k_gather_f.
-__global__ void k_gather_f_warp(int64_t n_own, const int32_t* __restrict__ node_ptr,
-                                const double* __restrict__ fscr, const double* __restrict__ fpart_in,
-                                const int32_t* __restrict__ own_nodes, const int32_t* __restrict__ rowptr_c,
-                                const int32_t* __restrict__ cols_c, const double* __restrict__ M,
-                                const double* __restrict__ fff, const double* __restrict__ v,
-                                const double* __restrict__ vn, const double* __restrict__ fext, double h, int mode,
-                                double* __restrict__ g, double* __restrict__ fint) {
-  const int lane = threadIdx.x & 31;
-  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (i >= n_own) return;
-  double f[3] = {0, 0, 0};
-  if (mode == 2) {
-    if (lane < 3) f[lane] = fpart_in[3 * i + lane];
-  } else {
-    const int64_t t0 = 3 * (int64_t)node_ptr[i], t1 = 3 * (int64_t)node_ptr[i + 1];
-    for (int64_t t = t0 + lane; t < t1; t += 32) f[(t - t0) % 3] += fscr[t];
-  }
-#pragma unroll
-  for (int d = 0; d < 3; ++d) f[d] = warp_sum(f[d]);
-  if (fint && lane < 3) fint[3 * i + lane] = f[lane];
-  if (mode == 1 || !g) return;
-  double m[3] = {0, 0, 0};
-  for (int32_t p = rowptr_c[i] + lane; p < rowptr_c[i + 1]; p += 32) {
-    const int64_t J = cols_c[p];
-    const double mm = M[p];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) m[d] += mm * (v[3 * J + d] - (vn ? vn[3 * J + d] : 0.0));
-  }
-#pragma unroll
-  for (int d = 0; d < 3; ++d) m[d] = warp_sum(m[d]);
-  if (lane < 3) {
-    const int64_t I = own_nodes[i];
-    g[3 * i + lane] = m[lane] / h + f[lane] - (fext ? fext[3 * I + lane] : 0.0) - fff[3 * i + lane];
-  }
-}
-
 tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, const double* fext, double h,
                              double* g, double* fint, bool partial_only, cudaStream_t s) {
   if (c->n_own == 0) return TLFEA_OK;
-  if (c->fdest && kUseWarpGatherF) {
-    k_gather_f_warp<<<grid_for(32 * c->n_own, 256), 256, 0, s>>>(
-        c->n_own, c->node_ptr, c->fscr, nullptr, c->own_nodes, c->rowptr_c, c->cols_c, c->M, c->fff, v, vn, fext, h,
-        partial_only ? 1 : 0, g, fint);
-    TL_CHECK_LAUNCH();
-    return TLFEA_OK;
-  }
   if (c->fdest) {
     k_gather_f_dof<<<grid_for(3 * c->n_own, 256), 256, 0, s>>>(
         f_args(c, c->fscr, nullptr, v, vn, fext, h, partial_only ? 1 : 0, g, fint));
@@ -467,13 +411,6 @@ tlfea_status launch_norms2(Context* c, const double* a, const double* b, double*
 tlfea_status launch_residual(Context* c, const double* fint, const double* v, const double* vn,
                              const double* fext, double h, double* g, cudaStream_t s) {
   if (c->n_own == 0) return TLFEA_OK;
-  if (g && kUseWarpGatherF) {
-    k_gather_f_warp<<<grid_for(32 * c->n_own, 256), 256, 0, s>>>(
-        c->n_own, c->node_ptr, c->fscr, fint, c->own_nodes, c->rowptr_c, c->cols_c, c->M, c->fff, v, vn, fext, h, 2,
-        g, nullptr);
-    TL_CHECK_LAUNCH();
-    return TLFEA_OK;
-  }
   if (g) {
     k_gather_f_dof<<<grid_for(3 * c->n_own, 256), 256, 0, s>>>(
         f_args(c, c->fscr, fint, v, vn, fext, h, 2, g, nullptr));

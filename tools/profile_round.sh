@@ -8,7 +8,7 @@ OUT=gpurun_out/$TAG
 mkdir -p $OUT
 timeout 900 python -m pytest tests -m gpu -q -x > $OUT/pytest_gpu.txt 2>&1; tail -2 $OUT/pytest_gpu.txt
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $OUT/smoke.txt 2>&1; tail -1 $OUT/smoke.txt
-for c in ${CFGS:-3 2 4 5}; do
+for c in ${CFGS:-3 2 4 5 6}; do
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 > $OUT/bench_cfg$c.json 2> $OUT/bench_cfg$c.err
   python -c "import json;d=json.load(open('$OUT/bench_cfg$c.json'));print('cfg$c', round(d['value']/1e6,2), 'M el/s', round(d['ms_per_step'],3), 'ms', d['roofline']['bound'], round(d['roofline']['frac'],3))" || tail -3 $OUT/bench_cfg$c.err
 done
