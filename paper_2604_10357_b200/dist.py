@@ -15,10 +15,17 @@ def offsets(counts) -> np.ndarray:
     return np.concatenate([[0], np.cumsum(np.asarray(counts, np.int64))])
 
 
-def exchange(send_buf, recv_buf, send_counts, recv_counts, group=None):
+def exchange(send_buf, recv_buf, send_counts, recv_counts, group=None, host_staging: bool = False):
     """Send send_buf[soff[p]:soff[p+1]] to every peer p and receive
-    recv_buf[roff[p]:roff[p+1]] from it (one batched group of P2P ops)."""
+    recv_buf[roff[p]:roff[p+1]] from it (one batched group of P2P ops).
+    host_staging: move CUDA buffers through host memory (gloo transport,
+    used to run several ranks on one GPU in tests; NCCL moves them directly)."""
     import torch.distributed as dist
+    if host_staging and send_buf.is_cuda:
+        rh = recv_buf.new_empty(recv_buf.shape, device="cpu")
+        exchange(send_buf.cpu(), rh, send_counts, recv_counts, group)
+        recv_buf.copy_(rh)
+        return
     soff, roff = offsets(send_counts), offsets(recv_counts)
     ops = []
     for p in range(len(send_counts)):
