@@ -57,6 +57,9 @@ def fp64_peak():
 # T10 per-block count of 71.9 flop), a model figure (+-20 %).
 FLOP_PER_QP = {("t10", False): 468, ("t10", True): 4420, ("ancf", False): 684, ("ancf", True): 10252,
                ("beam", False): 380, ("beam", True): 2970}
+# Mooney-Rivlin + Kelvin-Voigt, T10 Keast-5, force + tangent: the SURVEY
+# §8(d) hand model of ~46 kflop per element (+-30 %), i.e. per qp
+FLOP_PER_QP_MR_T10 = 46000 // 5
 
 
 def env_rank():
@@ -359,7 +362,10 @@ def run_ours(args):
     if dom == "element":
         bpe = bytes_per_element(mesh, info, not force_only, kv)
         bytes_launch = bpe * info["n_elements"]
-        flops_launch = FLOP_PER_QP[(elem, not force_only)] * info["n_qp"] * info["n_elements"]
+        per_qp = FLOP_PER_QP[(elem, not force_only)]
+        if elem == "t10" and cfg.material["model"] == 1 and not force_only:
+            per_qp = FLOP_PER_QP_MR_T10
+        flops_launch = per_qp * info["n_qp"] * info["n_elements"]
     elif dom == "fused":
         bytes_launch = fused_bytes_per_element(mesh, info, kv) * info["n_elements"]
         flops_launch = (FLOP_PER_QP[(elem, True)] * info["n_qp"] * info["n_elements"]
