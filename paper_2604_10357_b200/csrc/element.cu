@@ -828,7 +828,10 @@ __global__ void k_gather_units(int64_t n_units, int nen, int nub, const int32_t*
 // double-buffered per warp: one elected lane moves the next window of the
 // contiguous scratch range while the warp sums the current one.
 constexpr int kG3Warps = 4;
-constexpr int kG3WB = 64;                    // blocks per window
+#ifndef TLFEA_G3WB
+#define TLFEA_G3WB 64
+#endif
+constexpr int kG3WB = TLFEA_G3WB;            // blocks per window
 constexpr int kG3Buf = kG3WB * 9 + 2;        // doubles per buffer (+16 B alignment slack)
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
