@@ -131,6 +131,7 @@ struct Context {
   int n_cls = 0;                  // 0 = per-element tables (gradN / J0w above)
   uint8_t* cls = nullptr;         // [n_el] class id
   double* cls_tab = nullptr;      // [n_cls][nq][nen*3 + 1]  (gradN then J0w)
+  std::vector<int64_t> cls_rep;   // representative (first) element of each class
   // symmetric H gather units (upper blocks + blocks whose transpose is not owned)
   int64_t n_units = 0;
   int32_t* unit_p = nullptr;      // [n_units] coefficient block of (I,J)

@@ -372,13 +372,19 @@ __global__ void k_mass_pairs(int64_t n_el, int nen, const int32_t* __restrict__ 
   val[t] = t;
 }
 
+// M_IJ = sum of the element mass entries of block (I,J) in element order.
+// cls != nullptr: congruent elements share their class's mass matrix
+// (me then holds one nen x nen matrix per class).
 __global__ void k_mass_gather(int64_t nnz_c, const int32_t* __restrict__ ptr,
                               const int64_t* __restrict__ ent, const double* __restrict__ me,
-                              double* __restrict__ M) {
+                              const uint8_t* __restrict__ cls, int nen2, double* __restrict__ M) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= nnz_c) return;
   double s = 0.0;
-  for (int32_t k = ptr[p]; k < ptr[p + 1]; ++k) s += me[ent[k]];
+  for (int32_t k = ptr[p]; k < ptr[p + 1]; ++k) {
+    const int64_t t = ent[k];
+    s += cls ? me[(int64_t)cls[t / nen2] * nen2 + t % nen2] : me[t];
+  }
   M[p] = s;
 }
 
@@ -662,6 +668,7 @@ static tlfea_status build_geometry_classes(Context* c, const double* dX) {
   TL_TRY(c->alloc(&c->cls, (size_t)n));
   k_geom_assign<<<grid_for(n, 256), 256>>>(n, key2.p, idx2.p, run.p, c->cls);
   TL_CHECK_LAUNCH();
+  c->cls_rep = rep;
   TmpArr<int64_t> drep;
   TL_TRY(drep.get(rep.size()));
   TL_CUDA(cudaMemcpy(drep.p, rep.data(), sizeof(int64_t) * rep.size(), cudaMemcpyHostToDevice));
@@ -1372,11 +1379,35 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     TL_CUDA(cudaMemcpy(dmq.p, mq, sizeof(double) * 3 * nmq, cudaMemcpyHostToDevice));
     TL_CUDA(cudaMemcpy(dmw.p, mw, sizeof(double) * nmq, cudaMemcpyHostToDevice));
     const int64_t nm = NS * nen * nen;
-    TL_TRY(me.get(nm));
-    if (NS > 0) {
-      k_element_mass<<<grid_for(NS, 64), 64>>>(c->element, NS, nen, nmq, dsconn.p, dX, dsdims.p, dmq.p,
-                                              dmw.p, c->mat.rho0, me.p);
+    // single rank with geometry classes: one mass matrix per class (its
+    // representative element), read through the class id in the gather
+    const bool per_class = c->nranks == 1 && c->n_cls > 0 && NS == c->n_el;
+    TmpArr<int32_t> rconn;
+    TmpArr<double> rdims;
+    if (per_class) {
+      const int64_t nr = (int64_t)c->cls_rep.size();
+      std::vector<int32_t> hc((size_t)nr * nen);
+      std::vector<double> hd(dims.empty() ? 1 : (size_t)nr * 3, 0.0);
+      for (int64_t r = 0; r < nr; ++r) {
+        for (int a = 0; a < nen; ++a) hc[r * nen + a] = cc[c->cls_rep[r] * nen + a];
+        if (!dims.empty())
+          for (int k = 0; k < 3; ++k) hd[r * 3 + k] = dims[c->cls_rep[r] * 3 + k];
+      }
+      TL_TRY(rconn.get(hc.size()));
+      TL_TRY(rdims.get(hd.size()));
+      TL_TRY(me.get((size_t)nr * nen * nen));
+      TL_CUDA(cudaMemcpy(rconn.p, hc.data(), sizeof(int32_t) * hc.size(), cudaMemcpyHostToDevice));
+      TL_CUDA(cudaMemcpy(rdims.p, hd.data(), sizeof(double) * hd.size(), cudaMemcpyHostToDevice));
+      k_element_mass<<<grid_for(nr, 64), 64>>>(c->element, nr, nen, nmq, rconn.p, dX, dims.empty() ? nullptr : rdims.p,
+                                              dmq.p, dmw.p, c->mat.rho0, me.p);
       TL_CHECK_LAUNCH();
+    } else {
+      TL_TRY(me.get(nm));
+      if (NS > 0) {
+        k_element_mass<<<grid_for(NS, 64), 64>>>(c->element, NS, nen, nmq, dsconn.p, dX, dsdims.p, dmq.p,
+                                                dmw.p, c->mat.rho0, me.p);
+        TL_CHECK_LAUNCH();
+      }
     }
     TmpArr<int32_t> key;
     TmpArr<int64_t> val, sorted;
@@ -1393,7 +1424,8 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     int64_t nvalid = 0;
     TL_TRY(sort_and_ptr<int64_t>(nm, key.p, val.p, c->nnz_c, mptr.p, &sv, &nvalid, sorted));
     if (c->nnz_c > 0) {
-      k_mass_gather<<<grid_for(c->nnz_c, 256), 256>>>(c->nnz_c, mptr.p, sv, me.p, c->M);
+      k_mass_gather<<<grid_for(c->nnz_c, 256), 256>>>(c->nnz_c, mptr.p, sv, me.p, per_class ? c->cls : nullptr,
+                                                      nen * nen, c->M);
       TL_CHECK_LAUNCH();
     }
     if (c->n_own > 0) {
