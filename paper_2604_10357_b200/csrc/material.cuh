@@ -80,6 +80,9 @@ struct MRState {
   double C[6], Ci[6], J, I1, I2, J23, J43;
 };
 
+// 1/3 as a product: fp64 division is a long instruction sequence on the GPU
+constexpr double kThird = 1.0 / 3.0;
+
 __host__ __device__ __forceinline__ void mr_state(const double F[9], MRState& s) {
   right_cauchy_green(F, s.C);
   sym_inv(s.C, s.Ci);
@@ -88,14 +91,18 @@ __host__ __device__ __forceinline__ void mr_state(const double F[9], MRState& s)
   const double CC = s.C[0] * s.C[0] + s.C[1] * s.C[1] + s.C[2] * s.C[2] +
                     2.0 * (s.C[3] * s.C[3] + s.C[4] * s.C[4] + s.C[5] * s.C[5]);
   s.I2 = 0.5 * (s.I1 * s.I1 - CC);
+#ifdef __CUDA_ARCH__
+  s.J23 = rcbrt(s.J * s.J);
+#else
   s.J23 = 1.0 / cbrt(s.J * s.J);
+#endif
   s.J43 = s.J23 * s.J23;
 }
 
 __host__ __device__ __forceinline__ void mr_S(const MRState& s, double C10, double C01,
                                               double kappa, double S[6]) {
   const double a = 2.0 * C10 * s.J23, b = 2.0 * C01 * s.J43;
-  const double cinv = -a * s.I1 / 3.0 - b * 2.0 * s.I2 / 3.0 + kappa * s.J * (s.J - 1.0);
+  const double cinv = -(a * s.I1 + 2.0 * b * s.I2) * kThird + kappa * s.J * (s.J - 1.0);
 #pragma unroll
   for (int v = 0; v < 6; ++v) {
     const double id = v < 3 ? 1.0 : 0.0;
@@ -117,9 +124,9 @@ __host__ __device__ __forceinline__ void mr_Cv_column(const MRState& s, double C
   const double dI2 = s.I1 * dI1 - CdC;
   const double a = 2.0 * C10 * s.J23, b = 2.0 * C01 * s.J43;
   const double da = -(2.0 / 3.0) * tau * a, db = -(4.0 / 3.0) * tau * b;
-  const double cinv = -a * s.I1 / 3.0 - b * 2.0 * s.I2 / 3.0 + kappa * s.J * (s.J - 1.0);
-  const double dcinv = -da * s.I1 / 3.0 - a * dI1 / 3.0 - db * 2.0 * s.I2 / 3.0 -
-                       b * 2.0 * dI2 / 3.0 + kappa * (2.0 * s.J - 1.0) * s.J * tau;
+  const double cinv = -(a * s.I1 + 2.0 * b * s.I2) * kThird + kappa * s.J * (s.J - 1.0);
+  const double dcinv = -(da * s.I1 + a * dI1 + 2.0 * (db * s.I2 + b * dI2)) * kThird +
+                       kappa * (2.0 * s.J - 1.0) * s.J * tau;
 #pragma unroll
   for (int v = 0; v < 6; ++v) {
     int i, j;
