@@ -258,10 +258,13 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
     } else {
       const int comp = lane & 15;
       if (comp < 9 && (KV || half == 0)) {
-        double s = 0.0;
+        // pairwise tree over the 16 node partials (depth 4 instead of a 16-long chain)
+        const double* p = &s_part[wib][9 * half + comp][0];
+        double t8[8];
 #pragma unroll
-        for (int b = 0; b < NEN; ++b) s += s_part[wib][9 * half + comp][b];
-        s_F[wib][0][9 * half + comp] = s;
+        for (int b = 0; b < 8; ++b) t8[b] = p[2 * b] + p[2 * b + 1];
+        s_F[wib][0][9 * half + comp] =
+            ((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]));
       }
     }
     __syncwarp();
