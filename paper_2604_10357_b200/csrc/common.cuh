@@ -156,7 +156,9 @@ struct Context {
   uint32_t* fz_list = nullptr;    // [fz_items] type << 30 | index (0 element, 1 H gather, 2 f gather)
   int32_t* fz_lo = nullptr;       // [fz_nG + fz_nF] first element chunk read by a gather item
   int32_t* fz_hi = nullptr;       // [fz_nG + fz_nF] last element chunk read
-  uint32_t* fz_sync = nullptr;    // [1 + fz_chunks]: work ticket, completed element items per chunk
+  uint32_t* fz_sync = nullptr;
+  unsigned long long* g4_ticket = nullptr;  // H gather v4 work ticket (monotone across launches)
+  unsigned long long g4_base = 0;           // its value at the next launch's start    // [1 + fz_chunks]: work ticket, completed element items per chunk
   double* Kscr = nullptr;         // [n_el][n_ublk][9]
   double* fscr = nullptr;         // [n_el][nen][3]
   unsigned long long* err_flag = nullptr;  // min over (e*64+q) with det F <= 0 (MR)

@@ -81,6 +81,14 @@ __device__ __forceinline__ int partner(int a, int half, int j) {
 // halve the accumulators, so T10 SVK fits 4 CTAs (128 registers) without
 // spills — measured faster (config 3: 11.2 vs 11.4-12.8 ms). Mooney-Rivlin
 // and ANCF measured slower with two passes (their per-q work is larger).
+#ifndef TLFEA_2PH_QUNROLL
+#define TLFEA_2PH_QUNROLL 2  // phase-B quadrature loop (config 3: 2 -> 10.72 ms, 1 -> 11.0, 5 spills)
+#endif
+constexpr int kQUnroll = TLFEA_2PH_QUNROLL;
+#ifndef TLFEA_2PH_AUNROLL
+#define TLFEA_2PH_AUNROLL 10
+#endif
+constexpr int kAUnroll = TLFEA_2PH_AUNROLL;  // phase A node loops
 #ifndef TLFEA_T10_SVK_NPASS
 #define TLFEA_T10_SVK_NPASS 2
 #endif
@@ -475,6 +483,219 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
   }  // pass
 }
 
+// T10 + SVK (no Kelvin-Voigt) + geometry classes, two phases per warp group.
+// The lane-per-node layout of element_group recomputes the per-q kinematics
+// (F reduction, S, F F^T, g_a) on all 10 lanes of an element and again in
+// every block pass: about half of its fp64 instructions. Here
+//   phase A: lane (element, q), 15 of 32 lanes, computes F = sum_a x_a (x) grad N_a
+//            (Eq. F_assembly), S (reading Q5), F F^T and g_b = F grad N_b for the
+//            element's 10 nodes once, into shared memory;
+//   phase B: lane (element, node a) accumulates its upper blocks
+//            K_ab = s_ab I + lam g_a g_b^T + mu g_b g_a^T + mu d_ab F F^T
+//            (Eq. tangent_block) and f_a = sum_q F (w S grad N_a)
+//            (Eq. fint_local) from shared memory only; the second block pass
+//            re-reads instead of recomputing.
+#ifndef TLFEA_T10_2PH_NPASS
+#define TLFEA_T10_2PH_NPASS 3  // re-reading passes are cheap here: 3 x 2 blocks fit 128 registers without spills
+#endif
+template <int NQ>
+__device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab) {
+  constexpr int NEN = 10, GROUP = 10, EPW = 3, NUB = 55, NB = 6, TABW = 3 * NEN + 1;
+  constexpr int NPASS = TLFEA_T10_2PH_NPASS;
+  constexpr int NBP = (NB + NPASS - 1) / NPASS;
+  constexpr int KQ = 21;  // per (element, q): F (9), S (6), F F^T (6)
+  __shared__ double s_ga[kWarps][NQ][3][kLD];
+  __shared__ double s_k[kWarps][EPW][NQ][KQ];
+  __shared__ double s_x[kWarps][EPW][3 * NEN];
+  __shared__ double s_part[kWarps][9][kLD];
+  __shared__ int32_t s_dst[kWarps][EPW * NUB];
+  __shared__ int32_t s_pos[kWarps][32];
+  __shared__ int32_t s_cls[kWarps][EPW];
+  const int64_t n_el = A.n_el;
+  const MatDev& mat = A.mat;
+  const int32_t* __restrict__ dest = A.dest;
+  double* __restrict__ Kscr = A.Kscr;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const bool lane_active = lane < EPW * GROUP;
+  const int g = lane_active ? lane / GROUP : 0;
+  const int a = lane_active ? lane % GROUP : 0;
+  const int64_t e = grp * EPW + g;
+  const bool valid = lane_active && e < n_el;
+  const int gbase = g * GROUP;
+  const bool write = dest && !mat.dbg_nowrite;
+  if (write) {
+    const int64_t e0 = grp * EPW, lim = (n_el - e0) * NUB;
+    for (int t = lane; t < EPW * NUB; t += 32)
+      if (t < lim) pf_cp4(&s_dst[wib][t], dest + e0 * NUB + t);
+  }
+  if (lane_active) {
+    double xa[3] = {0, 0, 0};
+    int ce = 0;
+    if (valid) {
+      const int64_t I = A.conn[e * NEN + a];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) xa[i] = A.x[3 * I + i];
+      if (a == 0) ce = A.cls[e];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s_x[wib][g][3 * a + i] = xa[i];
+    if (a == 0) s_cls[wib][g] = ce;
+  }
+  __syncwarp();
+  // ---- phase A: one lane per (element, q)
+  if (lane < EPW * NQ) {
+    const int ge = lane / NQ, q = lane - NQ * (lane / NQ);
+    const double* t = s_tab + (s_cls[wib][ge] * NQ + q) * TABW;
+    const double* xs = s_x[wib][ge];
+    double F[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) F[r] = 0.0;
+#pragma unroll kAUnroll
+    for (int b = 0; b < NEN; ++b) {
+      const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double xi = xs[3 * b + i];
+        F[3 * i] = fma(xi, n0, F[3 * i]);
+        F[3 * i + 1] = fma(xi, n1, F[3 * i + 1]);
+        F[3 * i + 2] = fma(xi, n2, F[3 * i + 2]);
+      }
+    }
+    double S[6];
+    svk_S(F, mat.lam, mat.mu, S);
+    double* kq = s_k[wib][ge][q];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) kq[r] = F[r];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) kq[9 + r] = S[r];
+#pragma unroll
+    for (int vv = 0; vv < 6; ++vv) {
+      int i, k;
+      voigt_pair(vv, i, k);
+      kq[15 + vv] = F[3 * i] * F[3 * k] + F[3 * i + 1] * F[3 * k + 1] + F[3 * i + 2] * F[3 * k + 2];
+    }
+#pragma unroll kAUnroll
+    for (int b = 0; b < NEN; ++b) {
+      const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) s_ga[wib][q][i][ge * GROUP + b] = F[3 * i] * n0 + F[3 * i + 1] * n1 + F[3 * i + 2] * n2;
+    }
+  }
+  __syncwarp();
+  // ---- phase B: one lane per (element, node a)
+  const int ce = s_cls[wib][g];
+  double fa[3] = {0, 0, 0};
+  double K[NBP][9];
+#pragma unroll 1
+  for (int pass = 0; pass < NPASS; ++pass) {
+#pragma unroll
+    for (int j = 0; j < NBP; ++j)
+#pragma unroll
+      for (int r = 0; r < 9; ++r) K[j][r] = 0.0;
+#pragma unroll kQUnroll
+    for (int q = 0; q < NQ; ++q) {
+      const double* t = s_tab + (ce * NQ + q) * TABW;
+      const double* kq = s_k[wib][g][q];
+      const double gN[3] = {t[3 * a], t[3 * a + 1], t[3 * a + 2]};
+      const double w = t[3 * NEN];
+      double S[6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) S[r] = kq[9 + r];
+      double tw[3];  // w S grad N_a
+#pragma unroll
+      for (int I = 0; I < 3; ++I) tw[I] = w * (sget(S, I, 0) * gN[0] + sget(S, I, 1) * gN[1] + sget(S, I, 2) * gN[2]);
+      if (pass == 0) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          fa[i] = fma(kq[3 * i], tw[0], fma(kq[3 * i + 1], tw[1], fma(kq[3 * i + 2], tw[2], fa[i])));
+      }
+      const double lw = mat.lam * w, mw = mat.mu * w;
+      double gl[3], gm[3], gNm[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double gai = s_ga[wib][q][i][lane];
+        gl[i] = lw * gai;
+        gm[i] = mw * gai;
+        gNm[i] = mw * gN[i];
+      }
+      double B[6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) B[r] = kq[15 + r];
+#pragma unroll
+      for (int jj = 0; jj < NBP; ++jj) {
+        const int j = pass * NBP + jj;
+        const int b = j < NB ? partner<0>(a, 0, j) : -1;
+        if (b < 0) continue;
+        double* Kj = K[jj];
+        const int lb = gbase + b;
+        const double gb[3] = {s_ga[wib][q][0][lb], s_ga[wib][q][1][lb], s_ga[wib][q][2][lb]};
+        const double nb[3] = {t[3 * b], t[3 * b + 1], t[3 * b + 2]};
+        const double s = fma(tw[0], nb[0], fma(tw[1], nb[1], tw[2] * nb[2]));
+        const double d = fma(gNm[0], nb[0], fma(gNm[1], nb[1], gNm[2] * nb[2]));
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            double acc = fma(gl[i], gb[k], fma(gb[i], gm[k], fma(d, B[vidx(i, k)], Kj[3 * i + k])));
+            Kj[3 * i + k] = (i == k) ? acc + s : acc;
+          }
+      }
+    }
+    if (valid && pass == 0) {
+      const int64_t fp = A.fdest ? (int64_t)A.fdest[e * NEN + a] : e * NEN + a;
+      double* fo = A.fscr + fp * 3;
+      fo[0] = fa[0];
+      fo[1] = fa[1];
+      fo[2] = fa[2];
+    }
+    if (!mat.dbg_nowrite) {
+      // warp-staged block stores, as in element_group
+      constexpr int NLB = EPW * GROUP, NIT = (NLB + 2) / 3;
+      const int bi = lane / 9, rr = lane - 9 * (lane / 9);
+      if (write && pass == 0) {
+        pf_wait();
+        __syncwarp();
+      }
+#pragma unroll
+      for (int jj = 0; jj < NBP; ++jj) {
+        const int j = pass * NBP + jj;
+        const int b = (valid && j < NB) ? partner<0>(a, 0, j) : -1;
+        int32_t pos = -1;
+        if (b >= 0) {
+          const double* Kj = K[jj];
+          const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
+          bool tr = a > b;
+          pos = (int32_t)(e * NUB + ub);
+          if (dest) {
+            const int32_t dd = s_dst[wib][g * NUB + ub];
+            pos = dd >> 1;
+            tr = tr != ((dd & 1) != 0);
+          }
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) s_part[wib][tr ? 3 * k + i : 3 * i + k][lane] = Kj[3 * i + k];
+        }
+        s_pos[wib][lane] = pos;
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+          const int blk = 3 * it + bi;
+          if (lane < 27 && blk < NLB) {
+            const int32_t p = s_pos[wib][blk];
+            if (p >= 0) k_store(Kscr + (int64_t)p * 9 + rr, s_part[wib][rr][blk]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+#ifndef TLFEA_T10_2PH
+#define TLFEA_T10_2PH 1  // T10 SVK class-mode tangent eval through element_group_t10svk
+#endif
+
 template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS>
 __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>()) k_element(ElArgs A) {
   extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
@@ -486,9 +707,13 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>()) k_
   // A.cta_tiles consecutive tiles per CTA (class tables staged once)
   const int64_t t0 = (int64_t)blockIdx.x * A.cta_tiles;
 #pragma unroll 1
-  for (int k = 0; k < A.cta_tiles; ++k)
-    element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, TLFEA_DEST_ASYNC != 0>(
-        (t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
+  for (int k = 0; k < A.cta_tiles; ++k) {
+    if constexpr (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && TAN && CLS)
+      element_group_t10svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
+    else
+      element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, TLFEA_DEST_ASYNC != 0>(
+          (t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
+  }
 }
 
 
@@ -868,6 +1093,8 @@ struct GatherArgs {
   double h;
   double* H;
   int upper;  // UPPER H storage (u_deg = L | diagonal << 16, no transposed copy)
+  int sortT;  // transposed writes in address order across the warp (TLFEA_G3SORT)
+  int dbg_gt; // diagnostics (TLFEA_DBG_GT=1, timing only, corrupts the scratch): transposes to contiguous scratch
 };
 
 // Per-warp TMA staging: two windows and their mbarriers. `wk` counts the
@@ -931,7 +1158,7 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
     __syncwarp();
   }
   W.wk = wk0 + nwin;
-  if (!valid) return;
+  if (!valid && !(A.sortT && !A.upper)) return;
   const double mh = m / h;
   if (A.upper) {
     // UPPER storage (common.cuh): entry (d, f) at off + f + d (2 + 3 L) - d (d-1)/2,
@@ -948,10 +1175,54 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
   }
   const int deg = dg & 0xffff, degT = dg >> 16;
   double* out = H + off;
+  if (valid) {
 #pragma unroll
-  for (int d = 0; d < 3; ++d)
+    for (int d = 0; d < 3; ++d)
 #pragma unroll
-    for (int f = 0; f < 3; ++f) h_store(out + 3 * d * deg + f, fma(h, acc[3 * d + f], d == f ? mh : 0.0));
+      for (int f = 0; f < 3; ++f) h_store(out + 3 * d * deg + f, fma(h, acc[3 * d + f], d == f ? mh : 0.0));
+  }
+  if (A.dbg_gt) {
+    double* o2 = const_cast<double*>(Kscr) + P0 * 9 + lane;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int f = 0; f < 3; ++f) o2[32 * (3 * d + f)] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
+    return;
+  }
+  if (A.sortT) {
+    // Transposed blocks (J,I) of the group's units lie in many rows J; sorted
+    // by H offset across the warp (bitonic network over (offT, lane)), lanes
+    // holding adjacent pieces of one row J write them in the same instruction.
+    double* st = W.buf[0];  // both windows are consumed: reuse as [32][9] staging
+#pragma unroll
+    for (int r = 0; r < 9; ++r) st[r * 32 + lane] = acc[r];
+    uint32_t key = valid ? (uint32_t)offT : 0xffffffffu;
+    int src = lane;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const uint32_t ok = __shfl_xor_sync(0xffffffffu, key, j);
+        const int os = __shfl_xor_sync(0xffffffffu, src, j);
+        const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+        const bool less = ok < key || (ok == key && os < src);
+        if (lower == up ? less : !less) {
+          key = ok;
+          src = os;
+        }
+      }
+    const int dT = __shfl_sync(0xffffffffu, dg, src) >> 16;
+    const double mT = __shfl_sync(0xffffffffu, m, src) / h;
+    __syncwarp();
+    if (key != 0xffffffffu) {
+      double* o2 = H + (int32_t)key;
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int f = 0; f < 3; ++f) h_store(o2 + 3 * d * dT + f, fma(h, st[(3 * f + d) * 32 + src], d == f ? mT : 0.0));
+    }
+    return;
+  }
   if (offT >= 0) {
     double* o2 = H + offT;
 #pragma unroll
@@ -981,6 +1252,145 @@ __global__ void __launch_bounds__(kG3Warps * 32) k_gather_units_v3(GatherArgs A)
   G3Warp W;
   g3_init(s_buf, s_bar, W);
   gather_units_warp(((int64_t)blockIdx.x * kG3Warps + (threadIdx.x >> 5)) * 32, A, W);
+}
+
+// v4: persistent warps over 32-unit groups in grid-stride order (the groups
+// in flight stay a compact window of the unit list, as with v3's launch
+// order), with the window stream pipelined ACROSS groups: the next group's
+// metadata is loaded while the current group is summed, and its first TMA
+// window is issued while the current group's last window is consumed, so a
+// warp always has one window in flight instead of paying the metadata and
+// first-window latencies per group.
+struct G4Meta {
+  int64_t P0, P1;
+  int32_t my0, my1, off, offT, dg;
+  double m;
+};
+
+__device__ __forceinline__ void g4_meta(int64_t u0, const GatherArgs& A, G4Meta& M) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = u0 + lane, uend = min(u0 + 32, A.n_units);
+  M.P0 = A.unit_ptr[u0];
+  M.P1 = A.unit_ptr[uend];
+  M.my0 = M.my1 = M.dg = 0;
+  M.off = 0;
+  M.offT = -1;
+  M.m = 0.0;
+  if (u < A.n_units) {
+    M.my0 = A.unit_ptr[u];
+    M.my1 = A.unit_ptr[u + 1];
+    M.off = A.u_off[u];
+    M.offT = A.u_offT[u];
+    M.dg = A.u_deg[u];
+    M.m = A.u_m[u];
+  }
+}
+
+__device__ __forceinline__ void g4_issue(const double* Kscr, int64_t P0, int64_t P1, int k, double* buf, uint64_t* bar) {
+  const int64_t w0 = P0 + (int64_t)k * kG3WB, w1 = min(w0 + (int64_t)kG3WB, P1);
+  const uintptr_t a = (uintptr_t)(Kscr + w0 * 9) & ~(uintptr_t)15;
+  const uintptr_t b = ((uintptr_t)(Kscr + w1 * 9) + 15) & ~(uintptr_t)15;
+  bulk_load(buf, (const void*)a, (unsigned)(b - a), bar);
+}
+
+__device__ __forceinline__ void g4_write(const GatherArgs& A, const G4Meta& M, const double* acc) {
+  const double h = A.h, mh = M.m / h;
+  double* __restrict__ H = A.H;
+  if (A.upper) {
+    const int L = M.dg & 0xffff;
+    const bool diag = (M.dg >> 16) != 0;
+    double* out = H + M.off;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int f = 0; f < 3; ++f)
+        if (!diag || f >= d) out[f + d * (2 + 3 * L) - d * (d - 1) / 2] = fma(h, acc[3 * d + f], d == f ? mh : 0.0);
+    return;
+  }
+  const int deg = M.dg & 0xffff, degT = M.dg >> 16;
+  double* out = H + M.off;
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int f = 0; f < 3; ++f) h_store(out + 3 * d * deg + f, fma(h, acc[3 * d + f], d == f ? mh : 0.0));
+  if (M.offT >= 0) {
+    double* o2 = H + M.offT;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int f = 0; f < 3; ++f) h_store(o2 + 3 * d * degT + f, fma(h, acc[3 * f + d], d == f ? mh : 0.0));
+  }
+}
+
+__global__ void __launch_bounds__(kG3Warps * 32)
+    k_gather_units_v4(GatherArgs A, int64_t n_groups, unsigned long long* ticket, unsigned long long base) {
+  __shared__ __align__(16) double s_buf[kG3Warps][2][kG3Buf];
+  __shared__ __align__(8) uint64_t s_bar[kG3Warps][2];
+  G3Warp W;
+  g3_init(s_buf, s_bar, W);
+  const int lane = threadIdx.x & 31;
+  const double* __restrict__ Kscr = A.Kscr;
+  // groups are handed out by a global ticket in list order (like the block
+  // scheduler's launch order): every warp takes exactly one ticket past the
+  // end, so each launch advances the counter by n_groups + warps in the grid
+  auto take = [&]() -> int64_t {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1ull);
+    return (int64_t)(__shfl_sync(0xffffffffu, t, 0) - base);
+  };
+  int64_t g = take();
+  if (g >= n_groups) return;
+  G4Meta cur;
+  g4_meta(g * 32, A, cur);
+  uint32_t wi = 0;  // windows issued by this warp (buffer wi & 1)
+  uint32_t wc = 0;  // windows consumed (buffer wc & 1, phase (wc >> 1) & 1)
+  if (lane == 0 && cur.P1 > cur.P0) {
+    g4_issue(Kscr, cur.P0, cur.P1, 0, W.buf[wi & 1], &W.bar[wi & 1]);
+    ++wi;
+  }
+#pragma unroll 1
+  for (;;) {
+    const int64_t gn = take();
+    const bool has_next = gn < n_groups;
+    G4Meta nxt;
+    if (has_next) g4_meta(gn * 32, A, nxt);
+    const int nwin = (int)((cur.P1 - cur.P0 + kG3WB - 1) / kG3WB);
+    bool next_issued = false;
+    double acc[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) acc[r] = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < nwin; ++k) {
+      if (k + 1 < nwin) {
+        if (lane == 0) g4_issue(Kscr, cur.P0, cur.P1, k + 1, W.buf[wi & 1], &W.bar[wi & 1]);
+        ++wi;
+      } else if (has_next && nxt.P1 > nxt.P0) {
+        if (lane == 0) g4_issue(Kscr, nxt.P0, nxt.P1, 0, W.buf[wi & 1], &W.bar[wi & 1]);
+        ++wi;
+        next_issued = true;
+      }
+      mbar_wait(&W.bar[wc & 1], (wc >> 1) & 1);
+      const int64_t w0 = cur.P0 + (int64_t)k * kG3WB, w1 = min(w0 + (int64_t)kG3WB, cur.P1);
+      const int delta = (int)(((uintptr_t)(Kscr + w0 * 9) & 15) >> 3);
+      const double* buf = W.buf[wc & 1] + delta;
+      const int64_t a0 = max((int64_t)cur.my0, w0), a1 = min((int64_t)cur.my1, w1);
+      for (int64_t t = a0; t < a1; ++t) {
+        const double* sb = buf + (t - w0) * 9;
+#pragma unroll
+        for (int r = 0; r < 9; ++r) acc[r] += sb[r];
+      }
+      ++wc;
+      __syncwarp();
+    }
+    if (!next_issued && has_next && nxt.P1 > nxt.P0) {
+      if (lane == 0) g4_issue(Kscr, nxt.P0, nxt.P1, 0, W.buf[wi & 1], &W.bar[wi & 1]);
+      ++wi;
+    }
+    if (g * 32 + lane < A.n_units) g4_write(A, cur, acc);
+    if (!has_next) break;
+    cur = nxt;
+    g = gn;
+  }
 }
 
 // ------------------------------------------------- fused persistent eval
@@ -1048,8 +1458,12 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, 1>()) k_fuse
       const int64_t t0 = (int64_t)k * P.etiles;
       if (!(P.dbg & 2)) {
 #pragma unroll 1
-        for (int j = 0; j < P.etiles; ++j)
-          element_group<ELEM, NQ, MODEL, KV, true, true, 1>((t0 + j) * kWarps + wib, P.el, s_tab);
+        for (int j = 0; j < P.etiles; ++j) {
+          if constexpr (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV)
+            element_group_t10svk<NQ>((t0 + j) * kWarps + wib, P.el, s_tab);
+          else
+            element_group<ELEM, NQ, MODEL, KV, true, true, 1>((t0 + j) * kWarps + wib, P.el, s_tab);
+        }
       }
       // publish: the CTA's stores -> barrier -> one gpu-scope release by thread 0
       __syncthreads();
@@ -1222,6 +1636,20 @@ static GatherArgs gather_args(const Context* c, double h, double* H) {
   A.h = h;
   A.H = H;
   A.upper = c->upper;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("TLFEA_DBG_GT");
+      dbg = e ? atoi(e) : 0;
+    }
+    A.dbg_gt = dbg;
+    static int srt = -1;
+    if (srt < 0) {
+      const char* e = getenv("TLFEA_G3SORT");
+      srt = e ? atoi(e) : 0;
+    }
+    A.sortT = srt;
+  }
   return A;
 }
 
@@ -1311,6 +1739,27 @@ tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
   if (c->n_units == 0) return TLFEA_OK;
   if (c->u_off) {
     const int64_t per = (int64_t)kG3Warps * 32;
+    static int g4 = -1, g4_grid = 0;
+    if (g4 < 0) {
+      const char* e = getenv("TLFEA_G4");
+      g4 = e ? atoi(e) : 0;  // measured slower than v3 on config 3
+      int per_sm = 0, n_sm = 0, dev = 0;
+      TL_CUDA(cudaGetDevice(&dev));
+      TL_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+      TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_units_v4, kG3Warps * 32, 0));
+      const char* m = getenv("TLFEA_G4_CTAS");  // CTAs per SM override
+      if (m) per_sm = std::min(per_sm, atoi(m));
+      g4_grid = std::max(1, per_sm) * n_sm;
+    }
+    if (g4 && c->g4_ticket) {
+      const int64_t n_groups = (c->n_units + 31) / 32;
+      const int64_t grid = std::min<int64_t>(g4_grid, (n_groups + kG3Warps - 1) / kG3Warps);
+      k_gather_units_v4<<<(unsigned)grid, kG3Warps * 32, 0, s>>>(gather_args(c, h, H), n_groups, c->g4_ticket,
+                                                                  c->g4_base);
+      TL_CHECK_LAUNCH();
+      c->g4_base += (unsigned long long)n_groups + (unsigned long long)grid * kG3Warps;
+      return TLFEA_OK;
+    }
     k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(gather_args(c, h, H));
     TL_CHECK_LAUNCH();
     return TLFEA_OK;

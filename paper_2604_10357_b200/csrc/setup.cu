@@ -687,6 +687,32 @@ static tlfea_status build_geometry_classes(Context* c, const double* dX) {
   return TLFEA_OK;
 }
 
+// Tile order of the gather units: key (I >> t, J >> t, I & m, J & m), so a
+// 32-unit gather group covers a few 2^t x 2^t tiles of the block pattern and
+// both its direct (I,J) and its transposed (J,I) writes land in short runs of
+// adjacent blocks (with the plain (I,J) order the transposes are isolated
+// 24-byte pieces, one row each).
+__global__ void k_unit_tilekey(int64_t nu, int t, const int32_t* __restrict__ unit_p,
+                               const int32_t* __restrict__ blk_row, const int32_t* __restrict__ own_nodes,
+                               const int32_t* __restrict__ cols_c, unsigned long long* __restrict__ key,
+                               int32_t* __restrict__ idx) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= nu) return;
+  const int32_t p = unit_p[u];
+  const unsigned long long I = (unsigned)own_nodes[blk_row[p]], J = (unsigned)cols_c[p];
+  const unsigned long long m = (1ull << t) - 1;
+  key[u] = (((I >> t) << (31 - t)) | (J >> t)) << (2 * t) | ((I & m) << t) | (J & m);
+  idx[u] = (int32_t)u;
+}
+
+__global__ void k_permute2(int64_t n, const int32_t* __restrict__ idx, const int32_t* __restrict__ a,
+                           const int32_t* __restrict__ b, int32_t* __restrict__ a2, int32_t* __restrict__ b2) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  a2[u] = a[idx[u]];
+  b2[u] = b[idx[u]];
+}
+
 static tlfea_status build_units(Context* c) {
   c->n_units = 0;
   if (c->nnz_c == 0) return TLFEA_OK;
@@ -720,6 +746,25 @@ static tlfea_status build_units(Context* c) {
   TL_TRY(c->alloc(&c->unit_pT, (size_t)nu));
   TL_CUDA(cudaMemcpy(c->unit_p, up.p, sizeof(int32_t) * nu, cudaMemcpyDeviceToDevice));
   TL_CUDA(cudaMemcpy(c->unit_pT, upT.p, sizeof(int32_t) * nu, cudaMemcpyDeviceToDevice));
+  const char* ts = getenv("TLFEA_UNIT_TILE");
+  const int t = ts && ts[0] ? atoi(ts) : 0;
+  if (t > 0 && t < 16 && c->nranks == 1 && nu > 0) {
+    TmpArr<unsigned long long> key, key2;
+    TmpArr<int32_t> idx, idx2;
+    TL_TRY(key.get(nu));
+    TL_TRY(key2.get(nu));
+    TL_TRY(idx.get(nu));
+    TL_TRY(idx2.get(nu));
+    k_unit_tilekey<<<grid_for(nu, 256), 256>>>(nu, t, c->unit_p, c->blk_row, c->own_nodes, c->cols_c, key.p, idx.p);
+    TL_CHECK_LAUNCH();
+    bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, idx.p, idx2.p, nu, 0, 62);
+    TL_TRY(tmp.get(bytes));
+    TL_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, idx.p, idx2.p, nu, 0, 62));
+    count_launch();
+    k_permute2<<<grid_for(nu, 256), 256>>>(nu, idx2.p, up.p, upT.p, c->unit_p, c->unit_pT);
+    TL_CHECK_LAUNCH();
+  }
   return TLFEA_OK;
 }
 
@@ -769,6 +814,9 @@ static tlfea_status build_unit_meta(Context* c) {
   TL_TRY(c->alloc(&c->u_offT, (size_t)c->n_units));
   TL_TRY(c->alloc(&c->u_deg, (size_t)c->n_units));
   TL_TRY(c->alloc(&c->u_m, (size_t)c->n_units));
+  TL_TRY(c->alloc(&c->g4_ticket, 1));
+  TL_CUDA(cudaMemset(c->g4_ticket, 0, sizeof(unsigned long long)));
+  c->g4_base = 0;
   if (c->upper) {
     k_unit_meta_upper<<<grid_for(c->n_units, 256), 256>>>(c->n_units, c->unit_p, c->blk_row, c->rowptr_c, c->cols_c,
                                                           c->own_nodes, c->ubase, c->M, c->u_off, c->u_offT,
