@@ -495,11 +495,36 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
 //            (Eq. tangent_block) and f_a = sum_q F (w S grad N_a)
 //            (Eq. fint_local) from shared memory only; the second block pass
 //            re-reads instead of recomputing.
+// Per-lane inputs of a T10 warp group (node coordinates, class id), loaded
+// before the CTA stages its class tables so the two dependent global loads
+// (conn -> x) overlap the table copy instead of stalling the group start.
+struct T10Pre {
+  double xa[3];
+  int ce;
+  int32_t fd;  // force scratch position of (e, a)
+};
+__device__ __forceinline__ void t10_preload(int64_t grp, const ElArgs& A, T10Pre& p) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane / 10, a = lane % 10;
+  const int64_t e = grp * 3 + g;
+  p.xa[0] = p.xa[1] = p.xa[2] = 0.0;
+  p.ce = 0;
+  p.fd = 0;
+  if (lane < 30 && e < A.n_el) {
+    p.fd = A.fdest ? A.fdest[e * 10 + a] : (int32_t)(e * 10 + a);
+    const int64_t I = A.conn[e * 10 + a];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) p.xa[i] = A.x[3 * I + i];
+    if (a == 0) p.ce = A.cls[e];
+  }
+}
+
 #ifndef TLFEA_T10_2PH_NPASS
 #define TLFEA_T10_2PH_NPASS 3  // re-reading passes are cheap here: 3 x 2 blocks fit 128 registers without spills
 #endif
 template <int NQ>
-__device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab) {
+__device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab,
+                                                     const T10Pre& pre) {
   constexpr int NEN = 10, GROUP = 10, EPW = 3, NUB = 55, NB = 6, TABW = 3 * NEN + 1;
   constexpr int NPASS = TLFEA_T10_2PH_NPASS;
   constexpr int NBP = (NB + NPASS - 1) / NPASS;
@@ -529,17 +554,9 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
       if (t < lim) pf_cp4(&s_dst[wib][t], dest + e0 * NUB + t);
   }
   if (lane_active) {
-    double xa[3] = {0, 0, 0};
-    int ce = 0;
-    if (valid) {
-      const int64_t I = A.conn[e * NEN + a];
 #pragma unroll
-      for (int i = 0; i < 3; ++i) xa[i] = A.x[3 * I + i];
-      if (a == 0) ce = A.cls[e];
-    }
-#pragma unroll
-    for (int i = 0; i < 3; ++i) s_x[wib][g][3 * a + i] = xa[i];
-    if (a == 0) s_cls[wib][g] = ce;
+    for (int i = 0; i < 3; ++i) s_x[wib][g][3 * a + i] = pre.xa[i];
+    if (a == 0) s_cls[wib][g] = pre.ce;
   }
   __syncwarp();
   // ---- phase A: one lane per (element, q)
@@ -642,8 +659,7 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
       }
     }
     if (valid && pass == 0) {
-      const int64_t fp = A.fdest ? (int64_t)A.fdest[e * NEN + a] : e * NEN + a;
-      double* fo = A.fscr + fp * 3;
+      double* fo = A.fscr + (int64_t)pre.fd * 3;
       fo[0] = fa[0];
       fo[1] = fa[1];
       fo[2] = fa[2];
@@ -699,18 +715,31 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
 template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS>
 __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>()) k_element(ElArgs A) {
   extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
-  if (CLS) {
-    const int tot = A.n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1);
-    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_tab[t] = A.cls_tab[t];
-    __syncthreads();
-  }
+  constexpr bool T2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && TAN && CLS;
   // A.cta_tiles consecutive tiles per CTA (class tables staged once)
   const int64_t t0 = (int64_t)blockIdx.x * A.cta_tiles;
+  T10Pre pre;
+  if constexpr (T2PH) t10_preload(t0 * kWarps + (threadIdx.x >> 5), A, pre);
+  if (CLS) {
+    // all loads of a thread in flight at once (one L2 round trip, not one per element)
+    const int tot = A.n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1);
+    constexpr int U = 8;
+    for (int t = threadIdx.x; t < tot; t += U * blockDim.x) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = t + u * (int)blockDim.x < tot ? A.cls_tab[t + u * blockDim.x] : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (t + u * (int)blockDim.x < tot) s_tab[t + u * blockDim.x] = v[u];
+    }
+    __syncthreads();
+  }
 #pragma unroll 1
   for (int k = 0; k < A.cta_tiles; ++k) {
-    if constexpr (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && TAN && CLS)
-      element_group_t10svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
-    else
+    if constexpr (T2PH) {
+      if (k > 0) t10_preload((t0 + k) * kWarps + (threadIdx.x >> 5), A, pre);
+      element_group_t10svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
+    } else
       element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, TLFEA_DEST_ASYNC != 0>(
           (t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
   }
@@ -1459,9 +1488,11 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, 1>()) k_fuse
       if (!(P.dbg & 2)) {
 #pragma unroll 1
         for (int j = 0; j < P.etiles; ++j) {
-          if constexpr (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV)
-            element_group_t10svk<NQ>((t0 + j) * kWarps + wib, P.el, s_tab);
-          else
+          if constexpr (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV) {
+            T10Pre pre;
+            t10_preload((t0 + j) * kWarps + wib, P.el, pre);
+            element_group_t10svk<NQ>((t0 + j) * kWarps + wib, P.el, s_tab, pre);
+          } else
             element_group<ELEM, NQ, MODEL, KV, true, true, 1>((t0 + j) * kWarps + wib, P.el, s_tab);
         }
       }

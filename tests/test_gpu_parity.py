@@ -60,6 +60,14 @@ CASES = {
                                             dict(synth.SVK_PAPER, **synth.KV_TIRE), 0),
     "t10_single_element": lambda: (synth.Mesh(0, synth.kuhn_t10_box(1, 1, 1, 1, 1, 1).X,
                                               synth.kuhn_t10_box(1, 1, 1, 1, 1, 1).conn[:1]), dict(synth.MR_PAPER), 1),
+    # class-mode SVK (two-phase element group): a lone element and a tail that
+    # ends inside a warp group (100 = 3 * 33 + 1) and inside a CTA tile
+    "t10_single_element_svk": lambda: (synth.Mesh(0, synth.kuhn_t10_box(1, 1, 1, 1, 1, 1).X,
+                                                  synth.kuhn_t10_box(1, 1, 1, 1, 1, 1).conn[:1]),
+                                       dict(synth.SVK_PAPER), 1),
+    "t10_100el_svk_keast5_ragged": lambda: (synth.Mesh(0, synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).X,
+                                                       synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).conn[:100]),
+                                            dict(synth.SVK_PAPER), 1),
     "t10_4x3x2_perturbed_svk_kv_keast5": lambda: (synth.perturbed(synth.kuhn_t10_box(4, 3, 2, 0.8, 0.6, 0.4)),
                                                   dict(synth.SVK_PAPER, **synth.KV_TIRE), 1),
     "t10_3x3x2_perturbed_mr_4pt": lambda: (synth.perturbed(synth.kuhn_t10_box(3, 3, 2, 0.6, 0.6, 0.4)),
