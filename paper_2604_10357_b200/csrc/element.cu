@@ -1122,7 +1122,6 @@ struct GatherArgs {
   double h;
   double* H;
   int upper;  // UPPER H storage (u_deg = L | diagonal << 16, no transposed copy)
-  int sortT;  // transposed writes in address order across the warp (TLFEA_G3SORT)
   int dbg_gt; // diagnostics (TLFEA_DBG_GT=1, timing only, corrupts the scratch): transposes to contiguous scratch
 };
 
@@ -1187,7 +1186,7 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
     __syncwarp();
   }
   W.wk = wk0 + nwin;
-  if (!valid && !(A.sortT && !A.upper)) return;
+  if (!valid) return;
   const double mh = m / h;
   if (A.upper) {
     // UPPER storage (common.cuh): entry (d, f) at off + f + d (2 + 3 L) - d (d-1)/2,
@@ -1204,52 +1203,16 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
   }
   const int deg = dg & 0xffff, degT = dg >> 16;
   double* out = H + off;
-  if (valid) {
 #pragma unroll
-    for (int d = 0; d < 3; ++d)
+  for (int d = 0; d < 3; ++d)
 #pragma unroll
-      for (int f = 0; f < 3; ++f) h_store(out + 3 * d * deg + f, fma(h, acc[3 * d + f], d == f ? mh : 0.0));
-  }
+    for (int f = 0; f < 3; ++f) h_store(out + 3 * d * deg + f, fma(h, acc[3 * d + f], d == f ? mh : 0.0));
   if (A.dbg_gt) {
     double* o2 = const_cast<double*>(Kscr) + P0 * 9 + lane;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
       for (int f = 0; f < 3; ++f) o2[32 * (3 * d + f)] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
-    return;
-  }
-  if (A.sortT) {
-    // Transposed blocks (J,I) of the group's units lie in many rows J; sorted
-    // by H offset across the warp (bitonic network over (offT, lane)), lanes
-    // holding adjacent pieces of one row J write them in the same instruction.
-    double* st = W.buf[0];  // both windows are consumed: reuse as [32][9] staging
-#pragma unroll
-    for (int r = 0; r < 9; ++r) st[r * 32 + lane] = acc[r];
-    uint32_t key = valid ? (uint32_t)offT : 0xffffffffu;
-    int src = lane;
-#pragma unroll
-    for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        const uint32_t ok = __shfl_xor_sync(0xffffffffu, key, j);
-        const int os = __shfl_xor_sync(0xffffffffu, src, j);
-        const bool up = (lane & k) == 0, lower = (lane & j) == 0;
-        const bool less = ok < key || (ok == key && os < src);
-        if (lower == up ? less : !less) {
-          key = ok;
-          src = os;
-        }
-      }
-    const int dT = __shfl_sync(0xffffffffu, dg, src) >> 16;
-    const double mT = __shfl_sync(0xffffffffu, m, src) / h;
-    __syncwarp();
-    if (key != 0xffffffffu) {
-      double* o2 = H + (int32_t)key;
-#pragma unroll
-      for (int d = 0; d < 3; ++d)
-#pragma unroll
-        for (int f = 0; f < 3; ++f) h_store(o2 + 3 * d * dT + f, fma(h, st[(3 * f + d) * 32 + src], d == f ? mT : 0.0));
-    }
     return;
   }
   if (offT >= 0) {
@@ -1674,12 +1637,6 @@ static GatherArgs gather_args(const Context* c, double h, double* H) {
       dbg = e ? atoi(e) : 0;
     }
     A.dbg_gt = dbg;
-    static int srt = -1;
-    if (srt < 0) {
-      const char* e = getenv("TLFEA_G3SORT");
-      srt = e ? atoi(e) : 0;
-    }
-    A.sortT = srt;
   }
   return A;
 }
