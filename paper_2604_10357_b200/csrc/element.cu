@@ -708,14 +708,92 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
   }
 }
 
+// Force-only counterpart (tlfea_force_only, the AdamW inner evaluation): phase A,
+// one lane per (element, q), forms w P = w F S (Eq. F_assembly, reading Q5, J0 w
+// folded in) once; phase B, one lane per (element, node a), contracts
+// f_a = sum_q (w P) grad N_a (Eq. fint_local). The lane-per-node kernel reduced
+// F and evaluated S on all 10 lanes of an element at every q.
+template <int NQ>
+__device__ __forceinline__ void element_group_t10svk_force(int64_t grp, const ElArgs& A,
+                                                           const double* __restrict__ s_tab, const T10Pre& pre) {
+  constexpr int NEN = 10, GROUP = 10, EPW = 3, TABW = 3 * NEN + 1;
+  __shared__ double s_x[kWarps][EPW][3 * NEN];
+  __shared__ double s_pw[kWarps][EPW][NQ][9];
+  __shared__ int32_t s_cls[kWarps][EPW];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const bool lane_active = lane < EPW * GROUP;
+  const int g = lane_active ? lane / GROUP : 0;
+  const int a = lane_active ? lane % GROUP : 0;
+  const int64_t e = grp * EPW + g;
+  const bool valid = lane_active && e < A.n_el;
+  if (lane_active) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s_x[wib][g][3 * a + i] = pre.xa[i];
+    if (a == 0) s_cls[wib][g] = pre.ce;
+  }
+  __syncwarp();
+  if (lane < EPW * NQ) {
+    const int ge = lane / NQ, q = lane - NQ * (lane / NQ);
+    const double* t = s_tab + (s_cls[wib][ge] * NQ + q) * TABW;
+    const double* xs = s_x[wib][ge];
+    double F[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) F[r] = 0.0;
+#pragma unroll
+    for (int b = 0; b < NEN; ++b) {
+      const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double xi = xs[3 * b + i];
+        F[3 * i] = fma(xi, n0, F[3 * i]);
+        F[3 * i + 1] = fma(xi, n1, F[3 * i + 1]);
+        F[3 * i + 2] = fma(xi, n2, F[3 * i + 2]);
+      }
+    }
+    double S[6];
+    svk_S(F, A.mat.lam, A.mat.mu, S);
+    const double w = t[3 * NEN];
+    double* pw = s_pw[wib][ge][q];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int J = 0; J < 3; ++J)
+        pw[3 * i + J] = w * (F[3 * i] * sget(S, 0, J) + F[3 * i + 1] * sget(S, 1, J) + F[3 * i + 2] * sget(S, 2, J));
+  }
+  __syncwarp();
+  if (!valid) return;
+  const int ce = s_cls[wib][g];
+  double fa[3] = {0, 0, 0};
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const double* t = s_tab + (ce * NQ + q) * TABW + 3 * a;
+    const double* pw = s_pw[wib][g][q];
+    const double n0 = t[0], n1 = t[1], n2 = t[2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) fa[i] = fma(pw[3 * i], n0, fma(pw[3 * i + 1], n1, fma(pw[3 * i + 2], n2, fa[i])));
+  }
+  double* fo = A.fscr + (int64_t)pre.fd * 3;
+  fo[0] = fa[0];
+  fo[1] = fa[1];
+  fo[2] = fa[2];
+}
+
 #ifndef TLFEA_T10_2PH
 #define TLFEA_T10_2PH 1  // T10 SVK class-mode tangent eval through element_group_t10svk
 #endif
 
+#ifndef TLFEA_T10_FMINB
+#define TLFEA_T10_FMINB 6  // T10 SVK force-only (two-phase) CTAs per SM: 80 registers, no spills (config 5: 0.674 ms vs 0.784 at 4, 0.676 at 8)
+#endif
+template <int ELEM, int MODEL, int NPASS, bool KV, bool TAN>
+__host__ __device__ constexpr int el_minb_k() {
+  return (ELEM == 0 && MODEL == 0 && !KV && !TAN) ? TLFEA_T10_FMINB : el_minb<ELEM, MODEL, NPASS>();
+}
+
 template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS>
-__global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>()) k_element(ElArgs A) {
+__global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV, TAN>()) k_element(ElArgs A) {
   extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
-  constexpr bool T2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && TAN && CLS;
+  constexpr bool T2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && CLS;  // tangent or force only
   // A.cta_tiles consecutive tiles per CTA (class tables staged once)
   const int64_t t0 = (int64_t)blockIdx.x * A.cta_tiles;
   T10Pre pre;
@@ -738,7 +816,10 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, NPASS>()) k_
   for (int k = 0; k < A.cta_tiles; ++k) {
     if constexpr (T2PH) {
       if (k > 0) t10_preload((t0 + k) * kWarps + (threadIdx.x >> 5), A, pre);
-      element_group_t10svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
+      if constexpr (TAN)
+        element_group_t10svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
+      else
+        element_group_t10svk_force<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
     } else
       element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, TLFEA_DEST_ASYNC != 0>(
           (t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
