@@ -559,16 +559,23 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
     if (a == 0) s_cls[wib][g] = pre.ce;
   }
   __syncwarp();
-  // ---- phase A: one lane per (element, q)
-  if (lane < EPW * NQ) {
-    const int ge = lane / NQ, q = lane - NQ * (lane / NQ);
+  // ---- phase A: two lanes per (element, q), each owning 5 of the 10 nodes
+  // (EPW * NQ * 2 = 30 lanes for Keast-5): partial F over its nodes, the halves
+  // exchanged by one shuffle; lane h = 0 then stores F and S, lane h = 1 F F^T,
+  // and each lane writes g_b = F grad N_b for its own nodes.
+  static_assert(EPW * NQ * 2 <= 32, "phase A: two lanes per (element, q)");
+  {
+    const bool act = lane < EPW * NQ * 2;
+    const int pr = act ? lane >> 1 : 0, hf = lane & 1;
+    const int ge = pr / NQ, q = pr - NQ * (pr / NQ);
     const double* t = s_tab + (s_cls[wib][ge] * NQ + q) * TABW;
     const double* xs = s_x[wib][ge];
     double F[9];
 #pragma unroll
     for (int r = 0; r < 9; ++r) F[r] = 0.0;
-#pragma unroll kAUnroll
-    for (int b = 0; b < NEN; ++b) {
+#pragma unroll
+    for (int bb = 0; bb < NEN / 2; ++bb) {
+      const int b = hf * (NEN / 2) + bb;
       const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
@@ -578,24 +585,37 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
         F[3 * i + 2] = fma(xi, n2, F[3 * i + 2]);
       }
     }
-    double S[6];
-    svk_S(F, mat.lam, mat.mu, S);
-    double* kq = s_k[wib][ge][q];
+    // F = (nodes 0-4) + (nodes 5-9), the same order on both lanes
 #pragma unroll
-    for (int r = 0; r < 9; ++r) kq[r] = F[r];
-#pragma unroll
-    for (int r = 0; r < 6; ++r) kq[9 + r] = S[r];
-#pragma unroll
-    for (int vv = 0; vv < 6; ++vv) {
-      int i, k;
-      voigt_pair(vv, i, k);
-      kq[15 + vv] = F[3 * i] * F[3 * k] + F[3 * i + 1] * F[3 * k + 1] + F[3 * i + 2] * F[3 * k + 2];
+    for (int r = 0; r < 9; ++r) {
+      const double o = __shfl_xor_sync(0xffffffffu, F[r], 1);
+      F[r] = hf ? o + F[r] : F[r] + o;
     }
-#pragma unroll kAUnroll
-    for (int b = 0; b < NEN; ++b) {
-      const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+    if (act) {
+      double* kq = s_k[wib][ge][q];
+      if (hf == 0) {
+        double S[6];
+        svk_S(F, mat.lam, mat.mu, S);
 #pragma unroll
-      for (int i = 0; i < 3; ++i) s_ga[wib][q][i][ge * GROUP + b] = F[3 * i] * n0 + F[3 * i + 1] * n1 + F[3 * i + 2] * n2;
+        for (int r = 0; r < 9; ++r) kq[r] = F[r];
+#pragma unroll
+        for (int r = 0; r < 6; ++r) kq[9 + r] = S[r];
+      } else {
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv) {
+          int i, k;
+          voigt_pair(vv, i, k);
+          kq[15 + vv] = F[3 * i] * F[3 * k] + F[3 * i + 1] * F[3 * k + 1] + F[3 * i + 2] * F[3 * k + 2];
+        }
+      }
+#pragma unroll
+      for (int bb = 0; bb < NEN / 2; ++bb) {
+        const int b = hf * (NEN / 2) + bb;
+        const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          s_ga[wib][q][i][ge * GROUP + b] = F[3 * i] * n0 + F[3 * i + 1] * n1 + F[3 * i + 2] * n2;
+      }
     }
   }
   __syncwarp();
