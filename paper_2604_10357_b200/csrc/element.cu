@@ -798,6 +798,206 @@ __device__ __forceinline__ void element_group_t10svk_force(int64_t grp, const El
   fo[2] = fa[2];
 }
 
+// ANCF3443 plate element (16 coefficients, GL 4x4x3 = 48 points), SVK, no KV,
+// geometry classes: the two-phase scheme of element_group_t10svk with one
+// element per warp and the quadrature points in chunks of QC = 8.
+//   phase A (per chunk): lanes (q, s), four per point, each owning 4 of the 16
+//            coefficients: partial F, two shuffles, then S (s = 0) or F F^T
+//            (s = 1) and g_b = F grad N_b of its coefficients into shared memory;
+//   phase B (per chunk): lanes (node a, half) accumulate their 4-5 upper blocks
+//            over the chunk's points (and f_a on half 0) from shared memory.
+// The lane-per-node kernel evaluated the per-point kinematics on all 32 lanes
+// (fp64 pipe 62 % busy on config 4, ~40 % of it kinematics).
+template <int NQ>
+__device__ __forceinline__ void element_group_ancf_svk(int64_t e, const ElArgs& A, const double* __restrict__ s_tab) {
+  constexpr int NEN = 16, NUB = 136, NB = 5, TABW = 3 * NEN + 1, QC = 8, LPQ = 4, NPL = NEN / LPQ, LDG = NEN + 1;
+  static_assert(NQ % QC == 0 && QC * LPQ == 32, "quadrature points in whole chunks, one lane group per point");
+  __shared__ double s_ga[kWarps][QC][3][LDG];
+  __shared__ double s_k[kWarps][QC][21];  // F (9), S (6), F F^T (6)
+  __shared__ double s_x[kWarps][3 * NEN];
+  __shared__ double s_part[kWarps][9][kLD];
+  __shared__ int32_t s_dst[kWarps][NUB];
+  __shared__ int32_t s_pos[kWarps][32];
+  const int64_t n_el = A.n_el;
+  const MatDev& mat = A.mat;
+  const int32_t* __restrict__ dest = A.dest;
+  double* __restrict__ Kscr = A.Kscr;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int a = lane & 15, half = lane >> 4;
+  const bool valid = e < n_el;
+  if (!valid) return;  // warp-uniform (one element per warp)
+  const bool write = dest && !mat.dbg_nowrite;
+  if (write) {
+    for (int t = lane; t < NUB; t += 32) pf_cp4(&s_dst[wib][t], dest + e * NUB + t);
+  }
+  const int ce = A.cls[e];
+  if (half == 0) {
+    const int64_t I = A.conn[e * NEN + a];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s_x[wib][3 * a + i] = A.x[3 * I + i];
+  }
+  const int32_t fd = (half == 0) ? (A.fdest ? A.fdest[e * NEN + a] : (int32_t)(e * NEN + a)) : 0;
+  __syncwarp();
+  double fa[3] = {0, 0, 0};
+  double K[NB][9];
+#pragma unroll
+  for (int j = 0; j < NB; ++j)
+#pragma unroll
+    for (int r = 0; r < 9; ++r) K[j][r] = 0.0;
+#pragma unroll 1
+  for (int q0 = 0; q0 < NQ; q0 += QC) {
+    // ---- phase A: LPQ = 4 lanes per point, NPL = 4 coefficients each
+    {
+      const int qq = lane / LPQ, sub = lane % LPQ;
+      const double* t = s_tab + (ce * NQ + q0 + qq) * TABW;
+      double F[9];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) F[r] = 0.0;
+#pragma unroll
+      for (int bb = 0; bb < NPL; ++bb) {
+        const int b = sub * NPL + bb;
+        const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const double xi = s_x[wib][3 * b + i];
+          F[3 * i] = fma(xi, n0, F[3 * i]);
+          F[3 * i + 1] = fma(xi, n1, F[3 * i + 1]);
+          F[3 * i + 2] = fma(xi, n2, F[3 * i + 2]);
+        }
+      }
+      // F = (p0 + p1) + (p2 + p3), the same bits on all four lanes
+#pragma unroll
+      for (int m = 1; m < LPQ; m <<= 1)
+#pragma unroll
+        for (int r = 0; r < 9; ++r) {
+          const double o = __shfl_xor_sync(0xffffffffu, F[r], m);
+          F[r] = (sub & m) ? o + F[r] : F[r] + o;
+        }
+      double* kq = s_k[wib][qq];
+      if (sub == 0) {
+        double S[6];
+        svk_S(F, mat.lam, mat.mu, S);
+#pragma unroll
+        for (int r = 0; r < 9; ++r) kq[r] = F[r];
+#pragma unroll
+        for (int r = 0; r < 6; ++r) kq[9 + r] = S[r];
+      } else if (sub == 1) {
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv) {
+          int i, k;
+          voigt_pair(vv, i, k);
+          kq[15 + vv] = F[3 * i] * F[3 * k] + F[3 * i + 1] * F[3 * k + 1] + F[3 * i + 2] * F[3 * k + 2];
+        }
+      }
+#pragma unroll
+      for (int bb = 0; bb < NPL; ++bb) {
+        const int b = sub * NPL + bb;
+        const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) s_ga[wib][qq][i][b] = F[3 * i] * n0 + F[3 * i + 1] * n1 + F[3 * i + 2] * n2;
+      }
+    }
+    __syncwarp();
+    // ---- phase B
+#pragma unroll 1
+    for (int qq = 0; qq < QC; ++qq) {
+      const double* t = s_tab + (ce * NQ + q0 + qq) * TABW;
+      const double* kq = s_k[wib][qq];
+      const double gN[3] = {t[3 * a], t[3 * a + 1], t[3 * a + 2]};
+      const double w = t[3 * NEN];
+      double S[6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) S[r] = kq[9 + r];
+      double tw[3];
+#pragma unroll
+      for (int I = 0; I < 3; ++I) tw[I] = w * (sget(S, I, 0) * gN[0] + sget(S, I, 1) * gN[1] + sget(S, I, 2) * gN[2]);
+      if (half == 0) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          fa[i] = fma(kq[3 * i], tw[0], fma(kq[3 * i + 1], tw[1], fma(kq[3 * i + 2], tw[2], fa[i])));
+      }
+      const double lw = mat.lam * w, mw = mat.mu * w;
+      double gl[3], gm[3], gNm[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double gai = s_ga[wib][qq][i][a];
+        gl[i] = lw * gai;
+        gm[i] = mw * gai;
+        gNm[i] = mw * gN[i];
+      }
+      double B[6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) B[r] = kq[15 + r];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int b = partner<1>(a, half, j);
+        if (b < 0) continue;
+        double* Kj = K[j];
+        const double gb[3] = {s_ga[wib][qq][0][b], s_ga[wib][qq][1][b], s_ga[wib][qq][2][b]};
+        const double nb[3] = {t[3 * b], t[3 * b + 1], t[3 * b + 2]};
+        const double sv = fma(tw[0], nb[0], fma(tw[1], nb[1], tw[2] * nb[2]));
+        const double d = fma(gNm[0], nb[0], fma(gNm[1], nb[1], gNm[2] * nb[2]));
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            double acc = fma(gl[i], gb[k], fma(gb[i], gm[k], fma(d, B[vidx(i, k)], Kj[3 * i + k])));
+            Kj[3 * i + k] = (i == k) ? acc + sv : acc;
+          }
+      }
+    }
+    __syncwarp();
+  }
+  if (half == 0) {
+    double* fo = A.fscr + (int64_t)fd * 3;
+    fo[0] = fa[0];
+    fo[1] = fa[1];
+    fo[2] = fa[2];
+  }
+  if (mat.dbg_nowrite) return;
+  // warp-staged block stores, as in element_group
+  constexpr int NLB = 32, NIT = (NLB + 2) / 3;
+  const int bi = lane / 9, rr = lane - 9 * (lane / 9);
+  if (write) {
+    pf_wait();
+    __syncwarp();
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const int b = partner<1>(a, half, j);
+    int32_t pos = -1;
+    if (b >= 0) {
+      const double* Kj = K[j];
+      const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
+      bool tr = a > b;
+      pos = (int32_t)(e * NUB + ub);
+      if (dest) {
+        const int32_t dd = s_dst[wib][ub];
+        pos = dd >> 1;
+        tr = tr != ((dd & 1) != 0);
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) s_part[wib][tr ? 3 * k + i : 3 * i + k][lane] = Kj[3 * i + k];
+    }
+    s_pos[wib][lane] = pos;
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int blk = 3 * it + bi;
+      if (lane < 27 && blk < NLB) {
+        const int32_t p = s_pos[wib][blk];
+        if (p >= 0) k_store(Kscr + (int64_t)p * 9 + rr, s_part[wib][rr][blk]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+#ifndef TLFEA_ANCF_2PH
+#define TLFEA_ANCF_2PH 1  // ANCF3443 SVK class-mode tangent eval through element_group_ancf_svk
+#endif
 #ifndef TLFEA_T10_2PH
 #define TLFEA_T10_2PH 1  // T10 SVK class-mode tangent eval through element_group_t10svk
 #endif
@@ -814,6 +1014,7 @@ template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS>
 __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV, TAN>()) k_element(ElArgs A) {
   extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
   constexpr bool T2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && CLS;  // tangent or force only
+  constexpr bool A2PH = TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV && TAN && CLS;
   // A.cta_tiles consecutive tiles per CTA (class tables staged once)
   const int64_t t0 = (int64_t)blockIdx.x * A.cta_tiles;
   T10Pre pre;
@@ -840,6 +1041,8 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
         element_group_t10svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
       else
         element_group_t10svk_force<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
+    } else if constexpr (A2PH) {
+      element_group_ancf_svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
     } else
       element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, TLFEA_DEST_ASYNC != 0>(
           (t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
@@ -1556,6 +1759,8 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, 1>()) k_fuse
             T10Pre pre;
             t10_preload((t0 + j) * kWarps + wib, P.el, pre);
             element_group_t10svk<NQ>((t0 + j) * kWarps + wib, P.el, s_tab, pre);
+          } else if constexpr (TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV) {
+            element_group_ancf_svk<NQ>((t0 + j) * kWarps + wib, P.el, s_tab);
           } else
             element_group<ELEM, NQ, MODEL, KV, true, true, 1>((t0 + j) * kWarps + wib, P.el, s_tab);
         }

@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
-VAR=X VALS="0 1" bash tools/ab_env.sh
+P=paper_2604_10357_b200
+CFG=4 LIBS="$P/libtlfea.so $P/libtlfea_old.so" TILES=1 bash tools/ab.sh
