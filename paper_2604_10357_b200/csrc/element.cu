@@ -82,7 +82,7 @@ __device__ __forceinline__ int partner(int a, int half, int j) {
 // spills — measured faster (config 3: 11.2 vs 11.4-12.8 ms). Mooney-Rivlin
 // and ANCF measured slower with two passes (their per-q work is larger).
 #ifndef TLFEA_2PH_QUNROLL
-#define TLFEA_2PH_QUNROLL 2  // phase-B quadrature loop (config 3: 2 -> 10.72 ms, 1 -> 11.0, 5 spills)
+#define TLFEA_2PH_QUNROLL 1  // phase-B quadrature loop (config 3, 2 passes / 3 CTAs: 1 -> 9.96 ms, 2 -> 10.02)
 #endif
 constexpr int kQUnroll = TLFEA_2PH_QUNROLL;
 #ifndef TLFEA_2PH_AUNROLL
@@ -520,7 +520,10 @@ __device__ __forceinline__ void t10_preload(int64_t grp, const ElArgs& A, T10Pre
 }
 
 #ifndef TLFEA_T10_2PH_NPASS
-#define TLFEA_T10_2PH_NPASS 3  // re-reading passes are cheap here: 3 x 2 blocks fit 128 registers without spills
+#define TLFEA_T10_2PH_NPASS 2  // config 3: 2 passes at 3 CTAs/SM (166 registers) 9.96 ms; 3 passes at 4 CTAs 10.72; 1 pass 12.97
+#endif
+#ifndef TLFEA_T10_2PH_MINB
+#define TLFEA_T10_2PH_MINB 3
 #endif
 template <int NQ>
 __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab,
@@ -798,6 +801,12 @@ __device__ __forceinline__ void element_group_t10svk_force(int64_t grp, const El
   fo[2] = fa[2];
 }
 
+#ifndef TLFEA_ANCF_NPASS
+#define TLFEA_ANCF_NPASS 1  // block passes (each re-runs phase A per chunk)
+#endif
+#ifndef TLFEA_ANCF_MINB
+#define TLFEA_ANCF_MINB 2
+#endif
 // ANCF3443 plate element (16 coefficients, GL 4x4x3 = 48 points), SVK, no KV,
 // geometry classes: the two-phase scheme of element_group_t10svk with one
 // element per warp and the quadrature points in chunks of QC = 8.
@@ -838,10 +847,17 @@ __device__ __forceinline__ void element_group_ancf_svk(int64_t e, const ElArgs& 
   }
   const int32_t fd = (half == 0) ? (A.fdest ? A.fdest[e * NEN + a] : (int32_t)(e * NEN + a)) : 0;
   __syncwarp();
+  constexpr int NPASS = TLFEA_ANCF_NPASS, NBP = (NB + NPASS - 1) / NPASS;
   double fa[3] = {0, 0, 0};
-  double K[NB][9];
+  double K[NBP][9];
+  if (write) {
+    pf_wait();
+    __syncwarp();
+  }
+#pragma unroll 1
+  for (int pass = 0; pass < NPASS; ++pass) {
 #pragma unroll
-  for (int j = 0; j < NB; ++j)
+  for (int j = 0; j < NBP; ++j)
 #pragma unroll
     for (int r = 0; r < 9; ++r) K[j][r] = 0.0;
 #pragma unroll 1
@@ -911,7 +927,7 @@ __device__ __forceinline__ void element_group_ancf_svk(int64_t e, const ElArgs& 
       double tw[3];
 #pragma unroll
       for (int I = 0; I < 3; ++I) tw[I] = w * (sget(S, I, 0) * gN[0] + sget(S, I, 1) * gN[1] + sget(S, I, 2) * gN[2]);
-      if (half == 0) {
+      if (half == 0 && pass == 0) {
 #pragma unroll
         for (int i = 0; i < 3; ++i)
           fa[i] = fma(kq[3 * i], tw[0], fma(kq[3 * i + 1], tw[1], fma(kq[3 * i + 2], tw[2], fa[i])));
@@ -929,10 +945,11 @@ __device__ __forceinline__ void element_group_ancf_svk(int64_t e, const ElArgs& 
 #pragma unroll
       for (int r = 0; r < 6; ++r) B[r] = kq[15 + r];
 #pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        const int b = partner<1>(a, half, j);
+      for (int jj = 0; jj < NBP; ++jj) {
+        const int j = pass * NBP + jj;
+        const int b = j < NB ? partner<1>(a, half, j) : -1;
         if (b < 0) continue;
-        double* Kj = K[j];
+        double* Kj = K[jj];
         const double gb[3] = {s_ga[wib][qq][0][b], s_ga[wib][qq][1][b], s_ga[wib][qq][2][b]};
         const double nb[3] = {t[3 * b], t[3 * b + 1], t[3 * b + 2]};
         const double sv = fma(tw[0], nb[0], fma(tw[1], nb[1], tw[2] * nb[2]));
@@ -948,26 +965,23 @@ __device__ __forceinline__ void element_group_ancf_svk(int64_t e, const ElArgs& 
     }
     __syncwarp();
   }
-  if (half == 0) {
+  if (half == 0 && pass == 0) {
     double* fo = A.fscr + (int64_t)fd * 3;
     fo[0] = fa[0];
     fo[1] = fa[1];
     fo[2] = fa[2];
   }
-  if (mat.dbg_nowrite) return;
+  if (mat.dbg_nowrite) continue;
   // warp-staged block stores, as in element_group
   constexpr int NLB = 32, NIT = (NLB + 2) / 3;
   const int bi = lane / 9, rr = lane - 9 * (lane / 9);
-  if (write) {
-    pf_wait();
-    __syncwarp();
-  }
 #pragma unroll
-  for (int j = 0; j < NB; ++j) {
-    const int b = partner<1>(a, half, j);
+  for (int jj = 0; jj < NBP; ++jj) {
+    const int j = pass * NBP + jj;
+    const int b = j < NB ? partner<1>(a, half, j) : -1;
     int32_t pos = -1;
     if (b >= 0) {
-      const double* Kj = K[j];
+      const double* Kj = K[jj];
       const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
       bool tr = a > b;
       pos = (int32_t)(e * NUB + ub);
@@ -993,6 +1007,7 @@ __device__ __forceinline__ void element_group_ancf_svk(int64_t e, const ElArgs& 
     }
     __syncwarp();
   }
+  }  // pass
 }
 
 #ifndef TLFEA_ANCF_2PH
@@ -1005,13 +1020,16 @@ __device__ __forceinline__ void element_group_ancf_svk(int64_t e, const ElArgs& 
 #ifndef TLFEA_T10_FMINB
 #define TLFEA_T10_FMINB 6  // T10 SVK force-only (two-phase) CTAs per SM: 80 registers, no spills (config 5: 0.674 ms vs 0.784 at 4, 0.676 at 8)
 #endif
-template <int ELEM, int MODEL, int NPASS, bool KV, bool TAN>
+template <int ELEM, int MODEL, int NPASS, bool KV, bool TAN, bool CLS>
 __host__ __device__ constexpr int el_minb_k() {
-  return (ELEM == 0 && MODEL == 0 && !KV && !TAN) ? TLFEA_T10_FMINB : el_minb<ELEM, MODEL, NPASS>();
+  return (ELEM == 0 && MODEL == 0 && !KV && !TAN)                         ? TLFEA_T10_FMINB
+         : (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && TAN && CLS)  ? TLFEA_T10_2PH_MINB
+         : (TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV && TAN && CLS) ? TLFEA_ANCF_MINB
+                                                                            : el_minb<ELEM, MODEL, NPASS>();
 }
 
 template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS>
-__global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV, TAN>()) k_element(ElArgs A) {
+__global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV, TAN, CLS>()) k_element(ElArgs A) {
   extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
   constexpr bool T2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && CLS;  // tangent or force only
   constexpr bool A2PH = TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV && TAN && CLS;

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
-P=paper_2604_10357_b200
-CFG=4 LIBS="$P/libtlfea.so $P/libtlfea_old.so" TILES=1 bash tools/ab.sh
+for c in 3 5 4; do CFG=$c VAR=X VALS=0 bash tools/ab_env.sh; done
