@@ -2072,7 +2072,13 @@ tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
       c->g4_base += (unsigned long long)n_groups + (unsigned long long)grid * kG3Warps;
       return TLFEA_OK;
     }
-    k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(gather_args(c, h, H));
+    static int pad = -1;  // diagnostics: dynamic shared memory that caps the resident CTAs per SM
+    if (pad < 0) {
+      const char* e = getenv("TLFEA_G3_SMEM_PAD");
+      pad = e ? atoi(e) : 0;
+      if (pad > 0) TL_CUDA(cudaFuncSetAttribute(k_gather_units_v3, cudaFuncAttributeMaxDynamicSharedMemorySize, pad));
+    }
+    k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, pad, s>>>(gather_args(c, h, H));
     TL_CHECK_LAUNCH();
     return TLFEA_OK;
   }

@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
-for c in 3 5 4; do CFG=$c VAR=X VALS=0 bash tools/ab_env.sh; done
+VAR=TLFEA_G3_SMEM_PAD VALS="0 8000 20000 38000" bash tools/ab_env.sh
