@@ -1010,6 +1010,211 @@ __device__ __forceinline__ void element_group_ancf_svk(int64_t e, const ElArgs& 
   }  // pass
 }
 
+// ANCF3243 beam (8 coefficients, GL 3x2x2 = 12 points), SVK, no KV, geometry
+// classes: the two-phase scheme with 4 elements per warp and the points in
+// chunks of QC = 4: phase A on lanes (element, point, half) — two lanes per
+// (element, point), 4 coefficients each — then phase B on lanes (element,
+// node a) over the chunk's points. One block pass (4-5 blocks per lane).
+template <int NQ>
+__device__ __forceinline__ void element_group_beam_svk(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab) {
+  constexpr int NEN = 8, GROUP = 8, EPW = 4, NUB = 36, NB = 5, TABW = 3 * NEN + 1, QC = 4;
+  static_assert(NQ % QC == 0 && EPW * QC * 2 == 32, "one lane pair per (element, point) of a chunk");
+  __shared__ double s_ga[kWarps][QC][3][kLD];
+  __shared__ double s_k[kWarps][EPW][QC][21];
+  __shared__ double s_x[kWarps][EPW][3 * NEN];
+  __shared__ double s_part[kWarps][9][kLD];
+  __shared__ int32_t s_dst[kWarps][EPW * NUB];
+  __shared__ int32_t s_pos[kWarps][32];
+  __shared__ int32_t s_cls[kWarps][EPW];
+  const int64_t n_el = A.n_el;
+  const MatDev& mat = A.mat;
+  const int32_t* __restrict__ dest = A.dest;
+  double* __restrict__ Kscr = A.Kscr;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int g = lane / GROUP, a = lane % GROUP, gbase = g * GROUP;
+  const int64_t e = grp * EPW + g;
+  const bool valid = e < n_el;
+  const bool write = dest && !mat.dbg_nowrite;
+  if (write) {
+    const int64_t e0 = grp * EPW, lim = (n_el - e0) * NUB;
+    for (int t = lane; t < EPW * NUB; t += 32)
+      if (t < lim) pf_cp4(&s_dst[wib][t], dest + e0 * NUB + t);
+  }
+  {
+    double xa[3] = {0, 0, 0};
+    int ce = 0;
+    if (valid) {
+      const int64_t I = A.conn[e * NEN + a];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) xa[i] = A.x[3 * I + i];
+      if (a == 0) ce = A.cls[e];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s_x[wib][g][3 * a + i] = xa[i];
+    if (a == 0) s_cls[wib][g] = ce;
+  }
+  const int32_t fd = valid ? (A.fdest ? A.fdest[e * NEN + a] : (int32_t)(e * NEN + a)) : 0;
+  __syncwarp();
+  const int ce = s_cls[wib][g];
+  double fa[3] = {0, 0, 0};
+  double K[NB][9];
+#pragma unroll
+  for (int j = 0; j < NB; ++j)
+#pragma unroll
+    for (int r = 0; r < 9; ++r) K[j][r] = 0.0;
+#pragma unroll 1
+  for (int q0 = 0; q0 < NQ; q0 += QC) {
+    {  // ---- phase A
+      const int pr = lane >> 1, hf = lane & 1;
+      const int ge = pr / QC, qq = pr - QC * (pr / QC);
+      const double* t = s_tab + (s_cls[wib][ge] * NQ + q0 + qq) * TABW;
+      const double* xs = s_x[wib][ge];
+      double F[9];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) F[r] = 0.0;
+#pragma unroll
+      for (int bb = 0; bb < NEN / 2; ++bb) {
+        const int b = hf * (NEN / 2) + bb;
+        const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const double xi = xs[3 * b + i];
+          F[3 * i] = fma(xi, n0, F[3 * i]);
+          F[3 * i + 1] = fma(xi, n1, F[3 * i + 1]);
+          F[3 * i + 2] = fma(xi, n2, F[3 * i + 2]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 9; ++r) {
+        const double o = __shfl_xor_sync(0xffffffffu, F[r], 1);
+        F[r] = hf ? o + F[r] : F[r] + o;
+      }
+      double* kq = s_k[wib][ge][qq];
+      if (hf == 0) {
+        double S[6];
+        svk_S(F, mat.lam, mat.mu, S);
+#pragma unroll
+        for (int r = 0; r < 9; ++r) kq[r] = F[r];
+#pragma unroll
+        for (int r = 0; r < 6; ++r) kq[9 + r] = S[r];
+      } else {
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv) {
+          int i, k;
+          voigt_pair(vv, i, k);
+          kq[15 + vv] = F[3 * i] * F[3 * k] + F[3 * i + 1] * F[3 * k + 1] + F[3 * i + 2] * F[3 * k + 2];
+        }
+      }
+#pragma unroll
+      for (int bb = 0; bb < NEN / 2; ++bb) {
+        const int b = hf * (NEN / 2) + bb;
+        const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          s_ga[wib][qq][i][ge * GROUP + b] = F[3 * i] * n0 + F[3 * i + 1] * n1 + F[3 * i + 2] * n2;
+      }
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int qq = 0; qq < QC; ++qq) {  // ---- phase B
+      const double* t = s_tab + (ce * NQ + q0 + qq) * TABW;
+      const double* kq = s_k[wib][g][qq];
+      const double gN[3] = {t[3 * a], t[3 * a + 1], t[3 * a + 2]};
+      const double w = t[3 * NEN];
+      double S[6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) S[r] = kq[9 + r];
+      double tw[3];
+#pragma unroll
+      for (int I = 0; I < 3; ++I) tw[I] = w * (sget(S, I, 0) * gN[0] + sget(S, I, 1) * gN[1] + sget(S, I, 2) * gN[2]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        fa[i] = fma(kq[3 * i], tw[0], fma(kq[3 * i + 1], tw[1], fma(kq[3 * i + 2], tw[2], fa[i])));
+      const double lw = mat.lam * w, mw = mat.mu * w;
+      double gl[3], gm[3], gNm[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double gai = s_ga[wib][qq][i][lane];
+        gl[i] = lw * gai;
+        gm[i] = mw * gai;
+        gNm[i] = mw * gN[i];
+      }
+      double B[6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) B[r] = kq[15 + r];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int b = partner<2>(a, 0, j);
+        if (b < 0) continue;
+        double* Kj = K[j];
+        const int lb = gbase + b;
+        const double gb[3] = {s_ga[wib][qq][0][lb], s_ga[wib][qq][1][lb], s_ga[wib][qq][2][lb]};
+        const double nb[3] = {t[3 * b], t[3 * b + 1], t[3 * b + 2]};
+        const double sv = fma(tw[0], nb[0], fma(tw[1], nb[1], tw[2] * nb[2]));
+        const double d = fma(gNm[0], nb[0], fma(gNm[1], nb[1], gNm[2] * nb[2]));
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            double acc = fma(gl[i], gb[k], fma(gb[i], gm[k], fma(d, B[vidx(i, k)], Kj[3 * i + k])));
+            Kj[3 * i + k] = (i == k) ? acc + sv : acc;
+          }
+      }
+    }
+    __syncwarp();
+  }
+  if (valid) {
+    double* fo = A.fscr + (int64_t)fd * 3;
+    fo[0] = fa[0];
+    fo[1] = fa[1];
+    fo[2] = fa[2];
+  }
+  if (mat.dbg_nowrite) return;
+  constexpr int NLB = 32, NIT = (NLB + 2) / 3;
+  const int bi = lane / 9, rr = lane - 9 * (lane / 9);
+  if (write) {
+    pf_wait();
+    __syncwarp();
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const int b = valid ? partner<2>(a, 0, j) : -1;
+    int32_t pos = -1;
+    if (b >= 0) {
+      const double* Kj = K[j];
+      const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
+      bool tr = a > b;
+      pos = (int32_t)(e * NUB + ub);
+      if (dest) {
+        const int32_t dd = s_dst[wib][g * NUB + ub];
+        pos = dd >> 1;
+        tr = tr != ((dd & 1) != 0);
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) s_part[wib][tr ? 3 * k + i : 3 * i + k][lane] = Kj[3 * i + k];
+    }
+    s_pos[wib][lane] = pos;
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int blk = 3 * it + bi;
+      if (lane < 27 && blk < NLB) {
+        const int32_t p = s_pos[wib][blk];
+        if (p >= 0) k_store(Kscr + (int64_t)p * 9 + rr, s_part[wib][rr][blk]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+#ifndef TLFEA_BEAM_2PH
+#define TLFEA_BEAM_2PH 1  // ANCF3243 SVK class-mode tangent eval through element_group_beam_svk
+#endif
+#ifndef TLFEA_BEAM_MINB
+#define TLFEA_BEAM_MINB 3  // config 6: 1.19 ms (168 registers, 20 B spill) vs 1.24 at 2 CTAs, 1.40 lane-per-node
+#endif
 #ifndef TLFEA_ANCF_2PH
 #define TLFEA_ANCF_2PH 1  // ANCF3443 SVK class-mode tangent eval through element_group_ancf_svk
 #endif
@@ -1025,6 +1230,7 @@ __host__ __device__ constexpr int el_minb_k() {
   return (ELEM == 0 && MODEL == 0 && !KV && !TAN)                         ? TLFEA_T10_FMINB
          : (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && TAN && CLS)  ? TLFEA_T10_2PH_MINB
          : (TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV && TAN && CLS) ? TLFEA_ANCF_MINB
+         : (TLFEA_BEAM_2PH && ELEM == 2 && MODEL == 0 && !KV && TAN && CLS) ? TLFEA_BEAM_MINB
                                                                             : el_minb<ELEM, MODEL, NPASS>();
 }
 
@@ -1033,6 +1239,7 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
   extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
   constexpr bool T2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && CLS;  // tangent or force only
   constexpr bool A2PH = TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV && TAN && CLS;
+  constexpr bool B2PH = TLFEA_BEAM_2PH && ELEM == 2 && MODEL == 0 && !KV && TAN && CLS;
   // A.cta_tiles consecutive tiles per CTA (class tables staged once)
   const int64_t t0 = (int64_t)blockIdx.x * A.cta_tiles;
   T10Pre pre;
@@ -1061,6 +1268,8 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
         element_group_t10svk_force<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
     } else if constexpr (A2PH) {
       element_group_ancf_svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
+    } else if constexpr (B2PH) {
+      element_group_beam_svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
     } else
       element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, TLFEA_DEST_ASYNC != 0>(
           (t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);

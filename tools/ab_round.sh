@@ -1,2 +1,4 @@
 mkdir -p gpurun_out
-VAR=TLFEA_G3_SMEM_PAD VALS="0 8000 20000 38000" bash tools/ab_env.sh
+timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
+P=paper_2604_10357_b200
+CFG=6 LIBS="$P/libtlfea.so $P/libtlfea_m3.so $P/libtlfea_old.so" TILES=1 bash tools/ab.sh
