@@ -146,6 +146,13 @@ struct Context {
   int32_t* u_off = nullptr;       // [n_units] H offset of block (I,J): 9 rowptr_c[i] + 3 k
   int32_t* u_offT = nullptr;      // [n_units] H offset of (J,I) or -1
   int32_t* u_deg = nullptr;       // [n_units] deg(I) | deg(J) << 16
+  // split FULL gather (opt-in TLFEA_GT_SPLIT=1 at setup): the H gather writes
+  // the upper blocks only; k_transpose_lower copies them to the lower blocks
+  // in destination order
+  int64_t tr_n = 0;
+  int32_t* tr_src = nullptr;      // [tr_n] H offset of (I,J), sorted by tr_dst
+  int32_t* tr_dst = nullptr;      // [tr_n] H offset of (J,I)
+  int32_t* tr_deg = nullptr;      // [tr_n] deg(I) | deg(J) << 16
   double* u_m = nullptr;          // [n_units] M_IJ
   // fused persistent eval (single rank, class tables, gather-sorted scratch):
   // one launch works through a list of element items (kElTile elements x

@@ -1653,6 +1653,7 @@ struct GatherArgs {
   double h;
   double* H;
   int upper;  // UPPER H storage (u_deg = L | diagonal << 16, no transposed copy)
+  int skipT;  // split FULL gather: upper blocks only (k_transpose_lower writes the rest)
   int dbg_gt; // diagnostics (TLFEA_DBG_GT=1, timing only, corrupts the scratch): transposes to contiguous scratch
 };
 
@@ -1746,13 +1747,33 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
       for (int f = 0; f < 3; ++f) o2[32 * (3 * d + f)] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
     return;
   }
-  if (offT >= 0) {
+  if (offT >= 0 && !A.skipT) {
     double* o2 = H + offT;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
       for (int f = 0; f < 3; ++f) h_store(o2 + 3 * d * degT + f, fma(h, acc[3 * f + d], d == f ? mh : 0.0));
   }
+}
+
+// Split FULL gather, second half: lower block (J,I) = upper block (I,J)^T,
+// one thread per transposed block in destination order (coalesced writes;
+// the reads of the upper blocks are the scattered side).
+__global__ void k_transpose_lower(int64_t n, const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                                  const int32_t* __restrict__ deg, double* __restrict__ H) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t s0 = src[k], d0 = dst[k], dg = deg[k];
+  const int dI = dg & 0xffff, dJ = dg >> 16;
+  double v[9];
+#pragma unroll
+  for (int f = 0; f < 3; ++f)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) v[3 * d + f] = H[s0 + 3 * f * dI + d];
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int f = 0; f < 3; ++f) H[d0 + 3 * d * dJ + f] = v[3 * d + f];
 }
 
 __device__ __forceinline__ void g3_init(double (*s_buf)[2][kG3Buf], uint64_t (*s_bar)[2], G3Warp& W) {
@@ -1836,7 +1857,7 @@ __device__ __forceinline__ void g4_write(const GatherArgs& A, const G4Meta& M, c
   for (int d = 0; d < 3; ++d)
 #pragma unroll
     for (int f = 0; f < 3; ++f) h_store(out + 3 * d * deg + f, fma(h, acc[3 * d + f], d == f ? mh : 0.0));
-  if (M.offT >= 0) {
+  if (M.offT >= 0 && !A.skipT) {
     double* o2 = H + M.offT;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -2163,6 +2184,7 @@ static GatherArgs gather_args(const Context* c, double h, double* H) {
   A.h = h;
   A.H = H;
   A.upper = c->upper;
+  A.skipT = c->tr_n > 0 ? 1 : 0;
   {
     static int dbg = -1;
     if (dbg < 0) {
@@ -2289,6 +2311,10 @@ tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
     }
     k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, pad, s>>>(gather_args(c, h, H));
     TL_CHECK_LAUNCH();
+    if (c->tr_n > 0) {
+      k_transpose_lower<<<gridn(c->tr_n, 256), 256, 0, s>>>(c->tr_n, c->tr_src, c->tr_dst, c->tr_deg, H);
+      TL_CHECK_LAUNCH();
+    }
     return TLFEA_OK;
   }
   k_gather_units<<<gridn(c->n_units, 256), 256, 0, s>>>(c->n_units, c->nen, n_ublk_of(c->nen), c->unit_p,

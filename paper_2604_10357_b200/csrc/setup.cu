@@ -808,6 +808,63 @@ static tlfea_status build_sorted_scratch(Context* c) {
   return TLFEA_OK;
 }
 
+__global__ void k_tr_keys(int64_t n, const int32_t* __restrict__ u_offT, uint32_t* __restrict__ key,
+                          int32_t* __restrict__ idx) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  key[u] = (uint32_t)u_offT[u];  // -1 (no transpose) sorts last
+  idx[u] = (int32_t)u;
+}
+__global__ void k_tr_fill(int64_t n, const int32_t* __restrict__ idx, const int32_t* __restrict__ u_off,
+                          const int32_t* __restrict__ u_offT, const int32_t* __restrict__ u_deg,
+                          int32_t* __restrict__ src, int32_t* __restrict__ dst, int32_t* __restrict__ deg) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t u = idx[k];
+  src[k] = u_off[u];
+  dst[k] = u_offT[u];
+  deg[k] = u_deg[u];
+}
+__global__ void k_tr_count(int64_t n, const int32_t* __restrict__ u_offT, unsigned long long* __restrict__ cnt) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u < n && u_offT[u] >= 0) atomicAdd(cnt, 1ull);  // setup only: an integer count
+}
+
+static tlfea_status build_transpose_list(Context* c) {
+  const int64_t n = c->n_units;
+  TmpArr<uint32_t> key, key2;
+  TmpArr<int32_t> idx, idx2;
+  TmpArr<unsigned long long> cnt;
+  TL_TRY(key.get(n));
+  TL_TRY(key2.get(n));
+  TL_TRY(idx.get(n));
+  TL_TRY(idx2.get(n));
+  TL_TRY(cnt.get(1));
+  TL_CUDA(cudaMemset(cnt.p, 0, sizeof(unsigned long long)));
+  k_tr_keys<<<grid_for(n, 256), 256>>>(n, c->u_offT, key.p, idx.p);
+  TL_CHECK_LAUNCH();
+  k_tr_count<<<grid_for(n, 256), 256>>>(n, c->u_offT, cnt.p);
+  TL_CHECK_LAUNCH();
+  Tmp tmp;
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, idx.p, idx2.p, n);
+  TL_TRY(tmp.get(bytes));
+  TL_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, idx.p, idx2.p, n));
+  count_launch();
+  unsigned long long nt = 0;
+  TL_CUDA(cudaMemcpy(&nt, cnt.p, sizeof(nt), cudaMemcpyDeviceToHost));
+  c->tr_n = (int64_t)nt;
+  TL_TRY(c->alloc(&c->tr_src, (size_t)std::max<int64_t>(c->tr_n, 1)));
+  TL_TRY(c->alloc(&c->tr_dst, (size_t)std::max<int64_t>(c->tr_n, 1)));
+  TL_TRY(c->alloc(&c->tr_deg, (size_t)std::max<int64_t>(c->tr_n, 1)));
+  if (c->tr_n > 0) {
+    k_tr_fill<<<grid_for(c->tr_n, 256), 256>>>(c->tr_n, idx2.p, c->u_off, c->u_offT, c->u_deg, c->tr_src, c->tr_dst,
+                                               c->tr_deg);
+    TL_CHECK_LAUNCH();
+  }
+  return TLFEA_OK;
+}
+
 static tlfea_status build_unit_meta(Context* c) {
   if (c->n_units == 0 || !c->unit_ptr) return TLFEA_OK;
   TL_TRY(c->alloc(&c->u_off, (size_t)c->n_units));
@@ -826,6 +883,10 @@ static tlfea_status build_unit_meta(Context* c) {
                                                     c->u_off, c->u_offT, c->u_deg, c->u_m);
   }
   TL_CHECK_LAUNCH();
+  {
+    const char* e = getenv("TLFEA_GT_SPLIT");
+    if (!c->upper && e && atoi(e) > 0) TL_TRY(build_transpose_list(c));
+  }
   return TLFEA_OK;
 }
 
