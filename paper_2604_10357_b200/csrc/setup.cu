@@ -1466,7 +1466,7 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   }
 
   TL_TRY(build_units(c));
-  if (c->nranks == 1) TL_TRY(build_sorted_scratch(c));
+  if (c->nranks == 1 && env_int("TLFEA_SORTED", 1) != 0) TL_TRY(build_sorted_scratch(c));  // 0: element-major scratch (diagnostics)
 
   // ---- consistent mass over the setup elements (reading Q4) and f_ff
   TL_TRY(c->alloc(&c->M, (size_t)c->nnz_c));

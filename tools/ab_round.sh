@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-TLFEA_GT_SPLIT=1 timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -m gpu -q -x 2>&1 | tail -1
-VAR=TLFEA_GT_SPLIT VALS="0 1" bash tools/ab_env.sh
+timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
+P=paper_2604_10357_b200
+LIBS="$P/libtlfea.so $P/libtlfea_nobulk.so" TILES=1 bash tools/ab.sh
