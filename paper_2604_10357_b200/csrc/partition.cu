@@ -62,9 +62,12 @@ static void make_plan(int64_t NE, int nen, const int32_t* cc, int64_t n_coef, co
 // ------------------------------------------------------------------ kernels
 __device__ __forceinline__ int ublk_p(int n, int a, int b) { return a * n - (a * (a - 1)) / 2 + (b - a); }
 
+// Kscr is element-major, or gather-sorted when dest is given: block (e, ub)
+// at position dest >> 1, stored transposed (relative to a <= b) when dest & 1.
 __global__ void k_pack_blocks(int64_t n, int nen, int nub, const int32_t* __restrict__ ptr,
                               const uint32_t* __restrict__ ent, const int64_t* __restrict__ off,
-                              const double* __restrict__ Kscr, double* __restrict__ out) {
+                              const double* __restrict__ Kscr, const int32_t* __restrict__ dest,
+                              double* __restrict__ out) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= n) return;
   double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -72,11 +75,17 @@ __global__ void k_pack_blocks(int64_t n, int nen, int nub, const int32_t* __rest
     const uint32_t en = ent[t];
     const int64_t e = en >> 8;
     const int a = (en >> 4) & 15, b = en & 15;
-    if (a <= b) {
-      const double* s = Kscr + (e * nub + ublk_p(nen, a, b)) * 9;
+    const int64_t ub = e * nub + (a <= b ? ublk_p(nen, a, b) : ublk_p(nen, b, a));
+    bool tr = a > b;
+    const double* s = Kscr + ub * 9;
+    if (dest) {
+      const int32_t dd = dest[ub];
+      s = Kscr + (int64_t)(dd >> 1) * 9;
+      tr = tr != ((dd & 1) != 0);
+    }
+    if (!tr) {
       for (int r = 0; r < 9; ++r) acc[r] += s[r];
     } else {
-      const double* s = Kscr + (e * nub + ublk_p(nen, b, a)) * 9;
       for (int i = 0; i < 3; ++i)
         for (int kk = 0; kk < 3; ++kk) acc[3 * i + kk] += s[3 * kk + i];
     }
@@ -86,13 +95,15 @@ __global__ void k_pack_blocks(int64_t n, int nen, int nub, const int32_t* __rest
 
 __global__ void k_pack_nodes(int64_t n, int nen, const int32_t* __restrict__ ptr,
                              const uint32_t* __restrict__ ent, const int64_t* __restrict__ off,
-                             const double* __restrict__ fscr, double* __restrict__ out) {
+                             const double* __restrict__ fscr, const int32_t* __restrict__ fdest,
+                             double* __restrict__ out) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= n) return;
   double f0 = 0, f1 = 0, f2 = 0;
   for (int32_t t = ptr[k]; t < ptr[k + 1]; ++t) {
     const uint32_t en = ent[t];
-    const double* s = fscr + ((int64_t)(en >> 4) * nen + (en & 15)) * 3;
+    const int64_t ea = (int64_t)(en >> 4) * nen + (en & 15);
+    const double* s = fscr + (fdest ? (int64_t)fdest[ea] : ea) * 3;
     f0 += s[0];
     f1 += s[1];
     f2 += s[2];
@@ -269,12 +280,12 @@ tlfea_status setup_exchange(Context* c, const std::vector<int32_t>& cc, const st
 tlfea_status launch_pack_send(Context* c, double* send, bool force_only, cudaStream_t s) {
   if (!force_only && c->n_send_blk > 0) {
     k_pack_blocks<<<gridn(c->n_send_blk, 256), 256, 0, s>>>(c->n_send_blk, c->nen, n_ublk_of(c->nen), c->sblk_ptr,
-                                                            c->sblk_ent, c->send_blk_off, c->Kscr, send);
+                                                            c->sblk_ent, c->send_blk_off, c->Kscr, c->dest, send);
     TL_CHECK_LAUNCH();
   }
   if (c->n_send_node > 0) {
     k_pack_nodes<<<gridn(c->n_send_node, 256), 256, 0, s>>>(c->n_send_node, c->nen, c->snode_ptr, c->snode_ent,
-                                                            c->send_node_off, c->fscr, send);
+                                                            c->send_node_off, c->fscr, c->fdest, send);
     TL_CHECK_LAUNCH();
   }
   return TLFEA_OK;

@@ -577,6 +577,20 @@ __global__ void k_unit_meta_upper(int64_t n_units, const int32_t* __restrict__ u
   u_m[u] = M[p];
 }
 
+// Partitioned contexts: element blocks with neither row owned (and forces of
+// nodes owned elsewhere) belong to no gather unit / owned node; they get the
+// scratch positions after the unit ranges, in element-major order, and are
+// read only by the pack kernels (partition.cu).
+__global__ void k_neg_flag(int64_t n, const int32_t* __restrict__ arr, int32_t* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = arr[i] < 0 ? 1 : 0;
+}
+__global__ void k_assign_rest(int64_t n, int32_t* __restrict__ arr, const int32_t* __restrict__ scan, int32_t base,
+                              int shift) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && arr[i] < 0) arr[i] = (base + scan[i]) << shift;
+}
+
 __global__ void k_force_dest(int64_t n, int nen, const uint32_t* __restrict__ node_ent, int32_t* __restrict__ fdest) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n) return;
@@ -791,7 +805,7 @@ static tlfea_status build_sorted_scratch(Context* c) {
   count_launch();
   int32_t npos = 0;
   TL_CUDA(cudaMemcpy(&npos, c->unit_ptr + c->n_units, sizeof(int32_t), cudaMemcpyDeviceToHost));
-  if ((int64_t)npos != c->n_el * nub)
+  if ((int64_t)npos > c->n_el * nub || (c->nranks == 1 && (int64_t)npos != c->n_el * nub))
     return fail(TLFEA_E_CUDA, "internal: gather-sorted scratch covers " + std::to_string(npos) + " of " +
                                   std::to_string(c->n_el * nub) + " element blocks");
   if (c->n_units > 0) {
@@ -801,9 +815,32 @@ static tlfea_status build_sorted_scratch(Context* c) {
   }
   int32_t nf = 0;
   TL_CUDA(cudaMemcpy(&nf, c->node_ptr + c->n_own, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  TL_CUDA(cudaMemset(c->fdest, 0xff, sizeof(int32_t) * std::max<int64_t>(c->n_el, 1) * nen));
   if (nf > 0) {
     k_force_dest<<<grid_for(nf, 256), 256>>>(nf, nen, c->node_ent, c->fdest);
     TL_CHECK_LAUNCH();
+  }
+  // partitioned contexts: the blocks / forces no owned row receives
+  auto rest = [&](int32_t* arr, int64_t n, int32_t base, int shift) -> tlfea_status {
+    if (n == 0 || (int64_t)base >= n) return TLFEA_OK;
+    TmpArr<int32_t> flag, scan;
+    TL_TRY(flag.get(n));
+    TL_TRY(scan.get(n));
+    k_neg_flag<<<grid_for(n, 256), 256>>>(n, arr, flag.p);
+    TL_CHECK_LAUNCH();
+    Tmp t2;
+    size_t b2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, flag.p, scan.p, n);
+    TL_TRY(t2.get(b2));
+    TL_CUDA(cub::DeviceScan::ExclusiveSum(t2.p, b2, flag.p, scan.p, n));
+    count_launch();
+    k_assign_rest<<<grid_for(n, 256), 256>>>(n, arr, scan.p, base, shift);
+    TL_CHECK_LAUNCH();
+    return TLFEA_OK;
+  };
+  if (c->nranks > 1) {
+    TL_TRY(rest(c->dest, c->n_el * nub, npos, 1));
+    TL_TRY(rest(c->fdest, c->n_el * nen, nf, 0));
   }
   return TLFEA_OK;
 }
@@ -1466,7 +1503,7 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   }
 
   TL_TRY(build_units(c));
-  if (c->nranks == 1 && env_int("TLFEA_SORTED", 1) != 0) TL_TRY(build_sorted_scratch(c));  // 0: element-major scratch (diagnostics)
+  if (env_int("TLFEA_SORTED", 1) != 0) TL_TRY(build_sorted_scratch(c));  // 0: element-major scratch (diagnostics)
 
   // ---- consistent mass over the setup elements (reading Q4) and f_ff
   TL_TRY(c->alloc(&c->M, (size_t)c->nnz_c));
