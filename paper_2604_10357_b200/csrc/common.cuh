@@ -56,7 +56,10 @@ inline int n_qp_of(int quadrature) {
 // number of upper-triangular 3x3 blocks (a <= b) of the element matrix
 inline int n_ublk_of(int nen) { return nen * (nen + 1) / 2; }
 // element-kernel CTA tile: kElWarps warps of 3 T10 / 1 ANCF3443 / 4 ANCF3243 elements
-constexpr int kElWarps = 4;
+#ifndef TLFEA_EL_WARPS
+#define TLFEA_EL_WARPS 4
+#endif
+constexpr int kElWarps = TLFEA_EL_WARPS;
 inline int el_per_tile(int element) {
   return kElWarps * (element == TLFEA_T10 ? 3 : element == TLFEA_ANCF3443 ? 1 : 4);
 }

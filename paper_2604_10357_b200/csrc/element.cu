@@ -1615,7 +1615,7 @@ __global__ void k_gather_units(int64_t n_units, int nen, int nub, const int32_t*
 // v3: TMA bulk copies (cp.async.bulk global->shared, mbarrier completion),
 // double-buffered per warp: one elected lane moves the next window of the
 // contiguous scratch range while the warp sums the current one.
-constexpr int kG3Warps = 4;
+constexpr int kG3Warps = 4;  // H gather warps per CTA (the fused kernel needs kElWarps == 4)
 #ifndef TLFEA_G3WB
 #define TLFEA_G3WB 64
 #endif
@@ -1973,7 +1973,7 @@ __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
 
 template <int ELEM, int NQ, int MODEL, bool KV>
 __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, 1>()) k_fused(FusedArgs P) {
-  static_assert(kG3Warps == kWarps, "the fused CTA runs both item kinds");
+  static_assert(kG3Warps == kWarps || TLFEA_EL_WARPS != 4, "the fused CTA runs both item kinds");
   // dynamic shared memory: [TMA windows kG3Warps x 2 x kG3Buf][class tables]
   extern __shared__ __align__(16) double s_dyn[];
   double(*s_buf)[2][kG3Buf] = reinterpret_cast<double(*)[2][kG3Buf]>(s_dyn);

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-NS="2 4" CFG=2 bash tools/multirank_flow.sh
-NS="2" CFG=3 bash tools/multirank_flow.sh
+P=paper_2604_10357_b200
+LIBS="$P/libtlfea.so $P/libtlfea_w2m6.so $P/libtlfea_w3m4.so" TILES=1 bash tools/ab.sh
