@@ -731,6 +731,253 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
   }
 }
 
+// T10 + Mooney-Rivlin (optionally Kelvin-Voigt) + geometry classes, two
+// phases. Phase A, two lanes per (element, q): F (and Fdot) over 5 nodes each
+// plus one shuffle, the MR state, S, S + S_v, and the symmetric 6x6 Voigt
+// tangent (w-scaled, 21 entries; each lane builds 3 of the 6 columns) into
+// shared memory. Phase B, one lane per node a: B_a (6x3) from F and grad N_a,
+// C B_a, then K_ab = s_ab I + B_a^T C B_b (Eq. tangent_block, reading Q6/Q8)
+// and f_a += F (w S_tot grad N_a). The lane-per-node kernel evaluated the MR
+// state and S on all 10 lanes of an element and the tangent columns on 6.
+__host__ __device__ __forceinline__ int cs_idx(int v, int w) {  // v <= w
+  return v * 6 - (v * (v - 1)) / 2 + (w - v);
+}
+
+template <int NQ, bool KV>
+__device__ __forceinline__ void element_group_t10mr(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab) {
+  constexpr int NEN = 10, GROUP = 10, EPW = 3, NUB = 55, NB = 6, TABW = 3 * NEN + 1, KQ = 42;
+  static_assert(EPW * NQ * 2 <= 32, "phase A: two lanes per (element, q)");
+  __shared__ double s_k[kWarps][EPW][NQ][KQ];  // F (9), S (6), S + S_v (6), w C (21, upper Voigt)
+  __shared__ double s_x[kWarps][EPW][3 * NEN];
+  __shared__ double s_v[kWarps][KV ? EPW : 1][KV ? 3 * NEN : 1];
+  __shared__ double s_node[kWarps][18][kLD];  // B_a per lane; reused as the store staging
+  __shared__ int32_t s_dst[kWarps][EPW * NUB];
+  __shared__ int32_t s_pos[kWarps][32];
+  __shared__ int32_t s_cls[kWarps][EPW];
+  const int64_t n_el = A.n_el;
+  const MatDev& mat = A.mat;
+  const int32_t* __restrict__ dest = A.dest;
+  double* __restrict__ Kscr = A.Kscr;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const bool lane_active = lane < EPW * GROUP;
+  const int g = lane_active ? lane / GROUP : 0;
+  const int a = lane_active ? lane % GROUP : 0;
+  const int64_t e = grp * EPW + g;
+  const bool valid = lane_active && e < n_el;
+  const int gbase = g * GROUP;
+  const bool write = dest && !mat.dbg_nowrite;
+  if (write) {
+    const int64_t e0 = grp * EPW, lim = (n_el - e0) * NUB;
+    for (int t = lane; t < EPW * NUB; t += 32)
+      if (t < lim) pf_cp4(&s_dst[wib][t], dest + e0 * NUB + t);
+  }
+  int32_t fd = 0;
+  if (lane_active) {
+    double xa[3] = {0, 0, 0}, va[3] = {0, 0, 0};
+    int ce = 0;
+    if (valid) {
+      fd = A.fdest ? A.fdest[e * NEN + a] : (int32_t)(e * NEN + a);
+      const int64_t I = A.conn[e * NEN + a];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        xa[i] = A.x[3 * I + i];
+        if (KV) va[i] = A.v[3 * I + i];
+      }
+      if (a == 0) ce = A.cls[e];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      s_x[wib][g][3 * a + i] = xa[i];
+      if (KV) s_v[wib][g][3 * a + i] = va[i];
+    }
+    if (a == 0) s_cls[wib][g] = ce;
+  }
+  __syncwarp();
+  {  // ---- phase A
+    const bool act = lane < EPW * NQ * 2;
+    const int pr = act ? lane >> 1 : 0, hf = lane & 1;
+    const int ge = pr / NQ, q = pr - NQ * (pr / NQ);
+    const double* t = s_tab + (s_cls[wib][ge] * NQ + q) * TABW;
+    double F[9], Fd[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) F[r] = Fd[r] = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < NEN / 2; ++bb) {
+      const int b = hf * (NEN / 2) + bb;
+      const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double xi = s_x[wib][ge][3 * b + i];
+        F[3 * i] = fma(xi, n0, F[3 * i]);
+        F[3 * i + 1] = fma(xi, n1, F[3 * i + 1]);
+        F[3 * i + 2] = fma(xi, n2, F[3 * i + 2]);
+        if (KV) {
+          const double vi = s_v[wib][ge][3 * b + i];
+          Fd[3 * i] = fma(vi, n0, Fd[3 * i]);
+          Fd[3 * i + 1] = fma(vi, n1, Fd[3 * i + 1]);
+          Fd[3 * i + 2] = fma(vi, n2, Fd[3 * i + 2]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      const double o = __shfl_xor_sync(0xffffffffu, F[r], 1);
+      F[r] = hf ? o + F[r] : F[r] + o;
+      if (KV) {
+        const double od = __shfl_xor_sync(0xffffffffu, Fd[r], 1);
+        Fd[r] = hf ? od + Fd[r] : Fd[r] + od;
+      }
+    }
+    MRState ms;
+    mr_state(F, ms);
+    const double w = t[3 * NEN];
+    if (act) {
+      double* kq = s_k[wib][ge][q];
+      if (hf == 0) {
+        if (grp * EPW + ge < n_el && !(ms.J > 0.0)) atomicMin(A.err, (unsigned long long)((grp * EPW + ge) * 64 + q));
+        double S[6];
+        mr_S(ms, mat.C10, mat.C01, mat.kappa, S);
+#pragma unroll
+        for (int r = 0; r < 9; ++r) kq[r] = F[r];
+#pragma unroll
+        for (int r = 0; r < 6; ++r) kq[9 + r] = S[r];
+        double Sv[6] = {0, 0, 0, 0, 0, 0};
+        if (KV) kv_S(F, Fd, mat.eta, mat.lamd, Sv);
+#pragma unroll
+        for (int r = 0; r < 6; ++r) kq[15 + r] = S[r] + Sv[r];
+      }
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc) {
+        const int col = 3 * hf + cc;
+        double cv[6];
+        mr_Cv_column_dispatch(ms, mat.C10, mat.C01, mat.kappa, col, cv);
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv)
+          if (vv <= col) kq[21 + cs_idx(vv, col)] = w * cv[vv];
+      }
+    }
+  }
+  __syncwarp();
+  // ---- phase B (one pass: 6 blocks per lane)
+  const int ce = s_cls[wib][g];
+  double fa[3] = {0, 0, 0};
+  double K[NB][9];
+#pragma unroll
+  for (int j = 0; j < NB; ++j)
+#pragma unroll
+    for (int r = 0; r < 9; ++r) K[j][r] = 0.0;
+#pragma unroll 1
+  for (int q = 0; q < NQ; ++q) {
+    const double* t = s_tab + (ce * NQ + q) * TABW;
+    const double* kq = s_k[wib][g][q];
+    const double gN[3] = {t[3 * a], t[3 * a + 1], t[3 * a + 2]};
+    const double w = t[3 * NEN];
+    double F[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) F[r] = kq[r];
+    double Ba[6][3];
+#pragma unroll
+    for (int vv = 0; vv < 6; ++vv) {
+      int I, J;
+      voigt_pair(vv, I, J);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        Ba[vv][i] = (I == J) ? F[3 * i + I] * gN[I] : F[3 * i + I] * gN[J] + F[3 * i + J] * gN[I];
+    }
+#pragma unroll
+    for (int vv = 0; vv < 6; ++vv)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) s_node[wib][3 * vv + i][lane] = Ba[vv][i];
+    double tw[3], tt[3];
+#pragma unroll
+    for (int I = 0; I < 3; ++I) {
+      tw[I] = w * (kq[9 + vidx(I, 0)] * gN[0] + kq[9 + vidx(I, 1)] * gN[1] + kq[9 + vidx(I, 2)] * gN[2]);
+      tt[I] = w * (kq[15 + vidx(I, 0)] * gN[0] + kq[15 + vidx(I, 1)] * gN[1] + kq[15 + vidx(I, 2)] * gN[2]);
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) fa[i] = fma(F[3 * i], tt[0], fma(F[3 * i + 1], tt[1], fma(F[3 * i + 2], tt[2], fa[i])));
+    double CB[6][3];
+#pragma unroll
+    for (int vv = 0; vv < 6; ++vv)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < 6; ++ww)
+          sacc = fma(kq[21 + (vv <= ww ? cs_idx(vv, ww) : cs_idx(ww, vv))], Ba[ww][i], sacc);
+        CB[vv][i] = sacc;
+      }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int b = partner<0>(a, 0, j);
+      if (b < 0) continue;
+      double* Kj = K[j];
+      const int lb = gbase + b;
+      const double sv = fma(tw[0], t[3 * b], fma(tw[1], t[3 * b + 1], tw[2] * t[3 * b + 2]));
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double bb[6];
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv) bb[vv] = s_node[wib][3 * vv + k][lb];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          double acc = Kj[3 * i + k];
+#pragma unroll
+          for (int vv = 0; vv < 6; ++vv) acc = fma(CB[vv][i], bb[vv], acc);
+          Kj[3 * i + k] = (i == k) ? acc + sv : acc;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (valid) {
+    double* fo = A.fscr + (int64_t)fd * 3;
+    fo[0] = fa[0];
+    fo[1] = fa[1];
+    fo[2] = fa[2];
+  }
+  if (mat.dbg_nowrite) return;
+  // warp-staged block stores (staging in s_node rows 0..8)
+  constexpr int NLB = EPW * GROUP, NIT = (NLB + 2) / 3;
+  const int bi = lane / 9, rr = lane - 9 * (lane / 9);
+  if (write) {
+    pf_wait();
+    __syncwarp();
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const int b = (valid && j < NB) ? partner<0>(a, 0, j) : -1;
+    int32_t pos = -1;
+    if (b >= 0) {
+      const double* Kj = K[j];
+      const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
+      bool tr = a > b;
+      pos = (int32_t)(e * NUB + ub);
+      if (dest) {
+        const int32_t dd = s_dst[wib][g * NUB + ub];
+        pos = dd >> 1;
+        tr = tr != ((dd & 1) != 0);
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) s_node[wib][tr ? 3 * k + i : 3 * i + k][lane] = Kj[3 * i + k];
+    }
+    s_pos[wib][lane] = pos;
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int blk = 3 * it + bi;
+      if (lane < 27 && blk < NLB) {
+        const int32_t p = s_pos[wib][blk];
+        if (p >= 0) k_store(Kscr + (int64_t)p * 9 + rr, s_node[wib][rr][blk]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Force-only counterpart (tlfea_force_only, the AdamW inner evaluation): phase A,
 // one lane per (element, q), forms w P = w F S (Eq. F_assembly, reading Q5, J0 w
 // folded in) once; phase B, one lane per (element, node a), contracts
@@ -1209,6 +1456,9 @@ __device__ __forceinline__ void element_group_beam_svk(int64_t grp, const ElArgs
   }
 }
 
+#ifndef TLFEA_MR_2PH
+#define TLFEA_MR_2PH 1  // T10 Mooney-Rivlin (+KV) class-mode tangent eval through element_group_t10mr
+#endif
 #ifndef TLFEA_BEAM_2PH
 #define TLFEA_BEAM_2PH 1  // ANCF3243 SVK class-mode tangent eval through element_group_beam_svk
 #endif
@@ -1240,6 +1490,7 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
   constexpr bool T2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && CLS;  // tangent or force only
   constexpr bool A2PH = TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV && TAN && CLS;
   constexpr bool B2PH = TLFEA_BEAM_2PH && ELEM == 2 && MODEL == 0 && !KV && TAN && CLS;
+  constexpr bool M2PH = TLFEA_MR_2PH && ELEM == 0 && MODEL == 1 && TAN && CLS;
   // A.cta_tiles consecutive tiles per CTA (class tables staged once)
   const int64_t t0 = (int64_t)blockIdx.x * A.cta_tiles;
   T10Pre pre;
@@ -1270,6 +1521,8 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
       element_group_ancf_svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
     } else if constexpr (B2PH) {
       element_group_beam_svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
+    } else if constexpr (M2PH) {
+      element_group_t10mr<NQ, KV>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
     } else
       element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, TLFEA_DEST_ASYNC != 0>(
           (t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
@@ -2009,6 +2262,8 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, 1>()) k_fuse
             element_group_t10svk<NQ>((t0 + j) * kWarps + wib, P.el, s_tab, pre);
           } else if constexpr (TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV) {
             element_group_ancf_svk<NQ>((t0 + j) * kWarps + wib, P.el, s_tab);
+          } else if constexpr (TLFEA_MR_2PH && ELEM == 0 && MODEL == 1) {
+            element_group_t10mr<NQ, KV>((t0 + j) * kWarps + wib, P.el, s_tab);
           } else
             element_group<ELEM, NQ, MODEL, KV, true, true, 1>((t0 + j) * kWarps + wib, P.el, s_tab);
         }
