@@ -519,6 +519,28 @@ __device__ __forceinline__ void t10_preload(int64_t grp, const ElArgs& A, T10Pre
   }
 }
 
+// Table mode (meshes without geometry classes): the warp's 3 elements' per-(e,q)
+// tables (grad N, J0 w; the paper's layout) are staged into rows
+// slot = 3 wib + g of the dynamic shared table, so the two-phase groups read
+// them exactly like class tables (class id := slot).
+template <int NQ>
+__device__ __forceinline__ void t10_stage_tables(int64_t grp, const ElArgs& A, double* __restrict__ s_tab) {
+  constexpr int NEN = 10, EPW = 3, TABW = 3 * NEN + 1, PER = NQ * 3 * NEN;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t e0 = grp * EPW;
+  for (int t = lane; t < EPW * PER; t += 32) {
+    const int g = t / PER, r = t - PER * g, q = r / (3 * NEN), c = r - 3 * NEN * q;
+    const int64_t e = e0 + g;
+    s_tab[((wib * EPW + g) * NQ + q) * TABW + c] = e < A.n_el ? A.gradN[e * PER + r] : 0.0;
+  }
+  if (lane < EPW * NQ) {
+    const int g = lane / NQ, q = lane - NQ * g;
+    const int64_t e = e0 + g;
+    s_tab[((wib * EPW + g) * NQ + q) * TABW + 3 * NEN] = e < A.n_el ? A.J0w[e * NQ + q] : 0.0;
+  }
+  __syncwarp();
+}
+
 #ifndef TLFEA_T10_2PH_NPASS
 #define TLFEA_T10_2PH_NPASS 2  // config 3: 2 passes at 3 CTAs/SM (166 registers) 9.96 ms; 3 passes at 4 CTAs 10.72; 1 pass 12.97
 #endif
@@ -744,7 +766,8 @@ __host__ __device__ __forceinline__ int cs_idx(int v, int w) {  // v <= w
 }
 
 template <int NQ, bool KV>
-__device__ __forceinline__ void element_group_t10mr(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab) {
+__device__ __forceinline__ void element_group_t10mr(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab,
+                                                    bool table_mode = false) {
   constexpr int NEN = 10, GROUP = 10, EPW = 3, NUB = 55, NB = 6, TABW = 3 * NEN + 1, KQ = 42;
   static_assert(EPW * NQ * 2 <= 32, "phase A: two lanes per (element, q)");
   __shared__ double s_k[kWarps][EPW][NQ][KQ];  // F (9), S (6), S + S_v (6), w C (21, upper Voigt)
@@ -783,8 +806,9 @@ __device__ __forceinline__ void element_group_t10mr(int64_t grp, const ElArgs& A
         xa[i] = A.x[3 * I + i];
         if (KV) va[i] = A.v[3 * I + i];
       }
-      if (a == 0) ce = A.cls[e];
+      if (a == 0) ce = table_mode ? wib * EPW + g : A.cls[e];
     }
+    if (table_mode) ce = wib * EPW + g;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       s_x[wib][g][3 * a + i] = xa[i];
@@ -1487,10 +1511,12 @@ __host__ __device__ constexpr int el_minb_k() {
 template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS>
 __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV, TAN, CLS>()) k_element(ElArgs A) {
   extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
+  // (SVK in table mode measured slower two-phase: config 3 without classes 13.97 vs 12.61 ms, force only
+  // 1.20 vs 1.11 ms — staging the per-(e,q) tables serializes the group start; MR gains: 0.59 vs 0.71 ms)
   constexpr bool T2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && CLS;  // tangent or force only
   constexpr bool A2PH = TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV && TAN && CLS;
   constexpr bool B2PH = TLFEA_BEAM_2PH && ELEM == 2 && MODEL == 0 && !KV && TAN && CLS;
-  constexpr bool M2PH = TLFEA_MR_2PH && ELEM == 0 && MODEL == 1 && TAN && CLS;
+  constexpr bool M2PH = TLFEA_MR_2PH && ELEM == 0 && MODEL == 1 && TAN;
   // A.cta_tiles consecutive tiles per CTA (class tables staged once)
   const int64_t t0 = (int64_t)blockIdx.x * A.cta_tiles;
   T10Pre pre;
@@ -1522,7 +1548,8 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
     } else if constexpr (B2PH) {
       element_group_beam_svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
     } else if constexpr (M2PH) {
-      element_group_t10mr<NQ, KV>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
+      if constexpr (!CLS) t10_stage_tables<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
+      element_group_t10mr<NQ, KV>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, !CLS);
     } else
       element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, TLFEA_DEST_ASYNC != 0>(
           (t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
@@ -2398,7 +2425,16 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
     const unsigned g = (unsigned)((grid + A.cta_tiles - 1) / A.cta_tiles);
     k_element<ELEM, NQ, MODEL, KV, TAN, true, el_npass<ELEM, MODEL>()><<<g, kWarps * 32, smem, s>>>(A);
   } else {
-    k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>()><<<grid, kWarps * 32, 0, s>>>(A);
+    // the T10 two-phase groups stage each warp's element tables in dynamic shared memory
+    constexpr bool stage = ELEM == 0 && TLFEA_MR_2PH && MODEL == 1 && TAN;
+    const size_t smem = stage ? sizeof(double) * kWarps * G::EPW * NQ * (G::NEN * 3 + 1) : 0;
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+      TL_CUDA(cudaFuncSetAttribute(k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>()>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      smem_set = smem;
+    }
+    k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>()><<<grid, kWarps * 32, smem, s>>>(A);
   }
   TL_CHECK_LAUNCH();
   return TLFEA_OK;

@@ -639,6 +639,10 @@ static tlfea_status build_geometry_classes(Context* c, const double* dX) {
   const int max_cls = c->element == TLFEA_T10 ? 32 : 4;
   c->n_cls = 0;
   if (n == 0) return TLFEA_OK;
+  {
+    const char* e = getenv("TLFEA_NO_CLASSES");  // measure the per-(e,q) table path on any mesh
+    if (e && atoi(e) > 0) return TLFEA_OK;
+  }
   TmpArr<unsigned long long> key, key2;
   TmpArr<int64_t> idx, idx2;
   TmpArr<int32_t> flag, run;
