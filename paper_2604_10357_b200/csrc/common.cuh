@@ -149,13 +149,6 @@ struct Context {
   int32_t* u_off = nullptr;       // [n_units] H offset of block (I,J): 9 rowptr_c[i] + 3 k
   int32_t* u_offT = nullptr;      // [n_units] H offset of (J,I) or -1
   int32_t* u_deg = nullptr;       // [n_units] deg(I) | deg(J) << 16
-  // split FULL gather (opt-in TLFEA_GT_SPLIT=1 at setup): the H gather writes
-  // the upper blocks only; k_transpose_lower copies them to the lower blocks
-  // in destination order
-  int64_t tr_n = 0;
-  int32_t* tr_src = nullptr;      // [tr_n] H offset of (I,J), sorted by tr_dst
-  int32_t* tr_dst = nullptr;      // [tr_n] H offset of (J,I)
-  int32_t* tr_deg = nullptr;      // [tr_n] deg(I) | deg(J) << 16
   double* u_m = nullptr;          // [n_units] M_IJ
   // fused persistent eval (single rank, class tables, gather-sorted scratch):
   // one launch works through a list of element items (kElTile elements x
@@ -166,9 +159,7 @@ struct Context {
   uint32_t* fz_list = nullptr;    // [fz_items] type << 30 | index (0 element, 1 H gather, 2 f gather)
   int32_t* fz_lo = nullptr;       // [fz_nG + fz_nF] first element chunk read by a gather item
   int32_t* fz_hi = nullptr;       // [fz_nG + fz_nF] last element chunk read
-  uint32_t* fz_sync = nullptr;
-  unsigned long long* g4_ticket = nullptr;  // H gather v4 work ticket (monotone across launches)
-  unsigned long long g4_base = 0;           // its value at the next launch's start    // [1 + fz_chunks]: work ticket, completed element items per chunk
+  uint32_t* fz_sync = nullptr;    // [1 + fz_chunks]: work ticket, completed element items per chunk
   double* Kscr = nullptr;         // [n_el][n_ublk][9]
   double* fscr = nullptr;         // [n_el][nen][3]
   unsigned long long* err_flag = nullptr;  // min over (e*64+q) with det F <= 0 (MR)

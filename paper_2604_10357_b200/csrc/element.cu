@@ -1933,7 +1933,6 @@ struct GatherArgs {
   double h;
   double* H;
   int upper;  // UPPER H storage (u_deg = L | diagonal << 16, no transposed copy)
-  int skipT;  // split FULL gather: upper blocks only (k_transpose_lower writes the rest)
   int dbg_gt; // diagnostics (TLFEA_DBG_GT=1, timing only, corrupts the scratch): transposes to contiguous scratch
 };
 
@@ -2027,7 +2026,7 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
       for (int f = 0; f < 3; ++f) o2[32 * (3 * d + f)] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
     return;
   }
-  if (offT >= 0 && !A.skipT) {
+  if (offT >= 0) {
     double* o2 = H + offT;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -2036,25 +2035,6 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
   }
 }
 
-// Split FULL gather, second half: lower block (J,I) = upper block (I,J)^T,
-// one thread per transposed block in destination order (coalesced writes;
-// the reads of the upper blocks are the scattered side).
-__global__ void k_transpose_lower(int64_t n, const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
-                                  const int32_t* __restrict__ deg, double* __restrict__ H) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int32_t s0 = src[k], d0 = dst[k], dg = deg[k];
-  const int dI = dg & 0xffff, dJ = dg >> 16;
-  double v[9];
-#pragma unroll
-  for (int f = 0; f < 3; ++f)
-#pragma unroll
-    for (int d = 0; d < 3; ++d) v[3 * d + f] = H[s0 + 3 * f * dI + d];
-#pragma unroll
-  for (int d = 0; d < 3; ++d)
-#pragma unroll
-    for (int f = 0; f < 3; ++f) H[d0 + 3 * d * dJ + f] = v[3 * d + f];
-}
 
 __device__ __forceinline__ void g3_init(double (*s_buf)[2][kG3Buf], uint64_t (*s_bar)[2], G3Warp& W) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -2076,145 +2056,6 @@ __global__ void __launch_bounds__(kG3Warps * 32) k_gather_units_v3(GatherArgs A)
   G3Warp W;
   g3_init(s_buf, s_bar, W);
   gather_units_warp(((int64_t)blockIdx.x * kG3Warps + (threadIdx.x >> 5)) * 32, A, W);
-}
-
-// v4: persistent warps over 32-unit groups in grid-stride order (the groups
-// in flight stay a compact window of the unit list, as with v3's launch
-// order), with the window stream pipelined ACROSS groups: the next group's
-// metadata is loaded while the current group is summed, and its first TMA
-// window is issued while the current group's last window is consumed, so a
-// warp always has one window in flight instead of paying the metadata and
-// first-window latencies per group.
-struct G4Meta {
-  int64_t P0, P1;
-  int32_t my0, my1, off, offT, dg;
-  double m;
-};
-
-__device__ __forceinline__ void g4_meta(int64_t u0, const GatherArgs& A, G4Meta& M) {
-  const int lane = threadIdx.x & 31;
-  const int64_t u = u0 + lane, uend = min(u0 + 32, A.n_units);
-  M.P0 = A.unit_ptr[u0];
-  M.P1 = A.unit_ptr[uend];
-  M.my0 = M.my1 = M.dg = 0;
-  M.off = 0;
-  M.offT = -1;
-  M.m = 0.0;
-  if (u < A.n_units) {
-    M.my0 = A.unit_ptr[u];
-    M.my1 = A.unit_ptr[u + 1];
-    M.off = A.u_off[u];
-    M.offT = A.u_offT[u];
-    M.dg = A.u_deg[u];
-    M.m = A.u_m[u];
-  }
-}
-
-__device__ __forceinline__ void g4_issue(const double* Kscr, int64_t P0, int64_t P1, int k, double* buf, uint64_t* bar) {
-  const int64_t w0 = P0 + (int64_t)k * kG3WB, w1 = min(w0 + (int64_t)kG3WB, P1);
-  const uintptr_t a = (uintptr_t)(Kscr + w0 * 9) & ~(uintptr_t)15;
-  const uintptr_t b = ((uintptr_t)(Kscr + w1 * 9) + 15) & ~(uintptr_t)15;
-  bulk_load(buf, (const void*)a, (unsigned)(b - a), bar);
-}
-
-__device__ __forceinline__ void g4_write(const GatherArgs& A, const G4Meta& M, const double* acc) {
-  const double h = A.h, mh = M.m / h;
-  double* __restrict__ H = A.H;
-  if (A.upper) {
-    const int L = M.dg & 0xffff;
-    const bool diag = (M.dg >> 16) != 0;
-    double* out = H + M.off;
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-#pragma unroll
-      for (int f = 0; f < 3; ++f)
-        if (!diag || f >= d) out[f + d * (2 + 3 * L) - d * (d - 1) / 2] = fma(h, acc[3 * d + f], d == f ? mh : 0.0);
-    return;
-  }
-  const int deg = M.dg & 0xffff, degT = M.dg >> 16;
-  double* out = H + M.off;
-#pragma unroll
-  for (int d = 0; d < 3; ++d)
-#pragma unroll
-    for (int f = 0; f < 3; ++f) h_store(out + 3 * d * deg + f, fma(h, acc[3 * d + f], d == f ? mh : 0.0));
-  if (M.offT >= 0 && !A.skipT) {
-    double* o2 = H + M.offT;
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-#pragma unroll
-      for (int f = 0; f < 3; ++f) h_store(o2 + 3 * d * degT + f, fma(h, acc[3 * f + d], d == f ? mh : 0.0));
-  }
-}
-
-__global__ void __launch_bounds__(kG3Warps * 32)
-    k_gather_units_v4(GatherArgs A, int64_t n_groups, unsigned long long* ticket, unsigned long long base) {
-  __shared__ __align__(16) double s_buf[kG3Warps][2][kG3Buf];
-  __shared__ __align__(8) uint64_t s_bar[kG3Warps][2];
-  G3Warp W;
-  g3_init(s_buf, s_bar, W);
-  const int lane = threadIdx.x & 31;
-  const double* __restrict__ Kscr = A.Kscr;
-  // groups are handed out by a global ticket in list order (like the block
-  // scheduler's launch order): every warp takes exactly one ticket past the
-  // end, so each launch advances the counter by n_groups + warps in the grid
-  auto take = [&]() -> int64_t {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(ticket, 1ull);
-    return (int64_t)(__shfl_sync(0xffffffffu, t, 0) - base);
-  };
-  int64_t g = take();
-  if (g >= n_groups) return;
-  G4Meta cur;
-  g4_meta(g * 32, A, cur);
-  uint32_t wi = 0;  // windows issued by this warp (buffer wi & 1)
-  uint32_t wc = 0;  // windows consumed (buffer wc & 1, phase (wc >> 1) & 1)
-  if (lane == 0 && cur.P1 > cur.P0) {
-    g4_issue(Kscr, cur.P0, cur.P1, 0, W.buf[wi & 1], &W.bar[wi & 1]);
-    ++wi;
-  }
-#pragma unroll 1
-  for (;;) {
-    const int64_t gn = take();
-    const bool has_next = gn < n_groups;
-    G4Meta nxt;
-    if (has_next) g4_meta(gn * 32, A, nxt);
-    const int nwin = (int)((cur.P1 - cur.P0 + kG3WB - 1) / kG3WB);
-    bool next_issued = false;
-    double acc[9];
-#pragma unroll
-    for (int r = 0; r < 9; ++r) acc[r] = 0.0;
-#pragma unroll 1
-    for (int k = 0; k < nwin; ++k) {
-      if (k + 1 < nwin) {
-        if (lane == 0) g4_issue(Kscr, cur.P0, cur.P1, k + 1, W.buf[wi & 1], &W.bar[wi & 1]);
-        ++wi;
-      } else if (has_next && nxt.P1 > nxt.P0) {
-        if (lane == 0) g4_issue(Kscr, nxt.P0, nxt.P1, 0, W.buf[wi & 1], &W.bar[wi & 1]);
-        ++wi;
-        next_issued = true;
-      }
-      mbar_wait(&W.bar[wc & 1], (wc >> 1) & 1);
-      const int64_t w0 = cur.P0 + (int64_t)k * kG3WB, w1 = min(w0 + (int64_t)kG3WB, cur.P1);
-      const int delta = (int)(((uintptr_t)(Kscr + w0 * 9) & 15) >> 3);
-      const double* buf = W.buf[wc & 1] + delta;
-      const int64_t a0 = max((int64_t)cur.my0, w0), a1 = min((int64_t)cur.my1, w1);
-      for (int64_t t = a0; t < a1; ++t) {
-        const double* sb = buf + (t - w0) * 9;
-#pragma unroll
-        for (int r = 0; r < 9; ++r) acc[r] += sb[r];
-      }
-      ++wc;
-      __syncwarp();
-    }
-    if (!next_issued && has_next && nxt.P1 > nxt.P0) {
-      if (lane == 0) g4_issue(Kscr, nxt.P0, nxt.P1, 0, W.buf[wi & 1], &W.bar[wi & 1]);
-      ++wi;
-    }
-    if (g * 32 + lane < A.n_units) g4_write(A, cur, acc);
-    if (!has_next) break;
-    cur = nxt;
-    g = gn;
-  }
 }
 
 // ------------------------------------------------- fused persistent eval
@@ -2475,7 +2316,6 @@ static GatherArgs gather_args(const Context* c, double h, double* H) {
   A.h = h;
   A.H = H;
   A.upper = c->upper;
-  A.skipT = c->tr_n > 0 ? 1 : 0;
   {
     static int dbg = -1;
     if (dbg < 0) {
@@ -2573,39 +2413,8 @@ tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
   if (c->n_units == 0) return TLFEA_OK;
   if (c->u_off) {
     const int64_t per = (int64_t)kG3Warps * 32;
-    static int g4 = -1, g4_grid = 0;
-    if (g4 < 0) {
-      const char* e = getenv("TLFEA_G4");
-      g4 = e ? atoi(e) : 0;  // measured slower than v3 on config 3
-      int per_sm = 0, n_sm = 0, dev = 0;
-      TL_CUDA(cudaGetDevice(&dev));
-      TL_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-      TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_units_v4, kG3Warps * 32, 0));
-      const char* m = getenv("TLFEA_G4_CTAS");  // CTAs per SM override
-      if (m) per_sm = std::min(per_sm, atoi(m));
-      g4_grid = std::max(1, per_sm) * n_sm;
-    }
-    if (g4 && c->g4_ticket) {
-      const int64_t n_groups = (c->n_units + 31) / 32;
-      const int64_t grid = std::min<int64_t>(g4_grid, (n_groups + kG3Warps - 1) / kG3Warps);
-      k_gather_units_v4<<<(unsigned)grid, kG3Warps * 32, 0, s>>>(gather_args(c, h, H), n_groups, c->g4_ticket,
-                                                                  c->g4_base);
-      TL_CHECK_LAUNCH();
-      c->g4_base += (unsigned long long)n_groups + (unsigned long long)grid * kG3Warps;
-      return TLFEA_OK;
-    }
-    static int pad = -1;  // diagnostics: dynamic shared memory that caps the resident CTAs per SM
-    if (pad < 0) {
-      const char* e = getenv("TLFEA_G3_SMEM_PAD");
-      pad = e ? atoi(e) : 0;
-      if (pad > 0) TL_CUDA(cudaFuncSetAttribute(k_gather_units_v3, cudaFuncAttributeMaxDynamicSharedMemorySize, pad));
-    }
-    k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, pad, s>>>(gather_args(c, h, H));
+    k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(gather_args(c, h, H));
     TL_CHECK_LAUNCH();
-    if (c->tr_n > 0) {
-      k_transpose_lower<<<gridn(c->tr_n, 256), 256, 0, s>>>(c->tr_n, c->tr_src, c->tr_dst, c->tr_deg, H);
-      TL_CHECK_LAUNCH();
-    }
     return TLFEA_OK;
   }
   k_gather_units<<<gridn(c->n_units, 256), 256, 0, s>>>(c->n_units, c->nen, n_ublk_of(c->nen), c->unit_p,

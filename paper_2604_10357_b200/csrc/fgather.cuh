@@ -9,6 +9,11 @@
 
 namespace tlfea {
 
+#ifndef TLFEA_FG_UNROLL
+#define TLFEA_FG_UNROLL 4
+#endif
+constexpr int kFgUnroll = TLFEA_FG_UNROLL;
+
 struct FArgs {
   int64_t n_own;
   const int32_t* node_ptr;   // [n_own+1] node-sorted force scratch ranges
@@ -37,14 +42,14 @@ __device__ __forceinline__ void gather_f_dof_one(int64_t t, const FArgs& A) {
     f = A.fpart_in[t];
   } else {
     const int32_t t0 = A.node_ptr[i], t1 = A.node_ptr[i + 1];
-#pragma unroll 4
+#pragma unroll kFgUnroll
     for (int32_t s = t0; s < t1; ++s) f += A.fscr[3 * (int64_t)s + d];
   }
   if (A.fint) A.fint[t] = f;
   if (A.mode == 1 || !A.g) return;
   double m = 0.0;
   const int32_t p0 = A.rowptr_c[i], p1 = A.rowptr_c[i + 1];
-#pragma unroll 4
+#pragma unroll kFgUnroll
   for (int32_t p = p0; p < p1; ++p) {
     const int64_t J = A.cols_c[p];
     m += A.M[p] * (A.v[3 * J + d] - (A.vn ? A.vn[3 * J + d] : 0.0));

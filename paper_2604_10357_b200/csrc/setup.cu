@@ -705,32 +705,6 @@ static tlfea_status build_geometry_classes(Context* c, const double* dX) {
   return TLFEA_OK;
 }
 
-// Tile order of the gather units: key (I >> t, J >> t, I & m, J & m), so a
-// 32-unit gather group covers a few 2^t x 2^t tiles of the block pattern and
-// both its direct (I,J) and its transposed (J,I) writes land in short runs of
-// adjacent blocks (with the plain (I,J) order the transposes are isolated
-// 24-byte pieces, one row each).
-__global__ void k_unit_tilekey(int64_t nu, int t, const int32_t* __restrict__ unit_p,
-                               const int32_t* __restrict__ blk_row, const int32_t* __restrict__ own_nodes,
-                               const int32_t* __restrict__ cols_c, unsigned long long* __restrict__ key,
-                               int32_t* __restrict__ idx) {
-  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (u >= nu) return;
-  const int32_t p = unit_p[u];
-  const unsigned long long I = (unsigned)own_nodes[blk_row[p]], J = (unsigned)cols_c[p];
-  const unsigned long long m = (1ull << t) - 1;
-  key[u] = (((I >> t) << (31 - t)) | (J >> t)) << (2 * t) | ((I & m) << t) | (J & m);
-  idx[u] = (int32_t)u;
-}
-
-__global__ void k_permute2(int64_t n, const int32_t* __restrict__ idx, const int32_t* __restrict__ a,
-                           const int32_t* __restrict__ b, int32_t* __restrict__ a2, int32_t* __restrict__ b2) {
-  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (u >= n) return;
-  a2[u] = a[idx[u]];
-  b2[u] = b[idx[u]];
-}
-
 static tlfea_status build_units(Context* c) {
   c->n_units = 0;
   if (c->nnz_c == 0) return TLFEA_OK;
@@ -764,25 +738,6 @@ static tlfea_status build_units(Context* c) {
   TL_TRY(c->alloc(&c->unit_pT, (size_t)nu));
   TL_CUDA(cudaMemcpy(c->unit_p, up.p, sizeof(int32_t) * nu, cudaMemcpyDeviceToDevice));
   TL_CUDA(cudaMemcpy(c->unit_pT, upT.p, sizeof(int32_t) * nu, cudaMemcpyDeviceToDevice));
-  const char* ts = getenv("TLFEA_UNIT_TILE");
-  const int t = ts && ts[0] ? atoi(ts) : 0;
-  if (t > 0 && t < 16 && c->nranks == 1 && nu > 0) {
-    TmpArr<unsigned long long> key, key2;
-    TmpArr<int32_t> idx, idx2;
-    TL_TRY(key.get(nu));
-    TL_TRY(key2.get(nu));
-    TL_TRY(idx.get(nu));
-    TL_TRY(idx2.get(nu));
-    k_unit_tilekey<<<grid_for(nu, 256), 256>>>(nu, t, c->unit_p, c->blk_row, c->own_nodes, c->cols_c, key.p, idx.p);
-    TL_CHECK_LAUNCH();
-    bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, idx.p, idx2.p, nu, 0, 62);
-    TL_TRY(tmp.get(bytes));
-    TL_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, idx.p, idx2.p, nu, 0, 62));
-    count_launch();
-    k_permute2<<<grid_for(nu, 256), 256>>>(nu, idx2.p, up.p, upT.p, c->unit_p, c->unit_pT);
-    TL_CHECK_LAUNCH();
-  }
   return TLFEA_OK;
 }
 
@@ -849,72 +804,12 @@ static tlfea_status build_sorted_scratch(Context* c) {
   return TLFEA_OK;
 }
 
-__global__ void k_tr_keys(int64_t n, const int32_t* __restrict__ u_offT, uint32_t* __restrict__ key,
-                          int32_t* __restrict__ idx) {
-  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (u >= n) return;
-  key[u] = (uint32_t)u_offT[u];  // -1 (no transpose) sorts last
-  idx[u] = (int32_t)u;
-}
-__global__ void k_tr_fill(int64_t n, const int32_t* __restrict__ idx, const int32_t* __restrict__ u_off,
-                          const int32_t* __restrict__ u_offT, const int32_t* __restrict__ u_deg,
-                          int32_t* __restrict__ src, int32_t* __restrict__ dst, int32_t* __restrict__ deg) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int32_t u = idx[k];
-  src[k] = u_off[u];
-  dst[k] = u_offT[u];
-  deg[k] = u_deg[u];
-}
-__global__ void k_tr_count(int64_t n, const int32_t* __restrict__ u_offT, unsigned long long* __restrict__ cnt) {
-  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (u < n && u_offT[u] >= 0) atomicAdd(cnt, 1ull);  // setup only: an integer count
-}
-
-static tlfea_status build_transpose_list(Context* c) {
-  const int64_t n = c->n_units;
-  TmpArr<uint32_t> key, key2;
-  TmpArr<int32_t> idx, idx2;
-  TmpArr<unsigned long long> cnt;
-  TL_TRY(key.get(n));
-  TL_TRY(key2.get(n));
-  TL_TRY(idx.get(n));
-  TL_TRY(idx2.get(n));
-  TL_TRY(cnt.get(1));
-  TL_CUDA(cudaMemset(cnt.p, 0, sizeof(unsigned long long)));
-  k_tr_keys<<<grid_for(n, 256), 256>>>(n, c->u_offT, key.p, idx.p);
-  TL_CHECK_LAUNCH();
-  k_tr_count<<<grid_for(n, 256), 256>>>(n, c->u_offT, cnt.p);
-  TL_CHECK_LAUNCH();
-  Tmp tmp;
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, idx.p, idx2.p, n);
-  TL_TRY(tmp.get(bytes));
-  TL_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, idx.p, idx2.p, n));
-  count_launch();
-  unsigned long long nt = 0;
-  TL_CUDA(cudaMemcpy(&nt, cnt.p, sizeof(nt), cudaMemcpyDeviceToHost));
-  c->tr_n = (int64_t)nt;
-  TL_TRY(c->alloc(&c->tr_src, (size_t)std::max<int64_t>(c->tr_n, 1)));
-  TL_TRY(c->alloc(&c->tr_dst, (size_t)std::max<int64_t>(c->tr_n, 1)));
-  TL_TRY(c->alloc(&c->tr_deg, (size_t)std::max<int64_t>(c->tr_n, 1)));
-  if (c->tr_n > 0) {
-    k_tr_fill<<<grid_for(c->tr_n, 256), 256>>>(c->tr_n, idx2.p, c->u_off, c->u_offT, c->u_deg, c->tr_src, c->tr_dst,
-                                               c->tr_deg);
-    TL_CHECK_LAUNCH();
-  }
-  return TLFEA_OK;
-}
-
 static tlfea_status build_unit_meta(Context* c) {
   if (c->n_units == 0 || !c->unit_ptr) return TLFEA_OK;
   TL_TRY(c->alloc(&c->u_off, (size_t)c->n_units));
   TL_TRY(c->alloc(&c->u_offT, (size_t)c->n_units));
   TL_TRY(c->alloc(&c->u_deg, (size_t)c->n_units));
   TL_TRY(c->alloc(&c->u_m, (size_t)c->n_units));
-  TL_TRY(c->alloc(&c->g4_ticket, 1));
-  TL_CUDA(cudaMemset(c->g4_ticket, 0, sizeof(unsigned long long)));
-  c->g4_base = 0;
   if (c->upper) {
     k_unit_meta_upper<<<grid_for(c->n_units, 256), 256>>>(c->n_units, c->unit_p, c->blk_row, c->rowptr_c, c->cols_c,
                                                           c->own_nodes, c->ubase, c->M, c->u_off, c->u_offT,
@@ -924,10 +819,7 @@ static tlfea_status build_unit_meta(Context* c) {
                                                     c->u_off, c->u_offT, c->u_deg, c->u_m);
   }
   TL_CHECK_LAUNCH();
-  {
-    const char* e = getenv("TLFEA_GT_SPLIT");
-    if (!c->upper && e && atoi(e) > 0) TL_TRY(build_transpose_list(c));
-  }
+
   return TLFEA_OK;
 }
 
