@@ -547,16 +547,17 @@ __device__ __forceinline__ void t10_stage_tables(int64_t grp, const ElArgs& A, d
 #ifndef TLFEA_T10_2PH_MINB
 #define TLFEA_T10_2PH_MINB 3
 #endif
-template <int NQ>
+template <int NQ, bool KV = false>
 __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab,
                                                      const T10Pre& pre) {
   constexpr int NEN = 10, GROUP = 10, EPW = 3, NUB = 55, NB = 6, TABW = 3 * NEN + 1;
   constexpr int NPASS = TLFEA_T10_2PH_NPASS;
   constexpr int NBP = (NB + NPASS - 1) / NPASS;
-  constexpr int KQ = 21;  // per (element, q): F (9), S (6), F F^T (6)
+  constexpr int KQ = KV ? 27 : 21;  // per (element, q): F (9), S (6), F F^T (6) [, S + S_v (6)]
   __shared__ double s_ga[kWarps][NQ][3][kLD];
   __shared__ double s_k[kWarps][EPW][NQ][KQ];
   __shared__ double s_x[kWarps][EPW][3 * NEN];
+  __shared__ double s_v[kWarps][KV ? EPW : 1][KV ? 3 * NEN : 1];
   __shared__ double s_part[kWarps][9][kLD];
   __shared__ int32_t s_dst[kWarps][EPW * NUB];
   __shared__ int32_t s_pos[kWarps][32];
@@ -582,6 +583,16 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
 #pragma unroll
     for (int i = 0; i < 3; ++i) s_x[wib][g][3 * a + i] = pre.xa[i];
     if (a == 0) s_cls[wib][g] = pre.ce;
+    if constexpr (KV) {
+      double va[3] = {0, 0, 0};
+      if (valid) {
+        const int64_t I = A.conn[e * NEN + a];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) va[i] = A.v[3 * I + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) s_v[wib][g][3 * a + i] = va[i];
+    }
   }
   __syncwarp();
   // ---- phase A: two lanes per (element, q), each owning 5 of the 10 nodes
@@ -616,6 +627,28 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
       const double o = __shfl_xor_sync(0xffffffffu, F[r], 1);
       F[r] = hf ? o + F[r] : F[r] + o;
     }
+    double Fd[9];  // Kelvin-Voigt: Fdot = sum_a v_a (x) grad N_a (reading Q9)
+    if constexpr (KV) {
+#pragma unroll
+      for (int r = 0; r < 9; ++r) Fd[r] = 0.0;
+#pragma unroll
+      for (int bb = 0; bb < NEN / 2; ++bb) {
+        const int b = hf * (NEN / 2) + bb;
+        const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const double vi = s_v[wib][ge][3 * b + i];
+          Fd[3 * i] = fma(vi, n0, Fd[3 * i]);
+          Fd[3 * i + 1] = fma(vi, n1, Fd[3 * i + 1]);
+          Fd[3 * i + 2] = fma(vi, n2, Fd[3 * i + 2]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 9; ++r) {
+        const double o = __shfl_xor_sync(0xffffffffu, Fd[r], 1);
+        Fd[r] = hf ? o + Fd[r] : Fd[r] + o;
+      }
+    }
     if (act) {
       double* kq = s_k[wib][ge][q];
       if (hf == 0) {
@@ -625,6 +658,12 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
         for (int r = 0; r < 9; ++r) kq[r] = F[r];
 #pragma unroll
         for (int r = 0; r < 6; ++r) kq[9 + r] = S[r];
+        if constexpr (KV) {  // the force takes S + S_v; the tangent the elastic part only (reading Q8)
+          double Sv[6];
+          kv_S(F, Fd, mat.eta, mat.lamd, Sv);
+#pragma unroll
+          for (int r = 0; r < 6; ++r) kq[21 + r] = S[r] + Sv[r];
+        }
       } else {
 #pragma unroll
         for (int vv = 0; vv < 6; ++vv) {
@@ -667,9 +706,19 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
 #pragma unroll
       for (int I = 0; I < 3; ++I) tw[I] = w * (sget(S, I, 0) * gN[0] + sget(S, I, 1) * gN[1] + sget(S, I, 2) * gN[2]);
       if (pass == 0) {
+        if constexpr (KV) {
+          double tt[3];  // w (S + S_v) grad N_a
 #pragma unroll
-        for (int i = 0; i < 3; ++i)
-          fa[i] = fma(kq[3 * i], tw[0], fma(kq[3 * i + 1], tw[1], fma(kq[3 * i + 2], tw[2], fa[i])));
+          for (int I = 0; I < 3; ++I)
+            tt[I] = w * (kq[21 + vidx(I, 0)] * gN[0] + kq[21 + vidx(I, 1)] * gN[1] + kq[21 + vidx(I, 2)] * gN[2]);
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+            fa[i] = fma(kq[3 * i], tt[0], fma(kq[3 * i + 1], tt[1], fma(kq[3 * i + 2], tt[2], fa[i])));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+            fa[i] = fma(kq[3 * i], tw[0], fma(kq[3 * i + 1], tw[1], fma(kq[3 * i + 2], tw[2], fa[i])));
+        }
       }
       const double lw = mat.lam * w, mw = mat.mu * w;
       double gl[3], gm[3], gNm[3];
@@ -1502,7 +1551,7 @@ __device__ __forceinline__ void element_group_beam_svk(int64_t grp, const ElArgs
 template <int ELEM, int MODEL, int NPASS, bool KV, bool TAN, bool CLS>
 __host__ __device__ constexpr int el_minb_k() {
   return (ELEM == 0 && MODEL == 0 && !KV && !TAN)                         ? TLFEA_T10_FMINB
-         : (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && TAN && CLS)  ? TLFEA_T10_2PH_MINB
+         : (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && TAN && CLS)         ? TLFEA_T10_2PH_MINB
          : (TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV && TAN && CLS) ? TLFEA_ANCF_MINB
          : (TLFEA_BEAM_2PH && ELEM == 2 && MODEL == 0 && !KV && TAN && CLS) ? TLFEA_BEAM_MINB
                                                                             : el_minb<ELEM, MODEL, NPASS>();
@@ -1517,6 +1566,7 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
   constexpr bool A2PH = TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV && TAN && CLS;
   constexpr bool B2PH = TLFEA_BEAM_2PH && ELEM == 2 && MODEL == 0 && !KV && TAN && CLS;
   constexpr bool M2PH = TLFEA_MR_2PH && ELEM == 0 && MODEL == 1 && TAN;
+  constexpr bool V2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && KV && TAN && CLS;  // SVK + Kelvin-Voigt
   // A.cta_tiles consecutive tiles per CTA (class tables staged once)
   const int64_t t0 = (int64_t)blockIdx.x * A.cta_tiles;
   T10Pre pre;
@@ -1547,6 +1597,10 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
       element_group_ancf_svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
     } else if constexpr (B2PH) {
       element_group_beam_svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
+    } else if constexpr (V2PH) {
+      T10Pre pv;
+      t10_preload((t0 + k) * kWarps + (threadIdx.x >> 5), A, pv);
+      element_group_t10svk<NQ, true>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pv);
     } else if constexpr (M2PH) {
       if constexpr (!CLS) t10_stage_tables<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
       element_group_t10mr<NQ, KV>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, !CLS);
@@ -2124,10 +2178,10 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, 1>()) k_fuse
       if (!(P.dbg & 2)) {
 #pragma unroll 1
         for (int j = 0; j < P.etiles; ++j) {
-          if constexpr (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV) {
+          if constexpr (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0) {
             T10Pre pre;
             t10_preload((t0 + j) * kWarps + wib, P.el, pre);
-            element_group_t10svk<NQ>((t0 + j) * kWarps + wib, P.el, s_tab, pre);
+            element_group_t10svk<NQ, KV>((t0 + j) * kWarps + wib, P.el, s_tab, pre);
           } else if constexpr (TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV) {
             element_group_ancf_svk<NQ>((t0 + j) * kWarps + wib, P.el, s_tab);
           } else if constexpr (TLFEA_MR_2PH && ELEM == 0 && MODEL == 1) {
