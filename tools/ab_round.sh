@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
-for c in 3 2; do CFG=$c VAR=X VALS=0 bash tools/ab_env.sh; done
-NS="2" CFG=3 bash tools/multirank_flow.sh
+VAR=TLFEA_GATHER_HF VALS="0 1 0 1" bash tools/ab_env.sh
+CFG=2 VAR=TLFEA_GATHER_HF VALS="0 1" bash tools/ab_env.sh
