@@ -68,6 +68,17 @@ CASES = {
     "t10_100el_svk_keast5_ragged": lambda: (synth.Mesh(0, synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).X,
                                                        synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).conn[:100]),
                                             dict(synth.SVK_PAPER), 1),
+    # two-phase SVK + KV and MR (+ KV) groups on a tail inside a warp group,
+    # with classes and (perturbed) with staged per-element tables
+    "t10_100el_svk_kv_keast5": lambda: (synth.Mesh(0, synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).X,
+                                                   synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).conn[:100]),
+                                        dict(synth.SVK_PAPER, **synth.KV_TIRE), 1),
+    "t10_100el_mr_kv_keast5": lambda: (synth.Mesh(0, synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).X,
+                                                  synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).conn[:100]),
+                                       dict(synth.MR_PAPER, **synth.KV_TIRE), 1),
+    "t10_100el_perturbed_mr_kv_4pt": lambda: (synth.perturbed(synth.Mesh(0, synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).X,
+                                                                         synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).conn[:100])),
+                                              dict(synth.MR_PAPER, **synth.KV_TIRE), 0),
     "t10_4x3x2_perturbed_svk_kv_keast5": lambda: (synth.perturbed(synth.kuhn_t10_box(4, 3, 2, 0.8, 0.6, 0.4)),
                                                   dict(synth.SVK_PAPER, **synth.KV_TIRE), 1),
     "t10_3x3x2_perturbed_mr_4pt": lambda: (synth.perturbed(synth.kuhn_t10_box(3, 3, 2, 0.6, 0.6, 0.4)),
