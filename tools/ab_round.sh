@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
-VAR=TLFEA_UNIT_BANDS VALS="1 8 4 16" bash tools/ab_env.sh
+P=paper_2604_10357_b200
+LIBS="$P/libtlfea.so $P/libtlfea_bm.so $P/libtlfea.so $P/libtlfea_bm.so" TILES=1 bash tools/ab.sh
