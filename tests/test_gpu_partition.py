@@ -113,3 +113,38 @@ def test_virtual_partition_force_only_custom_part(torch_cuda):
         for i, I in enumerate(r["owned"]):
             f[3 * I:3 * I + 3] = r["f"][3 * i:3 * i + 3]
     assert rel(f, f0) <= TOL
+
+
+@pytest.mark.parametrize("case", ["t10_svk", "t10_mr_kv", "beam"])
+def test_virtual_partition_scattered_tangent(torch_cuda, case):
+    """A scattered element partition (element e on rank e % 3): many element
+    blocks have neither row owned by their rank, so they live only in the
+    extra scratch positions and reach their owners through the pack lists."""
+    if case == "t10_svk":
+        mesh, mat, rule = synth.kuhn_t10_box(4, 3, 2, 0.8, 0.6, 0.4), dict(synth.SVK_PAPER), 1
+    elif case == "t10_mr_kv":
+        mesh, mat, rule = synth.kuhn_t10_box(4, 3, 2, 0.8, 0.6, 0.4), dict(synth.MR_PAPER, **synth.KV_TIRE), 1
+    else:
+        mesh, mat, rule = synth.ancf_beam(24), dict(synth.SVK_PAPER), 3
+    P = 3
+    part = (np.arange(mesh.n_el) % P).astype(np.int32)
+    h = 1e-3
+    if mesh.element == 0:
+        x, v, vn, fext = synth.t10_state(mesh, with_fext=True)
+    else:
+        x, v, vn = synth.ancf_state(mesh)
+        fext = np.random.default_rng(3).normal(size=x.shape)
+    pr = oracle.Problem(mesh, mat, rule)
+    g0, H0, f0 = pr.eval(x, v, vn, fext, h)
+    res = run_partitioned(torch_cuda, mesh, mat, rule, P, x, v, vn, fext, h, part=part)
+    g = np.zeros_like(g0)
+    H = np.zeros_like(H0)
+    for r in res:
+        for i, I in enumerate(r["owned"]):
+            g[3 * I:3 * I + 3] = r["g"][3 * i:3 * i + 3]
+            for dd in range(3):
+                a0, a1 = r["rowptr"][3 * i + dd], r["rowptr"][3 * i + dd + 1]
+                b0, b1 = pr.rowptr[3 * I + dd], pr.rowptr[3 * I + dd + 1]
+                assert np.array_equal(r["cols"][a0:a1], pr.cols[b0:b1])
+                H[b0:b1] = r["H"][a0:a1]
+    assert rel(g, g0) <= TOL and rel(H, H0) <= TOL
