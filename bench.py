@@ -468,7 +468,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--hessian", choices=["full", "upper"], default="full",
                     help="H storage (full DOF CSR = the headline; upper = NEXT-4 variant)")
+    ap.add_argument("--tables", action="store_true",
+                    help="per-(e,q) reference tables in HBM (the paper's layout, as for a mesh of non-congruent "
+                         "elements) instead of the shared-memory geometry classes")
     args = ap.parse_args()
+    if args.tables:
+        os.environ["TLFEA_NO_CLASSES"] = "1"  # read by tlfea_setup
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
