@@ -541,13 +541,36 @@ __device__ __forceinline__ void t10_stage_tables(int64_t grp, const ElArgs& A, d
   __syncwarp();
 }
 
+// The same staging issued as cp.async (8-byte copies, no wait here): the
+// tables stream in while the lanes load their node coordinates; the group
+// waits (cp.async.wait_all) right before phase A.
+__device__ __forceinline__ void pf_cp8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+template <int NQ>
+__device__ __forceinline__ void t10_stage_tables_async(int64_t grp, const ElArgs& A, double* __restrict__ s_tab) {
+  constexpr int NEN = 10, EPW = 3, TABW = 3 * NEN + 1, PER = NQ * 3 * NEN;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t e0 = grp * EPW;
+  const int nv = (int)min((int64_t)EPW, A.n_el - e0);  // valid elements of the group
+  for (int t = lane; t < nv * PER; t += 32) {
+    const int g = t / PER, r = t - PER * g, q = r / (3 * NEN), c = r - 3 * NEN * q;
+    pf_cp8(&s_tab[((wib * EPW + g) * NQ + q) * TABW + c], A.gradN + (e0 + g) * PER + r);
+  }
+  if (lane < nv * NQ) {
+    const int g = lane / NQ, q = lane - NQ * g;
+    pf_cp8(&s_tab[((wib * EPW + g) * NQ + q) * TABW + 3 * NEN], A.J0w + (e0 + g) * NQ + q);
+  }
+}
+
 #ifndef TLFEA_T10_2PH_NPASS
 #define TLFEA_T10_2PH_NPASS 2  // config 3: 2 passes at 3 CTAs/SM (166 registers) 9.96 ms; 3 passes at 4 CTAs 10.72; 1 pass 12.97
 #endif
 #ifndef TLFEA_T10_2PH_MINB
 #define TLFEA_T10_2PH_MINB 3
 #endif
-template <int NQ, bool KV = false>
+template <int NQ, bool KV = false, bool TA = false>
 __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab,
                                                      const T10Pre& pre) {
   constexpr int NEN = 10, GROUP = 10, EPW = 3, NUB = 55, NB = 6, TABW = 3 * NEN + 1;
@@ -595,6 +618,10 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
     }
   }
   __syncwarp();
+  if constexpr (TA) {  // table mode: the staged per-element tables have landed
+    pf_wait();
+    __syncwarp();
+  }
   // ---- phase A: two lanes per (element, q), each owning 5 of the 10 nodes
   // (EPW * NQ * 2 = 30 lanes for Keast-5): partial F over its nodes, the halves
   // exchanged by one shuffle; lane h = 0 then stores F and S, lane h = 1 F F^T,
@@ -1056,7 +1083,7 @@ __device__ __forceinline__ void element_group_t10mr(int64_t grp, const ElArgs& A
 // folded in) once; phase B, one lane per (element, node a), contracts
 // f_a = sum_q (w P) grad N_a (Eq. fint_local). The lane-per-node kernel reduced
 // F and evaluated S on all 10 lanes of an element at every q.
-template <int NQ>
+template <int NQ, bool TA = false>
 __device__ __forceinline__ void element_group_t10svk_force(int64_t grp, const ElArgs& A,
                                                            const double* __restrict__ s_tab, const T10Pre& pre) {
   constexpr int NEN = 10, GROUP = 10, EPW = 3, TABW = 3 * NEN + 1;
@@ -1075,6 +1102,10 @@ __device__ __forceinline__ void element_group_t10svk_force(int64_t grp, const El
     if (a == 0) s_cls[wib][g] = pre.ce;
   }
   __syncwarp();
+  if constexpr (TA) {
+    pf_wait();
+    __syncwarp();
+  }
   if (lane < EPW * NQ) {
     const int ge = lane / NQ, q = lane - NQ * (lane / NQ);
     const double* t = s_tab + (s_cls[wib][ge] * NQ + q) * TABW;
@@ -1551,7 +1582,7 @@ __device__ __forceinline__ void element_group_beam_svk(int64_t grp, const ElArgs
 template <int ELEM, int MODEL, int NPASS, bool KV, bool TAN, bool CLS>
 __host__ __device__ constexpr int el_minb_k() {
   return (ELEM == 0 && MODEL == 0 && !KV && !TAN)                         ? TLFEA_T10_FMINB
-         : (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && TAN && CLS)         ? TLFEA_T10_2PH_MINB
+         : (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && TAN && (CLS || !KV)) ? TLFEA_T10_2PH_MINB
          : (TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV && TAN && CLS) ? TLFEA_ANCF_MINB
          : (TLFEA_BEAM_2PH && ELEM == 2 && MODEL == 0 && !KV && TAN && CLS) ? TLFEA_BEAM_MINB
                                                                             : el_minb<ELEM, MODEL, NPASS>();
@@ -1562,7 +1593,7 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
   extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
   // (SVK in table mode measured slower two-phase: config 3 without classes 13.97 vs 12.61 ms, force only
   // 1.20 vs 1.11 ms — staging the per-(e,q) tables serializes the group start; MR gains: 0.59 vs 0.71 ms)
-  constexpr bool T2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV && CLS;  // tangent or force only
+  constexpr bool T2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && !KV;  // tangent or force only
   constexpr bool A2PH = TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV && TAN && CLS;
   constexpr bool B2PH = TLFEA_BEAM_2PH && ELEM == 2 && MODEL == 0 && !KV && TAN && CLS;
   constexpr bool M2PH = TLFEA_MR_2PH && ELEM == 0 && MODEL == 1 && TAN;
@@ -1570,6 +1601,7 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
   // A.cta_tiles consecutive tiles per CTA (class tables staged once)
   const int64_t t0 = (int64_t)blockIdx.x * A.cta_tiles;
   T10Pre pre;
+  if constexpr (T2PH && !CLS) t10_stage_tables_async<NQ>(t0 * kWarps + (threadIdx.x >> 5), A, s_tab);
   if constexpr (T2PH) t10_preload(t0 * kWarps + (threadIdx.x >> 5), A, pre);
   if (CLS) {
     // all loads of a thread in flight at once (one L2 round trip, not one per element)
@@ -1588,11 +1620,15 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
 #pragma unroll 1
   for (int k = 0; k < A.cta_tiles; ++k) {
     if constexpr (T2PH) {
-      if (k > 0) t10_preload((t0 + k) * kWarps + (threadIdx.x >> 5), A, pre);
+      if (k > 0) {
+        if constexpr (!CLS) t10_stage_tables_async<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
+        t10_preload((t0 + k) * kWarps + (threadIdx.x >> 5), A, pre);
+      }
+      if constexpr (!CLS) pre.ce = (threadIdx.x >> 5) * 3 + (threadIdx.x & 31) / 10;  // staged slot
       if constexpr (TAN)
-        element_group_t10svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
+        element_group_t10svk<NQ, false, !CLS>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
       else
-        element_group_t10svk_force<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
+        element_group_t10svk_force<NQ, !CLS>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
     } else if constexpr (A2PH) {
       element_group_ancf_svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
     } else if constexpr (B2PH) {
@@ -2321,7 +2357,7 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
     k_element<ELEM, NQ, MODEL, KV, TAN, true, el_npass<ELEM, MODEL>()><<<g, kWarps * 32, smem, s>>>(A);
   } else {
     // the T10 two-phase groups stage each warp's element tables in dynamic shared memory
-    constexpr bool stage = ELEM == 0 && TLFEA_MR_2PH && MODEL == 1 && TAN;
+    constexpr bool stage = ELEM == 0 && ((TLFEA_MR_2PH && MODEL == 1 && TAN) || (TLFEA_T10_2PH && MODEL == 0 && !KV));
     const size_t smem = stage ? sizeof(double) * kWarps * G::EPW * NQ * (G::NEN * 3 + 1) : 0;
     static size_t smem_set = 0;
     if (smem > smem_set) {

@@ -79,6 +79,9 @@ CASES = {
     "t10_100el_perturbed_mr_kv_4pt": lambda: (synth.perturbed(synth.Mesh(0, synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).X,
                                                                          synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).conn[:100])),
                                               dict(synth.MR_PAPER, **synth.KV_TIRE), 0),
+    "t10_100el_perturbed_svk_keast5": lambda: (synth.perturbed(synth.Mesh(0, synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).X,
+                                                                          synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).conn[:100])),
+                                               dict(synth.SVK_PAPER), 1),
     "t10_4x3x2_perturbed_svk_kv_keast5": lambda: (synth.perturbed(synth.kuhn_t10_box(4, 3, 2, 0.8, 0.6, 0.4)),
                                                   dict(synth.SVK_PAPER, **synth.KV_TIRE), 1),
     "t10_3x3x2_perturbed_mr_4pt": lambda: (synth.perturbed(synth.kuhn_t10_box(3, 3, 2, 0.6, 0.6, 0.4)),
@@ -145,7 +148,8 @@ def test_setup_exports(torch_cuda, case):
     assert rel(fff.cpu().numpy(), pr.fff) <= 1e-13
 
 
-@pytest.mark.parametrize("case", ["cfg1_svk_4pt", "t10_4x3x2_mr_kv_keast5", "ancf_3x3_svk", "beam_16_svk"])
+@pytest.mark.parametrize("case", ["cfg1_svk_4pt", "t10_4x3x2_mr_kv_keast5", "ancf_3x3_svk", "beam_16_svk",
+                                  "t10_100el_perturbed_svk_keast5"])
 def test_force_only_and_split_stages(torch_cuda, case):
     torch = torch_cuda
     mesh, mat, rule = CASES[case]()
