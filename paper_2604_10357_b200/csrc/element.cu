@@ -1560,6 +1560,9 @@ __device__ __forceinline__ void element_group_beam_svk(int64_t grp, const ElArgs
   }
 }
 
+#ifndef TLFEA_MR_MINB
+#define TLFEA_MR_MINB 2  // config 2: 0.509 ms at 2 CTAs/SM (248 registers); 3 CTAs spill 380 B, 0.575 ms
+#endif
 #ifndef TLFEA_MR_2PH
 #define TLFEA_MR_2PH 1  // T10 Mooney-Rivlin (+KV) class-mode tangent eval through element_group_t10mr
 #endif
@@ -1585,6 +1588,7 @@ __host__ __device__ constexpr int el_minb_k() {
          : (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && TAN && (CLS || !KV)) ? TLFEA_T10_2PH_MINB
          : (TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV && TAN && CLS) ? TLFEA_ANCF_MINB
          : (TLFEA_BEAM_2PH && ELEM == 2 && MODEL == 0 && !KV && TAN && CLS) ? TLFEA_BEAM_MINB
+         : (TLFEA_MR_2PH && ELEM == 0 && MODEL == 1 && TAN)                 ? TLFEA_MR_MINB
                                                                             : el_minb<ELEM, MODEL, NPASS>();
 }
 
