@@ -30,6 +30,10 @@ static inline unsigned grid_for(int64_t n, int block) {
 // dependent index -> value loads of the mass row have 3x the parallelism;
 // the three threads of a node share its row through L1.
 // mode: 0 full (f + residual), 1 f only, 2 residual from fpart_in.
+#ifndef TLFEA_FG_BLOCK
+#define TLFEA_FG_BLOCK 128  // config 3: 1.189 ms (128) vs 1.208 (256), 1.237 (512), 1.198 (64)
+#endif
+constexpr int kFgBlock = TLFEA_FG_BLOCK;
 __global__ void k_gather_f_dof(FArgs A) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t < 3 * A.n_own) gather_f_dof_one(t, A);
@@ -227,7 +231,7 @@ tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, cons
                              double* g, double* fint, bool partial_only, cudaStream_t s) {
   if (c->n_own == 0) return TLFEA_OK;
   if (c->fdest) {
-    k_gather_f_dof<<<grid_for(3 * c->n_own, 256), 256, 0, s>>>(
+    k_gather_f_dof<<<grid_for(3 * c->n_own, kFgBlock), kFgBlock, 0, s>>>(
         f_args(c, c->fscr, nullptr, v, vn, fext, h, partial_only ? 1 : 0, g, fint));
     TL_CHECK_LAUNCH();
     return TLFEA_OK;
@@ -412,7 +416,7 @@ tlfea_status launch_residual(Context* c, const double* fint, const double* v, co
                              const double* fext, double h, double* g, cudaStream_t s) {
   if (c->n_own == 0) return TLFEA_OK;
   if (g) {
-    k_gather_f_dof<<<grid_for(3 * c->n_own, 256), 256, 0, s>>>(
+    k_gather_f_dof<<<grid_for(3 * c->n_own, kFgBlock), kFgBlock, 0, s>>>(
         f_args(c, c->fscr, fint, v, vn, fext, h, 2, g, nullptr));
     TL_CHECK_LAUNCH();
     return TLFEA_OK;
