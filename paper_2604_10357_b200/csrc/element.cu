@@ -1156,7 +1156,7 @@ __device__ __forceinline__ void element_group_t10svk_force(int64_t grp, const El
 #define TLFEA_ANCF_NPASS 1  // block passes (each re-runs phase A per chunk)
 #endif
 #ifndef TLFEA_ANCF_MINB
-#define TLFEA_ANCF_MINB 2
+#define TLFEA_ANCF_MINB 3  // config 4: 1.312 ms at 3 CTAs/SM (168 registers, 28 B spill) vs 1.347 at 2
 #endif
 // ANCF3443 plate element (16 coefficients, GL 4x4x3 = 48 points), SVK, no KV,
 // geometry classes: the two-phase scheme of element_group_t10svk with one
