@@ -287,7 +287,7 @@ def run_ours(args):
     kv = cfg.material.get("eta_damp", 0) > 0 or cfg.material.get("lambda_damp", 0) > 0
     t_setup = time.perf_counter()
     ctx = T.Context.from_mesh(mesh, cfg.material, cfg.quadrature, rank=rank, nranks=world, device=local,
-                              hessian=args.hessian)
+                              hessian=args.hessian, reference_layout="tables" if args.tables else "auto")
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
     info = ctx.info
@@ -472,8 +472,6 @@ def main():
                     help="per-(e,q) reference tables in HBM (the paper's layout, as for a mesh of non-congruent "
                          "elements) instead of the shared-memory geometry classes")
     args = ap.parse_args()
-    if args.tables:
-        os.environ["TLFEA_NO_CLASSES"] = "1"  # read by tlfea_setup
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -155,6 +155,12 @@ typedef struct {
                              (entries with col >= row only, rows in order, the
                              cuDSS-facing matrix view).
                              UPPER: single rank, no constraints. */
+  int32_t reference_layout; /* 0 (default): geometry classes when every element
+                             is congruent to one of <= 32 (T10) / 4 (ANCF)
+                             reference shapes, else the per-(e,q) tables of
+                             §4.1; 1: the per-(e,q) tables always
+                             (the paper's layout, on any mesh). Results are
+                             the same either way (to rounding). */
 } tlfea_options;
 
 /* Sizes of a context (tlfea_info). Rows/DOFs are GLOBAL indices; in a
@@ -176,12 +182,9 @@ typedef struct {
   int32_t n_geometry_classes; /* > 0: congruent elements share reference
                                  tables (staged in shared memory); 0: the
                                  per-(e,q) tables of §4.1 are read from HBM */
-  int32_t fused_eval;      /* 1: tlfea_eval runs as ONE persistent kernel
-                              (element tiles + dependency-ordered H and f/g
-                              gather items, results bitwise equal to the
-                              three-kernel path); 0: three kernels. Opt-in
-                              (TLFEA_FUSED=1 in the environment at setup) for
-                              single-rank contexts with geometry classes. */
+  int32_t fused_eval;      /* 1: tlfea_eval runs the whole eval in one
+                              kernel (no tangent scratch); 0: element kernel
+                              + H gather + f/g gather. */
   int64_t n_constraints;   /* rows m of the context's constraint set (0: none) */
 } tlfea_info_t;
 

@@ -58,7 +58,8 @@ class Options(C.Structure):
     _fields_ = [("quadrature", C.c_int32), ("mass_rule", C.c_int32), ("gravity", C.c_double * 3),
                 ("ancf_dims", C.c_double * 3), ("rank", C.c_int32), ("nranks", C.c_int32),
                 ("elem_part", C.POINTER(C.c_int32)), ("device", C.c_int32),
-                ("constraints", C.POINTER(Constraints)), ("hessian_upper", C.c_int32)]
+                ("constraints", C.POINTER(Constraints)), ("hessian_upper", C.c_int32),
+                ("reference_layout", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -207,12 +208,16 @@ class Context:
     def __init__(self, element: int, conn: np.ndarray, X: np.ndarray, mat: dict, quadrature: int,
                  dims: np.ndarray | None = None, mass_rule: int = 0, gravity=(0.0, 0.0, 0.0),
                  rank: int = 0, nranks: int = 1, elem_part=None, device: int = 0, constraints: dict | None = None,
-                 hessian: str = "full"):
+                 hessian: str = "full", reference_layout: str = "auto"):
         """constraints: dict rowptr, cols (DOF ids), vals, b of c(q) = C q - b
         (tlfea_constraints; NEXT-3). hessian: "full" or "upper" storage of H
-        (options.hessian_upper; NEXT-4)."""
+        (options.hessian_upper; NEXT-4). reference_layout: "auto" (geometry
+        classes when the mesh allows) or "tables" (the paper's per-(e,q)
+        tables always; options.reference_layout)."""
         if hessian not in ("full", "upper"):
             raise ValueError("hessian must be 'full' or 'upper'")
+        if reference_layout not in ("auto", "tables"):
+            raise ValueError("reference_layout must be 'auto' or 'tables'")
         L = lib()
         con = None
         if constraints is not None:
@@ -231,7 +236,8 @@ class Context:
                     None if self._dims is None else self._dims.ctypes.data_as(C.POINTER(C.c_double)))
         opts = Options(quadrature, mass_rule, (C.c_double * 3)(*gravity), (C.c_double * 3)(0, 0, 0), rank, nranks,
                        None if self._part is None else self._part.ctypes.data_as(C.POINTER(C.c_int32)), device,
-                       None if con is None else C.pointer(con), 1 if hessian == "upper" else 0)
+                       None if con is None else C.pointer(con), 1 if hessian == "upper" else 0,
+                       1 if reference_layout == "tables" else 0)
         self.material = dict(mat)
         m = make_material(mat)
         h = C.c_void_p()
@@ -270,6 +276,26 @@ class Context:
     def _torch(self):
         import torch
         return torch
+
+    @property
+    def n_dof(self):
+        return 3 * self.info["n_coef"]
+
+    def _d(self, t, n, name):
+        """Device pointer of a contiguous float64 CUDA tensor with >= n values
+        on this context's device (argument checks only; None passes through)."""
+        if t is None:
+            return None
+        torch = self._torch()
+        if not isinstance(t, torch.Tensor) or t.device.type != "cuda" or t.device.index != self.device:
+            raise ValueError(f"{name}: expected a CUDA tensor on cuda:{self.device}")
+        if t.dtype != torch.float64:
+            raise ValueError(f"{name}: expected float64, got {t.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name}: must be contiguous")
+        if t.numel() < n:
+            raise ValueError(f"{name}: {t.numel()} values, {n} required")
+        return C.c_void_p(t.data_ptr())
 
     def empty_outputs(self):
         torch = self._torch()
@@ -318,6 +344,10 @@ class Context:
         return M, fff
 
     # -- evaluation
+    def _eval_ptrs(self, x, v, v_n, f_ext):
+        n = self.n_dof
+        return self._d(x, n, "x"), self._d(v, n, "v"), self._d(v_n, n, "v_n"), self._d(f_ext, n, "f_ext")
+
     def eval(self, x, v, v_n=None, f_ext=None, h=1e-3, g=None, H=None, f_int=None, stream=None, lam=None,
              rho=None):
         """tlfea_eval, or tlfea_eval_constrained when lam / rho are given."""
@@ -326,12 +356,14 @@ class Context:
             g = g0 if g is None else g
             H = H0 if H is None else H
         if lam is None and rho is None:
-            _check(lib().tlfea_eval(self.handle, _ptr(x), _ptr(v), _ptr(v_n), _ptr(f_ext), float(h), _ptr(g),
-                                    _ptr(H), _ptr(f_int), _stream(stream)))
+            _check(lib().tlfea_eval(self.handle, *self._eval_ptrs(x, v, v_n, f_ext), float(h),
+                                    self._d(g, 3 * self.n_own, "g"), self._d(H, self.nnz, "H"),
+                                    self._d(f_int, 3 * self.n_own, "f_int"), _stream(stream)))
         else:
-            _check(lib().tlfea_eval_constrained(self.handle, _ptr(x), _ptr(v), _ptr(v_n), _ptr(f_ext), float(h),
-                                                _ptr(lam), float(rho or 0.0), _ptr(g), _ptr(H), _ptr(f_int),
-                                                _stream(stream)))
+            _check(lib().tlfea_eval_constrained(self.handle, *self._eval_ptrs(x, v, v_n, f_ext), float(h),
+                                                self._d(lam, self.info["n_constraints"], "lam"), float(rho or 0.0),
+                                                self._d(g, 3 * self.n_own, "g"), self._d(H, self.nnz, "H"),
+                                                self._d(f_int, 3 * self.n_own, "f_int"), _stream(stream)))
         return g, H, f_int
 
     def constraint_residual(self, q, c=None, stream=None):
@@ -350,7 +382,8 @@ class Context:
     def force_only(self, x, v=None, f_int=None, stream=None):
         if f_int is None:
             f_int = self.empty_outputs()[2]
-        _check(lib().tlfea_force_only(self.handle, _ptr(x), _ptr(v), _ptr(f_int), _stream(stream)))
+        _check(lib().tlfea_force_only(self.handle, self._d(x, self.n_dof, "x"), self._d(v, self.n_dof, "v"),
+                                      self._d(f_int, 3 * self.n_own, "f_int"), _stream(stream)))
         return f_int
 
     def adamw_iteration(self, q_n, v_n, f_ext, h, l, params, v, m, s, g, q=None, f_int=None, norms=None,
@@ -366,9 +399,13 @@ class Context:
         if norms is None:
             norms = torch.empty(2, dtype=torch.float64, device=v.device)
         p = AdamWParams(*(float(params[k]) for k in ("alpha", "beta1", "beta2", "eps", "weight_decay")))
-        _check(lib().tlfea_adamw_iteration(self.handle, _ptr(q_n), _ptr(v_n), _ptr(f_ext), float(h), int(l),
-                                           C.byref(p), _ptr(lam), float(rho), _ptr(v), _ptr(m), _ptr(s), _ptr(g),
-                                           _ptr(q), _ptr(f_int), _ptr(norms), _stream(stream)))
+        n = self.n_dof
+        d = self._d
+        _check(lib().tlfea_adamw_iteration(self.handle, d(q_n, n, "q_n"), d(v_n, n, "v_n"), d(f_ext, n, "f_ext"),
+                                           float(h), int(l), C.byref(p), d(lam, self.info["n_constraints"], "lam"),
+                                           float(rho), d(v, n, "v"), d(m, n, "m"), d(s, n, "s"), d(g, n, "g"),
+                                           d(q, n, "q"), d(f_int, n, "f_int"), d(norms, 2, "norms"),
+                                           _stream(stream)))
         return q, norms
 
     def eval_host(self, x, v, v_n=None, f_ext=None, h=1e-3, g=None, H=None, f_int=None, stream=None):
@@ -382,26 +419,32 @@ class Context:
         i = self.info
         if P is None:
             P = torch.empty((i["n_elements"], i["n_qp"], 9), dtype=torch.float64, device=x.device)
-        _check(lib().tlfea_compute_stress(self.handle, _ptr(x), _ptr(v), _ptr(P), _stream(stream)))
+        _check(lib().tlfea_compute_stress(self.handle, self._d(x, self.n_dof, "x"), self._d(v, self.n_dof, "v"),
+                                          self._d(P, i["n_elements"] * i["n_qp"] * 9, "P"), _stream(stream)))
         return P
 
     def internal_force_from_stress(self, P, f_int=None, stream=None):
         if f_int is None:
             f_int = self.empty_outputs()[2]
-        _check(lib().tlfea_internal_force_from_stress(self.handle, _ptr(P), _ptr(f_int), _stream(stream)))
+        i = self.info
+        _check(lib().tlfea_internal_force_from_stress(self.handle, self._d(P, i["n_elements"] * i["n_qp"] * 9, "P"),
+                                                      self._d(f_int, 3 * self.n_own, "f_int"), _stream(stream)))
         return f_int
 
     def compute_gradient(self, f_int, v, v_n=None, f_ext=None, h=1e-3, g=None, stream=None):
         if g is None:
             g = self.empty_outputs()[0]
-        _check(lib().tlfea_compute_gradient(self.handle, _ptr(f_int), _ptr(v), _ptr(v_n), _ptr(f_ext), float(h),
-                                            _ptr(g), _stream(stream)))
+        n = self.n_dof
+        _check(lib().tlfea_compute_gradient(self.handle, self._d(f_int, 3 * self.n_own, "f_int"),
+                                            self._d(v, n, "v"), self._d(v_n, n, "v_n"), self._d(f_ext, n, "f_ext"),
+                                            float(h), self._d(g, 3 * self.n_own, "g"), _stream(stream)))
         return g
 
     def assemble_hessian(self, x, h=1e-3, H=None, stream=None):
         if H is None:
             H = self.empty_outputs()[1]
-        _check(lib().tlfea_assemble_hessian(self.handle, _ptr(x), float(h), _ptr(H), _stream(stream)))
+        _check(lib().tlfea_assemble_hessian(self.handle, self._d(x, self.n_dof, "x"), float(h),
+                                            self._d(H, self.nnz, "H"), _stream(stream)))
         return H
 
     def exchange_sizes(self):
@@ -412,12 +455,19 @@ class Context:
         return s, r
 
     def eval_begin(self, x, v, h, H, send_buf, force_only=False, stream=None):
-        _check(lib().tlfea_eval_begin(self.handle, _ptr(x), _ptr(v), int(force_only), float(h), _ptr(H),
-                                      _ptr(send_buf), _stream(stream)))
+        n = self.n_dof
+        _check(lib().tlfea_eval_begin(self.handle, self._d(x, n, "x"), self._d(v, n, "v"), int(force_only), float(h),
+                                      self._d(H, 0 if force_only else self.nnz, "H"),
+                                      self._d(send_buf, int(self.exchange_sizes()[0].sum()), "send_buf"),
+                                      _stream(stream)))
 
     def eval_finish(self, recv_buf, v, v_n, f_ext, h, g, H, f_int=None, force_only=False, stream=None):
-        _check(lib().tlfea_eval_finish(self.handle, _ptr(recv_buf), _ptr(v), _ptr(v_n), _ptr(f_ext), float(h),
-                                       int(force_only), _ptr(g), _ptr(H), _ptr(f_int), _stream(stream)))
+        n, no = self.n_dof, 3 * self.n_own
+        _check(lib().tlfea_eval_finish(self.handle, self._d(recv_buf, int(self.exchange_sizes()[1].sum()), "recv_buf"),
+                                       self._d(v, n, "v"), self._d(v_n, n, "v_n"), self._d(f_ext, n, "f_ext"),
+                                       float(h), int(force_only), self._d(g, no, "g"),
+                                       self._d(H, 0 if force_only else self.nnz, "H"), self._d(f_int, no, "f_int"),
+                                       _stream(stream)))
 
     def set_timing(self, enable: bool):
         _check(lib().tlfea_set_timing(self.handle, int(enable)))

@@ -15,6 +15,9 @@ namespace tlfea {
 void set_error(const std::string& msg);
 tlfea_status fail(tlfea_status st, const std::string& msg);
 void count_launch(int n = 1);
+// Opt-in dynamic shared memory above 48 KB is a per-device, per-kernel
+// attribute: applied once per (kernel, current device), thread-safe.
+tlfea_status ensure_dynamic_smem(const void* kernel, size_t bytes);
 
 #define TL_CUDA(call)                                                          \
   do {                                                                         \
@@ -79,7 +82,6 @@ struct MatDev {
   double C10, C01, kappa;
   double eta, lamd;
   double rho0;
-  int dbg_nowrite;  // diagnostics only: skip the tangent scratch stores (TLFEA_DBG_NOKWRITE=1)
 };
 
 // Device buffer helper (raw cudaMalloc, owned by the context)
@@ -101,6 +103,7 @@ struct Context {
   int64_t n_own = 0;           // owned coefficient rows
   int64_t nnz_c = 0;           // owned-row coefficient nnz
   int affine = 0;
+  int force_tables = 0;         // options.reference_layout = 1: never use geometry classes
   // H storage: full DOF CSR (9 nnz_c values) or UPPER (col >= row). UPPER row
   // 3I+d starts at ubase[I] + d (3 + 3 L_I) - d (d - 1) / 2, L_I = blocks
   // J > I of coefficient row I; block (I, J) with rank k among J >= I (k = 0:
@@ -150,16 +153,6 @@ struct Context {
   int32_t* u_offT = nullptr;      // [n_units] H offset of (J,I) or -1
   int32_t* u_deg = nullptr;       // [n_units] deg(I) | deg(J) << 16
   double* u_m = nullptr;          // [n_units] M_IJ
-  // fused persistent eval (single rank, class tables, gather-sorted scratch):
-  // one launch works through a list of element items (kElTile elements x
-  // fz_etiles) and H / f gather items, each gather item waiting on per-chunk
-  // completion counters of the element chunks it reads (setup.cu build_fused_plan)
-  int64_t fz_items = 0, fz_nE = 0, fz_nG = 0, fz_nF = 0;
-  int fz_chunks = 0, fz_etiles = 0, fz_chunk_items = 0, fz_gunits = 0, fz_fdofs = 0;
-  uint32_t* fz_list = nullptr;    // [fz_items] type << 30 | index (0 element, 1 H gather, 2 f gather)
-  int32_t* fz_lo = nullptr;       // [fz_nG + fz_nF] first element chunk read by a gather item
-  int32_t* fz_hi = nullptr;       // [fz_nG + fz_nF] last element chunk read
-  uint32_t* fz_sync = nullptr;    // [1 + fz_chunks]: work ticket, completed element items per chunk
   double* Kscr = nullptr;         // [n_el][n_ublk][9]
   double* fscr = nullptr;         // [n_el][nen][3]
   unsigned long long* err_flag = nullptr;  // min over (e*64+q) with det F <= 0 (MR)
@@ -239,11 +232,6 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
 tlfea_status launch_element_kernel(Context* c, const double* x, const double* v,
                                    bool tangent, cudaStream_t s);
 tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s);
-// fused element + H + f/g eval (one persistent launch); returns TLFEA_E_INVALID
-// without launching when the context has no fused plan
-bool fused_available(const Context* c);
-tlfea_status launch_fused_eval(Context* c, const double* x, const double* v, const double* vn, const double* fext,
-                               double h, double* g, double* H, double* fint, cudaStream_t s);
 tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, const double* fext,
                              double h, double* g, double* fint, bool partial_only,
                              cudaStream_t s);

@@ -128,7 +128,6 @@ struct ElArgs {
   const int32_t* dest;
   const int32_t* fdest;
   unsigned long long* err;
-  int cta_tiles;  // k_element: consecutive tiles per CTA
 };
 
 __device__ __forceinline__ void pf_cp4(void* smem, const void* gmem) {
@@ -184,7 +183,7 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
   // (SVK only: the Mooney-Rivlin tables already fill the 48 KB of static shared memory)
   constexpr bool DAX = DA && TAN && MODEL == 0;
   __shared__ int32_t s_dst[kWarps][DAX ? EPW * NUB : 1];
-  if (DAX && dest && !mat.dbg_nowrite) {
+  if (DAX && dest) {
     const int64_t e0 = grp * EPW, lim = (n_el - e0) * NUB;
     for (int t = lane; t < EPW * NUB; t += 32)
       if (t < lim) pf_cp4(&s_dst[wib][t], dest + e0 * NUB + t);
@@ -435,7 +434,7 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
   // block per lane (already in the orientation its receiver needs) in shared
   // memory and the warp writes the round's blocks as consecutive doubles, so a
   // warp store covers 3-4 whole blocks.
-  if (TAN && !mat.dbg_nowrite) {
+  if (TAN) {
     __shared__ int32_t s_pos[kWarps][32];  // block position (< 2^31, checked at setup)
     // store mapping: lane = 9 bi + r writes entry r of block 3 it + bi
     constexpr int NLB = MULTI ? EPW * GROUP : 32;  // lanes holding blocks
@@ -515,7 +514,7 @@ __device__ __forceinline__ void t10_preload(int64_t grp, const ElArgs& A, T10Pre
     const int64_t I = A.conn[e * 10 + a];
 #pragma unroll
     for (int i = 0; i < 3; ++i) p.xa[i] = A.x[3 * I + i];
-    if (a == 0) p.ce = A.cls[e];
+    if (a == 0 && A.cls) p.ce = A.cls[e];
   }
 }
 
@@ -596,7 +595,7 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
   const int64_t e = grp * EPW + g;
   const bool valid = lane_active && e < n_el;
   const int gbase = g * GROUP;
-  const bool write = dest && !mat.dbg_nowrite;
+  const bool write = dest;
   if (write) {
     const int64_t e0 = grp * EPW, lim = (n_el - e0) * NUB;
     for (int t = lane; t < EPW * NUB; t += 32)
@@ -785,7 +784,7 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
       fo[1] = fa[1];
       fo[2] = fa[2];
     }
-    if (!mat.dbg_nowrite) {
+    {
       // warp-staged block stores, as in element_group
       constexpr int NLB = EPW * GROUP, NIT = (NLB + 2) / 3;
       const int bi = lane / 9, rr = lane - 9 * (lane / 9);
@@ -864,7 +863,7 @@ __device__ __forceinline__ void element_group_t10mr(int64_t grp, const ElArgs& A
   const int64_t e = grp * EPW + g;
   const bool valid = lane_active && e < n_el;
   const int gbase = g * GROUP;
-  const bool write = dest && !mat.dbg_nowrite;
+  const bool write = dest;
   if (write) {
     const int64_t e0 = grp * EPW, lim = (n_el - e0) * NUB;
     for (int t = lane; t < EPW * NUB; t += 32)
@@ -1037,7 +1036,6 @@ __device__ __forceinline__ void element_group_t10mr(int64_t grp, const ElArgs& A
     fo[1] = fa[1];
     fo[2] = fa[2];
   }
-  if (mat.dbg_nowrite) return;
   // warp-staged block stores (staging in s_node rows 0..8)
   constexpr int NLB = EPW * GROUP, NIT = (NLB + 2) / 3;
   const int bi = lane / 9, rr = lane - 9 * (lane / 9);
@@ -1186,7 +1184,7 @@ __device__ __forceinline__ void element_group_ancf_svk(int64_t e, const ElArgs& 
   const int a = lane & 15, half = lane >> 4;
   const bool valid = e < n_el;
   if (!valid) return;  // warp-uniform (one element per warp)
-  const bool write = dest && !mat.dbg_nowrite;
+  const bool write = dest;
   if (write) {
     for (int t = lane; t < NUB; t += 32) pf_cp4(&s_dst[wib][t], dest + e * NUB + t);
   }
@@ -1322,7 +1320,6 @@ __device__ __forceinline__ void element_group_ancf_svk(int64_t e, const ElArgs& 
     fo[1] = fa[1];
     fo[2] = fa[2];
   }
-  if (mat.dbg_nowrite) continue;
   // warp-staged block stores, as in element_group
   constexpr int NLB = 32, NIT = (NLB + 2) / 3;
   const int bi = lane / 9, rr = lane - 9 * (lane / 9);
@@ -1385,7 +1382,7 @@ __device__ __forceinline__ void element_group_beam_svk(int64_t grp, const ElArgs
   const int g = lane / GROUP, a = lane % GROUP, gbase = g * GROUP;
   const int64_t e = grp * EPW + g;
   const bool valid = e < n_el;
-  const bool write = dest && !mat.dbg_nowrite;
+  const bool write = dest;
   if (write) {
     const int64_t e0 = grp * EPW, lim = (n_el - e0) * NUB;
     for (int t = lane; t < EPW * NUB; t += 32)
@@ -1520,7 +1517,6 @@ __device__ __forceinline__ void element_group_beam_svk(int64_t grp, const ElArgs
     fo[1] = fa[1];
     fo[2] = fa[2];
   }
-  if (mat.dbg_nowrite) return;
   constexpr int NLB = 32, NIT = (NLB + 2) / 3;
   const int bi = lane / 9, rr = lane - 9 * (lane / 9);
   if (write) {
@@ -1602,11 +1598,10 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
   constexpr bool B2PH = TLFEA_BEAM_2PH && ELEM == 2 && MODEL == 0 && !KV && TAN && CLS;
   constexpr bool M2PH = TLFEA_MR_2PH && ELEM == 0 && MODEL == 1 && TAN;
   constexpr bool V2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && KV && TAN && CLS;  // SVK + Kelvin-Voigt
-  // A.cta_tiles consecutive tiles per CTA (class tables staged once)
-  const int64_t t0 = (int64_t)blockIdx.x * A.cta_tiles;
+  const int64_t grp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);  // this warp's element group
   T10Pre pre;
-  if constexpr (T2PH && !CLS) t10_stage_tables_async<NQ>(t0 * kWarps + (threadIdx.x >> 5), A, s_tab);
-  if constexpr (T2PH) t10_preload(t0 * kWarps + (threadIdx.x >> 5), A, pre);
+  if constexpr (T2PH && !CLS) t10_stage_tables_async<NQ>(grp, A, s_tab);
+  if constexpr (T2PH) t10_preload(grp, A, pre);
   if (CLS) {
     // all loads of a thread in flight at once (one L2 round trip, not one per element)
     const int tot = A.n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1);
@@ -1621,370 +1616,29 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
     }
     __syncthreads();
   }
-#pragma unroll 1
-  for (int k = 0; k < A.cta_tiles; ++k) {
-    if constexpr (T2PH) {
-      if (k > 0) {
-        if constexpr (!CLS) t10_stage_tables_async<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
-        t10_preload((t0 + k) * kWarps + (threadIdx.x >> 5), A, pre);
-      }
-      if constexpr (!CLS) pre.ce = (threadIdx.x >> 5) * 3 + (threadIdx.x & 31) / 10;  // staged slot
-      if constexpr (TAN)
-        element_group_t10svk<NQ, false, !CLS>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
-      else
-        element_group_t10svk_force<NQ, !CLS>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pre);
-    } else if constexpr (A2PH) {
-      element_group_ancf_svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
-    } else if constexpr (B2PH) {
-      element_group_beam_svk<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
-    } else if constexpr (V2PH) {
-      T10Pre pv;
-      t10_preload((t0 + k) * kWarps + (threadIdx.x >> 5), A, pv);
-      element_group_t10svk<NQ, true>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, pv);
-    } else if constexpr (M2PH) {
-      if constexpr (!CLS) t10_stage_tables<NQ>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
-      element_group_t10mr<NQ, KV>((t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab, !CLS);
-    } else
-      element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, TLFEA_DEST_ASYNC != 0>(
-          (t0 + k) * kWarps + (threadIdx.x >> 5), A, s_tab);
-  }
+  if constexpr (T2PH) {
+    if constexpr (!CLS) pre.ce = (threadIdx.x >> 5) * 3 + (threadIdx.x & 31) / 10;  // staged slot
+    if constexpr (TAN)
+      element_group_t10svk<NQ, false, !CLS>(grp, A, s_tab, pre);
+    else
+      element_group_t10svk_force<NQ, !CLS>(grp, A, s_tab, pre);
+  } else if constexpr (A2PH) {
+    element_group_ancf_svk<NQ>(grp, A, s_tab);
+  } else if constexpr (B2PH) {
+    element_group_beam_svk<NQ>(grp, A, s_tab);
+  } else if constexpr (V2PH) {
+    T10Pre pv;
+    t10_preload(grp, A, pv);
+    element_group_t10svk<NQ, true>(grp, A, s_tab, pv);
+  } else if constexpr (M2PH) {
+    if constexpr (!CLS) t10_stage_tables<NQ>(grp, A, s_tab);
+    element_group_t10mr<NQ, KV>(grp, A, s_tab, !CLS);
+  } else
+    element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, TLFEA_DEST_ASYNC != 0>(grp, A, s_tab);
 }
 
-
-// ------------------------------------------------ FP64 tensor-core variant
-// T10 + SVK + congruent-element classes. The element tangent is split as
-//   K_ab = lam G_ab + mu G_ab^T + D_ab + sigma_ab I,
-//   G = sum_q w_q g(q) g(q)^T          (30x30 Gram of g_(a,i) = (F grad N_a)_i)
-//   D_ab = sum_q mu w_q d_ab(q) F F^T,  sigma_ab = sum_q w_q grad N_a . S grad N_b
-// (Eq. tangent_block P:527-534 for A = dP/dF of SVK, reading Q5). G — 55 % of
-// the flops — is a dense GEMM per element (M = N = 30 -> 32, K = n_qp -> 8):
-// 10 upper 8x8 tiles x 2 k-steps of mma.sync.m8n8k4.f64 (DMMA) per element.
-// D and sigma accumulate per q in the owner-lane layout of k_element; the
-// Gram blocks meet them through a compact shared-memory block store.
-constexpr int kTCWarps = 4;
-
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
-
-template <int NQ, bool KV>
-__global__ void __launch_bounds__(kTCWarps * 32, 2)
-    k_t10_tc(int64_t n_el, const int32_t* __restrict__ conn, const uint8_t* __restrict__ cls,
-             const double* __restrict__ cls_tab, int n_cls, const double* __restrict__ x,
-             const double* __restrict__ v, MatDev mat, double* __restrict__ fscr, double* __restrict__ Kscr,
-             const int32_t* __restrict__ dest, const int32_t* __restrict__ fdest) {
-  constexpr int NEN = 10, GROUP = 10, EPW = 3, NUB = 55, NB = 6;
-  constexpr int NC = KV ? 18 : 9;
-  constexpr int TABW = NEN * 3 + 1;
-  static_assert(NQ <= 8, "k-dimension holds at most 8 quadrature points");
-  __shared__ double s_part[kTCWarps][NC][kLD];
-  __shared__ double s_F[kTCWarps][EPW][NC];
-  // dynamic shared memory: [class tables][G operand][compact Gram blocks]
-  extern __shared__ __align__(16) double s_dyn[];
-  double* s_tab = s_dyn;
-  const int tab_len = (n_cls * NQ * TABW + 1) & ~1;
-  typedef double GOp[EPW][2][32][4];                 // [element][k-half][row (a,i)][q % 4]
-  typedef double GamBlk[EPW][NUB * 9];
-  GOp* s_G = reinterpret_cast<GOp*>(s_dyn + tab_len);
-  GamBlk* s_Gam = reinterpret_cast<GamBlk*>(s_dyn + tab_len + kTCWarps * EPW * 256);
-
-  {
-    const int tot = n_cls * NQ * TABW;
-    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_tab[t] = cls_tab[t];
-    double* z = &s_G[0][0][0][0][0];
-    for (int t = threadIdx.x; t < kTCWarps * EPW * 256; t += blockDim.x) z[t] = 0.0;
-    __syncthreads();
-  }
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const bool lane_active = lane < EPW * GROUP;
-  const int g = lane_active ? lane / GROUP : 0;
-  const int a = lane_active ? lane % GROUP : 0;
-  const int64_t ebase = ((int64_t)blockIdx.x * kTCWarps + wib) * EPW;
-  const int64_t e = ebase + g;
-  const bool valid = lane_active && e < n_el;
-  const int gbase = g * GROUP;
-
-  double xa[3] = {0, 0, 0}, va[3] = {0, 0, 0};
-  int ce = 0;
-  if (valid) {
-    const int64_t I = conn[e * NEN + a];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) xa[i] = x[3 * I + i];
-    if (KV) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i) va[i] = v[3 * I + i];
-    }
-    ce = cls[e];
-  }
-  double fa[3] = {0, 0, 0};
-  double Dm[NB][6], sg[NB];
-#pragma unroll
-  for (int j = 0; j < NB; ++j) {
-    sg[j] = 0.0;
-#pragma unroll
-    for (int r = 0; r < 6; ++r) Dm[j][r] = 0.0;
-  }
-
-  // ---------------- phase A: per quadrature point (3 elements per warp)
-#pragma unroll 1
-  for (int q = 0; q < NQ; ++q) {
-    const double* tq = s_tab + (ce * NQ + q) * TABW;
-    double gN[3] = {0, 0, 0}, w = 0.0;
-    if (valid) {
-      gN[0] = tq[3 * a];
-      gN[1] = tq[3 * a + 1];
-      gN[2] = tq[3 * a + 2];
-      w = tq[3 * NEN];
-    }
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int J = 0; J < 3; ++J) {
-        s_part[wib][3 * i + J][lane] = xa[i] * gN[J];
-        if (KV) s_part[wib][9 + 3 * i + J][lane] = va[i] * gN[J];
-      }
-    __syncwarp();
-    if (lane_active && a < 9) {
-      const double* p = &s_part[wib][a][gbase];
-      s_F[wib][g][a] = (((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]))) + (p[8] + p[9]);
-      if (KV) {
-        const double* pd = &s_part[wib][9 + a][gbase];
-        s_F[wib][g][9 + a] =
-            (((pd[0] + pd[1]) + (pd[2] + pd[3])) + ((pd[4] + pd[5]) + (pd[6] + pd[7]))) + (pd[8] + pd[9]);
-      }
-    }
-    __syncwarp();
-    double F[9], Fd[9];
-#pragma unroll
-    for (int r = 0; r < 9; ++r) {
-      F[r] = s_F[wib][g][r];
-      if (KV) Fd[r] = s_F[wib][g][9 + r];
-    }
-    double S[6], St[6];
-    svk_S(F, mat.lam, mat.mu, S);
-#pragma unroll
-    for (int r = 0; r < 6; ++r) St[r] = S[r];
-    if (KV) {
-      double Sv[6];
-      kv_S(F, Fd, mat.eta, mat.lamd, Sv);
-#pragma unroll
-      for (int r = 0; r < 6; ++r) St[r] += Sv[r];
-    }
-    {  // Stage 2 force
-      double t[3];
-#pragma unroll
-      for (int I = 0; I < 3; ++I)
-        t[I] = w * (sget(St, I, 0) * gN[0] + sget(St, I, 1) * gN[1] + sget(St, I, 2) * gN[2]);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) fa[i] = fma(F[3 * i], t[0], fma(F[3 * i + 1], t[1], fma(F[3 * i + 2], t[2], fa[i])));
-    }
-    // Gram operand: g_a = F grad N_a into G[(a,i)][q]
-    if (valid) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-        s_G[wib][g][q >> 2][3 * a + i][q & 3] = F[3 * i] * gN[0] + F[3 * i + 1] * gN[1] + F[3 * i + 2] * gN[2];
-    }
-    double B[6];
-#pragma unroll
-    for (int vv = 0; vv < 6; ++vv) {
-      int i, k;
-      voigt_pair(vv, i, k);
-      B[vv] = F[3 * i] * F[3 * k] + F[3 * i + 1] * F[3 * k + 1] + F[3 * i + 2] * F[3 * k + 2];
-    }
-    double tw[3], gNm[3];
-    const double mw = mat.mu * w;
-#pragma unroll
-    for (int I = 0; I < 3; ++I) {
-      tw[I] = w * (sget(S, I, 0) * gN[0] + sget(S, I, 1) * gN[1] + sget(S, I, 2) * gN[2]);
-      gNm[I] = mw * gN[I];
-    }
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      const int b = partner<0>(a, 0, j);
-      if (b < 0) continue;
-      const double nb0 = tq[3 * b], nb1 = tq[3 * b + 1], nb2 = tq[3 * b + 2];
-      sg[j] += fma(tw[0], nb0, fma(tw[1], nb1, tw[2] * nb2));
-      const double d = fma(gNm[0], nb0, fma(gNm[1], nb1, gNm[2] * nb2));
-#pragma unroll
-      for (int r = 0; r < 6; ++r) Dm[j][r] = fma(d, B[r], Dm[j][r]);
-    }
-    __syncwarp();
-  }
-
-  // ---------------- phase B: Gram G = sum_q w g g^T on the FP64 tensor cores
-  const int fr = lane >> 2, fc = lane & 3;
-  // per-lane destinations of the 20 accumulator entries in the compact block
-  // store (primary | mirror << 16, 0xffff = none), constant across elements
-  int gmap[20];
-  {
-    int n = 0;
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int ni = mi; ni < 4; ++ni)
-#pragma unroll
-        for (int h = 0; h < 2; ++h, ++n) {
-          const int r = 8 * mi + fr, c = 8 * ni + 2 * fc + h;
-          int prim = 0xffff, mir = 0xffff;
-          if (r < 30 && c < 30 && r <= c) {
-            const int A = r / 3, Bn = c / 3, ri = r % 3, ci = c % 3;
-            prim = ublk(NEN, A, Bn) * 9 + 3 * ri + ci;
-            if (A == Bn && ri != ci) mir = ublk(NEN, A, Bn) * 9 + 3 * ci + ri;
-          }
-          gmap[n] = prim | (mir << 16);
-        }
-  }
-#pragma unroll 1
-  for (int gg = 0; gg < EPW; ++gg) {
-    if (ebase + gg >= n_el) break;
-    const int cg = cls[ebase + gg];
-    double bf[2][4], af[2][4];
-#pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
-      const int q = 4 * kk + fc;
-      const double wq = q < NQ ? s_tab[(cg * NQ + q) * TABW + 3 * NEN] : 0.0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        bf[kk][t] = s_G[wib][gg][kk][8 * t + fr][fc];
-        af[kk][t] = wq * bf[kk][t];
-      }
-    }
-    double* gam = s_Gam[wib][gg];
-    int n = 0;
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int ni = mi; ni < 4; ++ni) {
-        double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) dmma884(c0, c1, af[kk][mi], bf[kk][ni]);
-#pragma unroll
-        for (int h = 0; h < 2; ++h, ++n) {
-          const double val = h ? c1 : c0;
-          const int prim = gmap[n] & 0xffff, mir = gmap[n] >> 16;
-          if (prim != 0xffff) gam[prim] = val;
-          if (mir != 0xffff) gam[mir] = val;
-        }
-      }
-  }
-  __syncwarp();
-
-  // ---------------- phase C: K_ab = lam G_ab + mu G_ab^T + D_ab + sigma_ab I
-  if (!valid) return;
-  {
-    double* fo = fscr + (fdest ? (int64_t)fdest[e * NEN + a] : e * NEN + a) * 3;
-    fo[0] = fa[0];
-    fo[1] = fa[1];
-    fo[2] = fa[2];
-  }
-  const double* gam = s_Gam[wib][g];
-#pragma unroll
-  for (int j = 0; j < NB; ++j) {
-    const int b = partner<0>(a, 0, j);
-    if (b < 0) continue;
-    const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
-    const double* gb = gam + ub * 9;
-    double Gab[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) Gab[3 * i + k] = a <= b ? gb[3 * i + k] : gb[3 * k + i];
-    double K[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        K[3 * i + k] = fma(mat.lam, Gab[3 * i + k], fma(mat.mu, Gab[3 * k + i], Dm[j][vidx(i, k)])) +
-                       (i == k ? sg[j] : 0.0);
-    bool tr = a > b;
-    int64_t pos = e * NUB + ub;
-    if (dest) {
-      const int32_t dd = dest[e * NUB + ub];
-      pos = dd >> 1;
-      tr = tr != ((dd & 1) != 0);
-    }
-    double* o = Kscr + pos * 9;
-    if (!tr) {
-#pragma unroll
-      for (int r = 0; r < 9; ++r) o[r] = K[r];
-    } else {
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) o[3 * k + i] = K[3 * i + k];
-    }
-  }
-}
 
 // ------------------------------------------------------------------ gather
-
-__device__ __forceinline__ void sum_block(const uint32_t* __restrict__ ent, int32_t t0, int32_t t1, int nen,
-                                          int nub, const double* __restrict__ Kscr, double acc[9]) {
-#pragma unroll
-  for (int r = 0; r < 9; ++r) acc[r] = 0.0;
-  for (int32_t t = t0; t < t1; ++t) {
-    const uint32_t en = __ldg(ent + t);
-    const int64_t e = en >> 8;
-    const int a = (en >> 4) & 15, b = en & 15;
-    double s[9];
-    const double* src = Kscr + (e * nub + (a <= b ? ublk(nen, a, b) : ublk(nen, b, a))) * 9;
-#pragma unroll
-    for (int r = 0; r < 9; ++r) s[r] = __ldcs(src + r);  // streamed: each block is read once
-    if (a <= b) {
-#pragma unroll
-      for (int r = 0; r < 9; ++r) acc[r] += s[r];
-    } else {
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) acc[3 * i + k] += s[3 * k + i];
-    }
-  }
-}
-
-// One thread per gather unit (I,J) [+ its transpose (J,I)]:
-//   H(I,J) = h sum_e K_e + M_IJ/h I,  H(J,I) = H(I,J)^T   (Eq. hessian)
-__global__ void k_gather_units(int64_t n_units, int nen, int nub, const int32_t* __restrict__ unit_p,
-                               const int32_t* __restrict__ unit_pT, const int32_t* __restrict__ blk_row,
-                               const int32_t* __restrict__ rowptr_c, const int32_t* __restrict__ blk_ptr,
-                               const uint32_t* __restrict__ blk_ent, const int32_t* __restrict__ unit_ptr,
-                               const double* __restrict__ Kscr, const double* __restrict__ M, double h,
-                               double* __restrict__ H) {
-  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (u >= n_units) return;
-  const int32_t p = unit_p[u], pT = unit_pT[u];
-  double acc[9];
-  if (unit_ptr) {  // gather-sorted scratch: contiguous, already oriented
-#pragma unroll
-    for (int r = 0; r < 9; ++r) acc[r] = 0.0;
-    for (int32_t t = unit_ptr[u]; t < unit_ptr[u + 1]; ++t) {
-      const double* src = Kscr + (int64_t)t * 9;
-#pragma unroll
-      for (int r = 0; r < 9; ++r) acc[r] += src[r];
-    }
-  } else {
-    sum_block(blk_ent, blk_ptr[p], blk_ptr[p + 1], nen, nub, Kscr, acc);
-  }
-  const double mh = M[p] / h;
-  {
-    const int32_t i = blk_row[p], b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0, k = p - b0;
-    double* out = H + 9 * (int64_t)b0 + 3 * k;
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-#pragma unroll
-      for (int f = 0; f < 3; ++f) out[3 * d * deg + f] = fma(h, acc[3 * d + f], d == f ? mh : 0.0);
-  }
-  if (pT >= 0) {
-    const int32_t i = blk_row[pT], b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0, k = pT - b0;
-    double* out = H + 9 * (int64_t)b0 + 3 * k;
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-#pragma unroll
-      for (int f = 0; f < 3; ++f) out[3 * d * deg + f] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
-  }
-}
 
 // v3: TMA bulk copies (cp.async.bulk global->shared, mbarrier completion),
 // double-buffered per warp: one elected lane moves the next window of the
@@ -2027,7 +1681,6 @@ struct GatherArgs {
   double h;
   double* H;
   int upper;  // UPPER H storage (u_deg = L | diagonal << 16, no transposed copy)
-  int dbg_gt; // diagnostics (TLFEA_DBG_GT=1, timing only, corrupts the scratch): transposes to contiguous scratch
 };
 
 // Per-warp TMA staging: two windows and their mbarriers. `wk` counts the
@@ -2112,14 +1765,6 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
   for (int d = 0; d < 3; ++d)
 #pragma unroll
     for (int f = 0; f < 3; ++f) h_store(out + 3 * d * deg + f, fma(h, acc[3 * d + f], d == f ? mh : 0.0));
-  if (A.dbg_gt) {
-    double* o2 = const_cast<double*>(Kscr) + P0 * 9 + lane;
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-#pragma unroll
-      for (int f = 0; f < 3; ++f) o2[32 * (3 * d + f)] = fma(h, acc[3 * f + d], d == f ? mh : 0.0);
-    return;
-  }
   if (offT >= 0) {
     double* o2 = H + offT;
 #pragma unroll
@@ -2152,152 +1797,7 @@ __global__ void __launch_bounds__(kG3Warps * 32) k_gather_units_v3(GatherArgs A)
   gather_units_warp(((int64_t)blockIdx.x * kG3Warps + (threadIdx.x >> 5)) * 32, A, W);
 }
 
-// ------------------------------------------------- fused persistent eval
-// One launch for the whole tangent eval (Stage 1 + 2, H gather, f / g):
-// CTAs take work items from a global ticket in list order. Element items
-// (fz_etiles CTA tiles) never wait; when one finishes it publishes its
-// chunk's completion counter (release). A gather item (512 units of H or
-// 1024 owned DOFs of f / g) first waits (acquire) until every element chunk
-// it reads is complete — the list places it a chunk after the last of them,
-// so the wait is normally already satisfied — and then reads the scratch
-// while it is still in L2. Items are handed out in list order and element
-// items never block, so every wait ends (no deadlock for any grid size).
-// Each H / f value is still summed by one thread in ascending element order:
-// the result is bitwise identical to the three-kernel path.
-struct FusedArgs {
-  ElArgs el;
-  GatherArgs ga;
-  FArgs fa;
-  const uint32_t* list;
-  int64_t n_items, nE, nG;
-  const int32_t* lo;
-  const int32_t* hi;
-  uint32_t* sync;  // [0] ticket, [1 + c] completed element items of chunk c
-  int etiles, chunk_items, gunits, fdofs;
-  int dbg;  // diagnostics (TLFEA_FZ_DBG): 1 skip gather items, 2 skip element work
-};
-
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-
-template <int ELEM, int NQ, int MODEL, bool KV>
-__global__ void __launch_bounds__(kWarps * 32, el_minb<ELEM, MODEL, 1>()) k_fused(FusedArgs P) {
-  static_assert(kG3Warps == kWarps || TLFEA_EL_WARPS != 4, "the fused CTA runs both item kinds");
-  // dynamic shared memory: [TMA windows kG3Warps x 2 x kG3Buf][class tables]
-  extern __shared__ __align__(16) double s_dyn[];
-  double(*s_buf)[2][kG3Buf] = reinterpret_cast<double(*)[2][kG3Buf]>(s_dyn);
-  double* s_tab = s_dyn + kG3Warps * 2 * kG3Buf;  // [n_cls][NQ][3 NEN + 1]
-  __shared__ __align__(8) uint64_t s_bar[kG3Warps][2];
-  __shared__ uint32_t s_item[2];
-  {
-    const int tot = P.el.n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1);
-    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_tab[t] = P.el.cls_tab[t];
-  }
-  G3Warp W;
-  g3_init(s_buf, s_bar, W);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint32_t* ticket = P.sync;
-  uint32_t* done = P.sync + 1;
-#pragma unroll 1
-  for (int it = 0;; ++it) {
-    if (threadIdx.x == 0) s_item[it & 1] = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t idx = s_item[it & 1];
-    if (idx >= P.n_items) break;
-    const uint32_t item = __ldg(P.list + idx);
-    const uint32_t type = item >> 30, k = item & 0x3fffffffu;
-    if (type == 0) {
-      const int64_t t0 = (int64_t)k * P.etiles;
-      if (!(P.dbg & 2)) {
-#pragma unroll 1
-        for (int j = 0; j < P.etiles; ++j) {
-          if constexpr (TLFEA_T10_2PH && ELEM == 0 && MODEL == 0) {
-            T10Pre pre;
-            t10_preload((t0 + j) * kWarps + wib, P.el, pre);
-            element_group_t10svk<NQ, KV>((t0 + j) * kWarps + wib, P.el, s_tab, pre);
-          } else if constexpr (TLFEA_ANCF_2PH && ELEM == 1 && MODEL == 0 && !KV) {
-            element_group_ancf_svk<NQ>((t0 + j) * kWarps + wib, P.el, s_tab);
-          } else if constexpr (TLFEA_MR_2PH && ELEM == 0 && MODEL == 1) {
-            element_group_t10mr<NQ, KV>((t0 + j) * kWarps + wib, P.el, s_tab);
-          } else
-            element_group<ELEM, NQ, MODEL, KV, true, true, 1>((t0 + j) * kWarps + wib, P.el, s_tab);
-        }
-      }
-      // publish: the CTA's stores -> barrier -> one gpu-scope release by thread 0
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        red_release_add(done + k / P.chunk_items, 1u);
-      }
-    } else if (!(P.dbg & 1)) {
-      const int64_t gi = type == 1 ? (int64_t)k : P.nG + k;
-      const int c0 = P.lo[gi], c1 = P.hi[gi];
-      if (wib == 0) {
-        for (int c = c0 + lane; c <= c1; c += 32) {
-          const uint32_t need = (uint32_t)min((int64_t)P.chunk_items, P.nE - (int64_t)c * P.chunk_items);
-          while (ld_acquire_u32(done + c) < need) __nanosleep(100);
-        }
-        __syncwarp();
-      }
-      __syncthreads();
-      if (type == 1) {
-        // scratch written by other SMs through the generic proxy, read here by TMA
-        if (lane == 0) asm volatile("fence.proxy.async.global;\n" ::: "memory");
-        __syncwarp();
-        const int64_t ub = (int64_t)k * P.gunits;
-#pragma unroll 1
-        for (int r = 0; r < P.gunits / (32 * kWarps); ++r) gather_units_warp(ub + (r * kWarps + wib) * 32, P.ga, W);
-      } else {
-        const int64_t t0 = (int64_t)k * P.fdofs, nd = 3 * P.fa.n_own;
-#pragma unroll 1
-        for (int r = 0; r < P.fdofs / (32 * kWarps); ++r) {
-          const int64_t t = t0 + r * (32 * kWarps) + threadIdx.x;
-          if (t < nd) gather_f_dof_one(t, P.fa);
-        }
-      }
-    }
-  }
-}
-
 // ------------------------------------------------------------- launchers
-
-// FP64 tensor-core tangent (k_t10_tc) on by default; TLFEA_TC=0 selects the
-// all-DFMA k_element (A/B measurements).
-static bool use_tc() {
-  // measured slower than the all-DFMA kernel on B200 (DMMA shares the FP64
-  // throughput and the fragment->block exchange adds shared-memory traffic):
-  // off by default, TLFEA_TC=1 enables it.
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("TLFEA_TC");
-    v = (s && s[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-// tiles per CTA of k_element with class tables (TLFEA_EL_TILES)
-static int el_cta_tiles() {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("TLFEA_EL_TILES");
-    v = (s && s[0]) ? std::max(1, atoi(s)) : 1;
-  }
-  return v;
-}
-static int dbg_nowrite() {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("TLFEA_DBG_NOKWRITE");
-    v = (s && s[0] == '1') ? 1 : 0;
-  }
-  return v;
-}
 
 static ElArgs el_args(const Context* c, const double* x, const double* v) {
   ElArgs A;
@@ -2316,60 +1816,28 @@ static ElArgs el_args(const Context* c, const double* x, const double* v) {
   A.dest = c->dest;
   A.fdest = c->fdest;
   A.err = c->err_flag;
-  A.cta_tiles = 1;
   return A;
 }
 
 template <int ELEM, int NQ, int MODEL, bool KV, bool TAN>
 static tlfea_status launch_el(Context* c, const double* x, const double* v, cudaStream_t s) {
   using G = Geo<ELEM>;
-  if constexpr (ELEM == 0 && MODEL == 0 && TAN) {
-    if (c->n_cls > 0 && use_tc()) {
-      const int tab_len = (c->n_cls * NQ * 31 + 1) & ~1;
-      const size_t smem = sizeof(double) * ((size_t)tab_len + kTCWarps * 3 * 256 + kTCWarps * 3 * 55 * 9);
-      static size_t smem_set = 0;
-      if (smem > smem_set) {
-        TL_CUDA(cudaFuncSetAttribute(k_t10_tc<NQ, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        smem_set = smem;
-      }
-      const int64_t per = (int64_t)kTCWarps * 3;
-      const unsigned grid = (unsigned)((c->n_el + per - 1) / per);
-      if (grid == 0) return TLFEA_OK;
-      k_t10_tc<NQ, KV><<<grid, kTCWarps * 32, smem, s>>>(c->n_el, c->conn, c->cls, c->cls_tab, c->n_cls, x, v,
-                                                         c->mat, c->fscr, c->Kscr, c->dest, c->fdest);
-      TL_CHECK_LAUNCH();
-      return TLFEA_OK;
-    }
-  }
   const int64_t per_cta = (int64_t)kWarps * G::EPW;
   const unsigned grid = (unsigned)((c->n_el + per_cta - 1) / per_cta);
   if (grid == 0) return TLFEA_OK;
-  c->mat.dbg_nowrite = dbg_nowrite();
   ElArgs A = el_args(c, x, v);
   if (c->n_cls > 0) {
     const size_t smem = sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
-    static size_t smem_set = 0;  // per template instantiation
-    if (smem > smem_set) {
-      TL_CUDA(cudaFuncSetAttribute(k_element<ELEM, NQ, MODEL, KV, TAN, true, el_npass<ELEM, MODEL>()>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      smem_set = smem;
-    }
-    // several tiles per CTA amortize the class-table staging; the grid is
-    // still dispatched in element order (compact in-flight window)
-    A.cta_tiles = el_cta_tiles();
-    const unsigned g = (unsigned)((grid + A.cta_tiles - 1) / A.cta_tiles);
-    k_element<ELEM, NQ, MODEL, KV, TAN, true, el_npass<ELEM, MODEL>()><<<g, kWarps * 32, smem, s>>>(A);
+    auto kern = k_element<ELEM, NQ, MODEL, KV, TAN, true, el_npass<ELEM, MODEL>()>;
+    TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
+    kern<<<grid, kWarps * 32, smem, s>>>(A);
   } else {
     // the T10 two-phase groups stage each warp's element tables in dynamic shared memory
     constexpr bool stage = ELEM == 0 && ((TLFEA_MR_2PH && MODEL == 1 && TAN) || (TLFEA_T10_2PH && MODEL == 0 && !KV));
     const size_t smem = stage ? sizeof(double) * kWarps * G::EPW * NQ * (G::NEN * 3 + 1) : 0;
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-      TL_CUDA(cudaFuncSetAttribute(k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>()>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      smem_set = smem;
-    }
-    k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>()><<<grid, kWarps * 32, smem, s>>>(A);
+    auto kern = k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>()>;
+    TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
+    kern<<<grid, kWarps * 32, smem, s>>>(A);
   }
   TL_CHECK_LAUNCH();
   return TLFEA_OK;
@@ -2410,110 +1878,13 @@ static GatherArgs gather_args(const Context* c, double h, double* H) {
   A.h = h;
   A.H = H;
   A.upper = c->upper;
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* e = getenv("TLFEA_DBG_GT");
-      dbg = e ? atoi(e) : 0;
-    }
-    A.dbg_gt = dbg;
-  }
   return A;
-}
-
-bool fused_available(const Context* c) { return c->fz_items > 0 && c->fz_list != nullptr; }
-
-template <int ELEM, int NQ, int MODEL, bool KV>
-static tlfea_status launch_fused_t(Context* c, const FusedArgs& P, cudaStream_t s) {
-  auto kern = k_fused<ELEM, NQ, MODEL, KV>;
-  static_assert((kG3Buf * sizeof(double)) % 16 == 0, "TMA windows stay 16-byte aligned");
-  const size_t smem =
-      sizeof(double) * ((size_t)kG3Warps * 2 * kG3Buf + (size_t)c->n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1));
-  static size_t smem_set = 0;
-  static int grid = 0;
-  if (smem > smem_set || grid == 0) {
-    TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
-    smem_set = std::max(smem, smem_set);
-    int per_sm = 0, n_sm = 0, dev = 0;
-    TL_CUDA(cudaGetDevice(&dev));
-    TL_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-    TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem_set));
-    grid = std::max(1, per_sm) * n_sm;
-  }
-  TL_CUDA(cudaMemsetAsync(c->fz_sync, 0, sizeof(uint32_t) * (1 + (size_t)c->fz_chunks), s));
-  kern<<<(unsigned)std::min<int64_t>(grid, c->fz_items), kWarps * 32, smem, s>>>(P);
-  TL_CHECK_LAUNCH();
-  return TLFEA_OK;
-}
-
-tlfea_status launch_fused_eval(Context* c, const double* x, const double* v, const double* vn, const double* fext,
-                               double h, double* g, double* H, double* fint, cudaStream_t s) {
-  if (!fused_available(c)) return fail(TLFEA_E_INVALID, "internal: no fused plan");
-  c->mat.dbg_nowrite = 0;
-  FusedArgs P;
-  P.el = el_args(c, x, v);
-  P.ga = gather_args(c, h, H);
-  P.fa.n_own = c->n_own;
-  P.fa.node_ptr = c->node_ptr;
-  P.fa.fscr = c->fscr;
-  P.fa.fpart_in = nullptr;
-  P.fa.own_nodes = c->own_nodes;
-  P.fa.rowptr_c = c->rowptr_c;
-  P.fa.cols_c = c->cols_c;
-  P.fa.M = c->M;
-  P.fa.fff = c->fff;
-  P.fa.v = v;
-  P.fa.vn = vn;
-  P.fa.fext = fext;
-  P.fa.h = h;
-  P.fa.mode = 0;
-  P.fa.g = g;
-  P.fa.fint = fint;
-  P.list = c->fz_list;
-  P.n_items = c->fz_items;
-  P.nE = c->fz_nE;
-  P.nG = c->fz_nG;
-  P.lo = c->fz_lo;
-  P.hi = c->fz_hi;
-  P.sync = c->fz_sync;
-  P.etiles = c->fz_etiles;
-  P.chunk_items = c->fz_chunk_items;
-  P.gunits = c->fz_gunits;
-  P.fdofs = c->fz_fdofs;
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* e = getenv("TLFEA_FZ_DBG");
-      dbg = e ? atoi(e) : 0;
-    }
-    P.dbg = dbg;
-  }
-  const bool kv = c->mat.kv && v != nullptr;
-  const int model = c->mat.model == TLFEA_SVK ? 0 : 1;
-#define TL_FUSED(E, Q)                                                                     \
-  do {                                                                                     \
-    if (model == 0) return kv ? launch_fused_t<E, Q, 0, true>(c, P, s) : launch_fused_t<E, Q, 0, false>(c, P, s); \
-    return kv ? launch_fused_t<E, Q, 1, true>(c, P, s) : launch_fused_t<E, Q, 1, false>(c, P, s);                 \
-  } while (0)
-  if (c->element == TLFEA_T10) {
-    if (c->nq == 4) TL_FUSED(0, 4);
-    TL_FUSED(0, 5);
-  }
-  TL_FUSED(1, 48);
-#undef TL_FUSED
 }
 
 tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
   if (c->n_units == 0) return TLFEA_OK;
-  if (c->u_off) {
-    const int64_t per = (int64_t)kG3Warps * 32;
-    k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(gather_args(c, h, H));
-    TL_CHECK_LAUNCH();
-    return TLFEA_OK;
-  }
-  k_gather_units<<<gridn(c->n_units, 256), 256, 0, s>>>(c->n_units, c->nen, n_ublk_of(c->nen), c->unit_p,
-                                                        c->unit_pT, c->blk_row, c->rowptr_c, c->blk_ptr,
-                                                        c->blk_ent, c->unit_ptr, c->Kscr, c->M, h, H);
+  const int64_t per = (int64_t)kG3Warps * 32;
+  k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(gather_args(c, h, H));
   TL_CHECK_LAUNCH();
   return TLFEA_OK;
 }

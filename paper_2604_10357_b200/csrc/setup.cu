@@ -5,6 +5,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <cstring>
 #include <numeric>
 
@@ -24,6 +26,21 @@ tlfea_status fail(tlfea_status st, const std::string& msg) {
   return st;
 }
 void count_launch(int n) { g_launches += n; }
+
+tlfea_status ensure_dynamic_smem(const void* kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return TLFEA_OK;
+  int dev = 0;
+  TL_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> applied;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = applied[{kernel, dev}];
+  if (bytes > have) {
+    TL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = bytes;
+  }
+  return TLFEA_OK;
+}
 const char* last_error() { return g_err.c_str(); }
 int64_t launch_count() { return g_launches.load(); }
 
@@ -639,10 +656,7 @@ static tlfea_status build_geometry_classes(Context* c, const double* dX) {
   const int max_cls = c->element == TLFEA_T10 ? 32 : 4;
   c->n_cls = 0;
   if (n == 0) return TLFEA_OK;
-  {
-    const char* e = getenv("TLFEA_NO_CLASSES");  // measure the per-(e,q) table path on any mesh
-    if (e && atoi(e) > 0) return TLFEA_OK;
-  }
+  if (c->force_tables) return TLFEA_OK;  // options.reference_layout = 1
   TmpArr<unsigned long long> key, key2;
   TmpArr<int64_t> idx, idx2;
   TmpArr<int32_t> flag, run;
@@ -823,121 +837,6 @@ static tlfea_status build_unit_meta(Context* c) {
   return TLFEA_OK;
 }
 
-// ------------------------------------------------- fused eval work list
-// Chunk range of the elements a gather item reads: H items = `per` units
-// (contributions through the inverse slot map), f items = `per` owned DOFs
-// (the node's incidence list).
-__global__ void k_item_erange_units(int64_t n_items, int64_t per, int64_t n_units, const int32_t* __restrict__ unit_p,
-                                    const int32_t* __restrict__ blk_ptr, const uint32_t* __restrict__ blk_ent,
-                                    int64_t epc, int32_t* __restrict__ lo, int32_t* __restrict__ hi) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n_items) return;
-  int64_t mn = INT64_MAX, mx = -1;
-  for (int64_t u = k * per; u < min((k + 1) * per, n_units); ++u) {
-    const int32_t p = unit_p[u];
-    for (int32_t t = blk_ptr[p]; t < blk_ptr[p + 1]; ++t) {
-      const int64_t e = blk_ent[t] >> 8;
-      mn = min(mn, e);
-      mx = max(mx, e);
-    }
-  }
-  lo[k] = mx < 0 ? 0 : (int32_t)(mn / epc);
-  hi[k] = mx < 0 ? -1 : (int32_t)(mx / epc);
-}
-
-__global__ void k_item_erange_dofs(int64_t n_items, int64_t per, int64_t n_dof, const int32_t* __restrict__ node_ptr,
-                                   const uint32_t* __restrict__ node_ent, int64_t epc, int32_t* __restrict__ lo,
-                                   int32_t* __restrict__ hi) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n_items) return;
-  const int64_t t0 = k * per, t1 = min((k + 1) * per, n_dof);
-  int64_t mn = INT64_MAX, mx = -1;
-  for (int64_t i = t0 / 3; i <= (t1 - 1) / 3; ++i)
-    for (int32_t t = node_ptr[i]; t < node_ptr[i + 1]; ++t) {
-      const int64_t e = node_ent[t] >> 4;
-      mn = min(mn, e);
-      mx = max(mx, e);
-    }
-  lo[k] = mx < 0 ? 0 : (int32_t)(mn / epc);
-  hi[k] = mx < 0 ? -1 : (int32_t)(mx / epc);
-}
-
-static int env_int(const char* name, int dflt) {
-  const char* s = getenv(name);
-  return (s && s[0]) ? atoi(s) : dflt;
-}
-
-// Work list of the fused persistent eval (element.cu k_fused): element items
-// in element order, chunked; each gather item is placed `lag` chunks after
-// the last chunk it reads, so by the time a CTA takes it the scratch it needs
-// is normally complete and still resident in L2. Opt-in (TLFEA_FUSED=1 at
-// setup): measured slower than the three-kernel eval on B200 (DESIGN.md §6 —
-// the element tiles hold the whole register file, so gather items get only
-// their 12 warps per SM and the two phases serialize instead of overlapping).
-// TLFEA_FZ_{ETILES,CHUNK,LAG} tune it.
-static tlfea_status build_fused_plan(Context* c) {
-  c->fz_items = 0;
-  if (env_int("TLFEA_FUSED", 0) == 0 || c->element == TLFEA_ANCF3243) return TLFEA_OK;
-  if (c->nranks != 1 || c->n_cls == 0 || !c->unit_ptr || !c->u_off || !c->fdest || c->n_el == 0 ||
-      c->n_units == 0 || c->n_own == 0)
-    return TLFEA_OK;
-  // lag in element items: must exceed the items in flight (~ resident CTAs,
-  // 3 x 148 for T10) or gather items spin; small enough that the scratch in
-  // between (lag x elements per item x ~4.2 KB) stays in the 126 MB L2.
-  const int etiles = std::max(1, env_int("TLFEA_FZ_ETILES", 1));
-  const int chunk_items = std::max(1, env_int("TLFEA_FZ_CHUNK", 64));
-  const int lag_items = std::max(0, env_int("TLFEA_FZ_LAG", 1024));
-  const int lag = (lag_items + chunk_items - 1) / chunk_items;
-  const int gunits = 4 * kGatherThreads, fdofs = 8 * kGatherThreads;
-  const int64_t ept = el_per_tile(c->element);
-  const int64_t nE = (c->n_el + ept * etiles - 1) / (ept * etiles);
-  const int64_t epc = ept * etiles * chunk_items;  // elements per chunk
-  const int64_t n_chunks = (nE + chunk_items - 1) / chunk_items;
-  const int64_t nG = (c->n_units + gunits - 1) / gunits;
-  const int64_t nF = (3 * c->n_own + fdofs - 1) / fdofs;
-  if (nE + nG + nF >= (int64_t(1) << 30)) return TLFEA_OK;
-  TL_TRY(c->alloc(&c->fz_lo, (size_t)(nG + nF)));
-  TL_TRY(c->alloc(&c->fz_hi, (size_t)(nG + nF)));
-  k_item_erange_units<<<grid_for(nG, 128), 128>>>(nG, gunits, c->n_units, c->unit_p, c->blk_ptr, c->blk_ent, epc,
-                                                  c->fz_lo, c->fz_hi);
-  TL_CHECK_LAUNCH();
-  k_item_erange_dofs<<<grid_for(nF, 128), 128>>>(nF, fdofs, 3 * c->n_own, c->node_ptr, c->node_ent, epc,
-                                                 c->fz_lo + nG, c->fz_hi + nG);
-  TL_CHECK_LAUNCH();
-  std::vector<int32_t> hi(nG + nF);
-  TL_CUDA(cudaMemcpy(hi.data(), c->fz_hi, sizeof(int32_t) * (nG + nF), cudaMemcpyDeviceToHost));
-  // bucket the gather items by release chunk (stable: H items, then f items, by index)
-  std::vector<int64_t> cnt(n_chunks + 1, 0);
-  auto slot = [&](int64_t k) { return std::min<int64_t>(std::max<int64_t>(hi[k], 0) + lag, n_chunks - 1); };
-  for (int64_t k = 0; k < nG + nF; ++k) cnt[slot(k) + 1]++;
-  for (int64_t ch = 0; ch < n_chunks; ++ch) cnt[ch + 1] += cnt[ch];
-  std::vector<uint32_t> gl(nG + nF);
-  {
-    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
-    for (int64_t k = 0; k < nG + nF; ++k)
-      gl[pos[slot(k)]++] = k < nG ? (1u << 30) | (uint32_t)k : (2u << 30) | (uint32_t)(k - nG);
-  }
-  std::vector<uint32_t> list;
-  list.reserve(nE + nG + nF);
-  for (int64_t ch = 0; ch < n_chunks; ++ch) {
-    for (int64_t i = ch * chunk_items; i < std::min<int64_t>((ch + 1) * chunk_items, nE); ++i) list.push_back((uint32_t)i);
-    for (int64_t t = cnt[ch]; t < cnt[ch + 1]; ++t) list.push_back(gl[t]);
-  }
-  TL_TRY(c->alloc(&c->fz_list, list.size()));
-  TL_CUDA(cudaMemcpy(c->fz_list, list.data(), sizeof(uint32_t) * list.size(), cudaMemcpyHostToDevice));
-  TL_TRY(c->alloc(&c->fz_sync, (size_t)(1 + n_chunks)));
-  c->fz_items = (int64_t)list.size();
-  c->fz_nE = nE;
-  c->fz_nG = nG;
-  c->fz_nF = nF;
-  c->fz_chunks = (int)n_chunks;
-  c->fz_etiles = etiles;
-  c->fz_chunk_items = chunk_items;
-  c->fz_gunits = gunits;
-  c->fz_fdofs = fdofs;
-  return TLFEA_OK;
-}
-
 static tlfea_status validate(const tlfea_mesh* mesh, const tlfea_material* mat,
                              const tlfea_options* opts) {
   if (!mesh || !mat || !opts) return fail(TLFEA_E_INVALID, "NULL mesh/material/options");
@@ -968,6 +867,8 @@ static tlfea_status validate(const tlfea_mesh* mesh, const tlfea_material* mat,
   if (opts->mass_rule != 0 && opts->mass_rule != 1) return fail(TLFEA_E_INVALID, "mass_rule must be 0 or 1");
   if (opts->nranks < 1 || opts->rank < 0 || opts->rank >= opts->nranks)
     return fail(TLFEA_E_INVALID, "bad rank / nranks");
+  if (opts->reference_layout != 0 && opts->reference_layout != 1)
+    return fail(TLFEA_E_INVALID, "reference_layout must be 0 or 1");
   if (opts->hessian_upper != 0 && opts->hessian_upper != 1)
     return fail(TLFEA_E_INVALID, "hessian_upper must be 0 or 1");
   if (opts->hessian_upper && (opts->nranks != 1 || (opts->constraints && opts->constraints->m > 0)))
@@ -1120,6 +1021,7 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   c->nen = n_en_of(mesh->element);
   c->nq = n_qp_of(opts->quadrature);
   c->mass_rule = opts->mass_rule;
+  c->force_tables = opts->reference_layout;
   c->mat_in = *mat;
   c->mat = make_matdev(*mat);
   for (int k = 0; k < 3; ++k) c->gravity[k] = opts->gravity[k];
@@ -1399,7 +1301,7 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   }
 
   TL_TRY(build_units(c));
-  if (env_int("TLFEA_SORTED", 1) != 0) TL_TRY(build_sorted_scratch(c));  // 0: element-major scratch (diagnostics)
+  TL_TRY(build_sorted_scratch(c));
 
   // ---- consistent mass over the setup elements (reading Q4) and f_ff
   TL_TRY(c->alloc(&c->M, (size_t)c->nnz_c));
@@ -1487,7 +1389,6 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   TL_TRY(c->alloc(&c->Kscr, (size_t)c->n_el * n_ublk_of(nen) * 9 + 4));
   TL_TRY(c->alloc(&c->fscr, (size_t)c->n_el * nen * 3));
   TL_TRY(c->alloc(&c->fpart, (size_t)3 * std::max<int64_t>(c->n_own, 1)));
-  TL_TRY(build_fused_plan(c));
 
   // ---- partition exchange lists
   if (c->nranks > 1) TL_TRY(setup_exchange(c, cc, part, owner, local));

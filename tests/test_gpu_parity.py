@@ -206,28 +206,6 @@ def test_many_body_force_only(torch_cuda):
     assert rel(f, f0) <= TOL
 
 
-@pytest.mark.parametrize("case", ["t10_5x3x1_svk_keast5_ragged", "t10_4x3x2_mr_kv_keast5",
-                                  "t10_3x2x2_svk_kv_4pt_morton", "ancf_5x5_mr_kv"])
-def test_fused_eval_bitwise(torch_cuda, case, monkeypatch):
-    """The opt-in fused persistent eval (TLFEA_FUSED=1 at setup) gives the
-    three-kernel results bit for bit (same per-value summation order) and
-    matches the oracle."""
-    mesh, mat, rule = CASES[case]()
-    h = synth.H_T10 if mesh.element == 0 else synth.H_ANCF
-    x, v, vn, fext = state(mesh)
-    ctx0, g0, H0, f0 = gpu_eval(torch_cuda, mesh, mat, rule, x, v, vn, fext, h)
-    assert ctx0.info["fused_eval"] == 0
-    monkeypatch.setenv("TLFEA_FUSED", "1")
-    monkeypatch.setenv("TLFEA_FZ_CHUNK", "2")   # many chunks even on a small mesh
-    monkeypatch.setenv("TLFEA_FZ_LAG", "1")
-    ctx1, g1, H1, f1 = gpu_eval(torch_cuda, mesh, mat, rule, x, v, vn, fext, h)
-    assert ctx1.info["fused_eval"] == 1
-    assert np.array_equal(g0, g1) and np.array_equal(H0, H1) and np.array_equal(f0, f1)
-    pr = oracle.Problem(mesh, mat, rule)
-    gr, Hr, fr = pr.eval(x, v, vn, fext, h)
-    assert rel(H1, Hr) <= TOL and rel(g1, gr) <= TOL and rel(f1, fr) <= TOL
-
-
 def test_eval_host_matches_device(torch_cuda):
     torch = torch_cuda
     import paper_2604_10357_b200 as T

@@ -1,7 +1,7 @@
 """UPPER storage of H (reading Q14) on the GPU vs the
 oracle's upper view: pattern and slot map bit-exact, values within the
 parity bar, the same values as the FULL storage at the kept entries, the
-fused path and the error cases."""
+and the error cases."""
 import numpy as np
 import pytest
 
@@ -38,7 +38,7 @@ CASES = {
 
 
 @pytest.mark.parametrize("case", list(CASES))
-def test_upper_h_parity(torch_cuda, case, monkeypatch):
+def test_upper_h_parity(torch_cuda, case):
     torch = torch_cuda
     import paper_2604_10357_b200 as T
     mesh, mat, rule = CASES[case]()
@@ -72,14 +72,6 @@ def test_upper_h_parity(torch_cuda, case, monkeypatch):
     _, Hf, _ = ctx_f.eval(d(x), d(v), d(vn), d(fext), h)
     torch.cuda.synchronize()
     assert np.array_equal(Hf.cpu().numpy()[keep], H.cpu().numpy())
-    # the opt-in fused path writes the same UPPER values
-    if mesh.element != 2:
-        monkeypatch.setenv("TLFEA_FUSED", "1")
-        ctx_z = T.Context.from_mesh(mesh, mat, rule, hessian="upper")
-        _, Hz, _ = ctx_z.eval(d(x), d(v), d(vn), d(fext), h)
-        torch.cuda.synchronize()
-        if ctx_z.info["fused_eval"]:
-            assert np.array_equal(Hz.cpu().numpy(), H.cpu().numpy())
 
 
 def test_upper_errors(torch_cuda):
