@@ -28,7 +28,8 @@ tlfea_status fail(tlfea_status st, const std::string& msg) {
 void count_launch(int n) { g_launches += n; }
 
 tlfea_status ensure_dynamic_smem(const void* kernel, size_t bytes) {
-  if (bytes <= 48 * 1024) return TLFEA_OK;
+  // (set even below 48 KB: static + dynamic above 48 KB needs the opt-in too)
+  if (bytes == 0) return TLFEA_OK;
   int dev = 0;
   TL_CUDA(cudaGetDevice(&dev));
   static std::mutex mu;
@@ -106,12 +107,6 @@ struct TmpArr {
     return TLFEA_OK;
   }
 };
-
-#define TL_TRY(expr)                      \
-  do {                                    \
-    tlfea_status st__ = (expr);           \
-    if (st__ != TLFEA_OK) return st__;    \
-  } while (0)
 
 static inline unsigned grid_for(int64_t n, int block) {
   return (unsigned)std::max<int64_t>(1, (n + block - 1) / block);
@@ -1380,6 +1375,7 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   }
 
   TL_TRY(build_unit_meta(c));
+  TL_TRY(build_tile_plan(c, mesh->X_ref));
 
   // ---- eval scratch
   // element blocks are addressed with 32-bit block positions

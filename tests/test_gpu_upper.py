@@ -67,11 +67,15 @@ def test_upper_h_parity(torch_cuda, case):
     sm_full = pr.slot_map()
     want = np.where(sm_full >= 0, full_to_upper[np.maximum(sm_full, 0)], -1)
     assert np.array_equal(ctx.slot_map().astype(np.int64), want)
-    # FULL storage, same values at the kept entries (same summation order)
+    # FULL storage, the same values at the kept entries (bitwise when both run
+    # the two-kernel path; the one-kernel FULL eval sums in another order)
     ctx_f = T.Context.from_mesh(mesh, mat, rule)
     _, Hf, _ = ctx_f.eval(d(x), d(v), d(vn), d(fext), h)
     torch.cuda.synchronize()
-    assert np.array_equal(Hf.cpu().numpy()[keep], H.cpu().numpy())
+    if ctx_f.info["fused_eval"]:
+        assert rel(Hf.cpu().numpy()[keep], H.cpu().numpy()) <= 1e-13
+    else:
+        assert np.array_equal(Hf.cpu().numpy()[keep], H.cpu().numpy())
 
 
 def test_upper_errors(torch_cuda):
