@@ -182,9 +182,9 @@ typedef struct {
   int32_t n_geometry_classes; /* > 0: congruent elements share reference
                                  tables (staged in shared memory); 0: the
                                  per-(e,q) tables of §4.1 are read from HBM */
-  int32_t fused_eval;      /* 1: tlfea_eval runs the whole eval in one
-                              kernel (no tangent scratch); 0: element kernel
-                              + H gather + f/g gather. */
+  int32_t fused_eval;      /* reserved: 0 (tlfea_eval = element kernel + H
+                              gather + f/g gather; DESIGN.md §6 records the
+                              one-kernel variants measured). */
   int64_t n_constraints;   /* rows m of the context's constraint set (0: none) */
 } tlfea_info_t;
 

@@ -115,7 +115,7 @@ tlfea_status tlfea_info(tlfea_ctx ctx, tlfea_info_t* o) {
   o->nranks = c.nranks;
   o->device_bytes = c.device_bytes;
   o->n_geometry_classes = c.n_cls;
-  o->fused_eval = c.n_tiles > 0 ? 1 : 0;
+  o->fused_eval = 0;
   o->n_constraints = c.n_con;
   return TLFEA_OK;
 }
@@ -253,10 +253,6 @@ tlfea_status tlfea_eval(tlfea_ctx ctx, const double* x, const double* v, const d
   TRY(use_device(c));
   const cudaStream_t s = as_stream(stream);
   c.last_stream = s;
-  if (c.n_tiles > 0) {
-    TIMED(4, launch_tile_eval(&c, x, v, v_n, f_ext, h, g_out, H_out, f_int_out, s));
-    return TLFEA_OK;
-  }
   TIMED(0, launch_element_kernel(&c, x, v, true, s));
   TIMED(1, launch_gather_H(&c, h, H_out, s));
   TIMED(2, launch_gather_f(&c, v, v_n, f_ext, h, g_out, f_int_out, false, s));

@@ -74,16 +74,6 @@ constexpr int kElWarps = TLFEA_EL_WARPS;
 inline int el_per_tile(int element) {
   return kElWarps * (element == TLFEA_T10 ? 3 : element == TLFEA_ANCF3443 ? 1 : 4);
 }
-// one-kernel eval (tile.cu): warps per CTA and staged elements per tile
-constexpr int kTileWarps = 8;
-constexpr int kTileMaxEl = 120;
-constexpr int kTileMaxNode = 344;  // nodes staged per tile (owned + halo)
-constexpr int kTileMaxOwn = 64;    // owned rows per tile (an aligned 4x4x4 Morton block)
-constexpr int kTileCap = 3;     // steps (elements) per lane (longer lane jobs are split over lanes)
-#ifndef TLFEA_TILE_KU
-#define TLFEA_TILE_KU 1
-#endif
-constexpr int kTileKU = TLFEA_TILE_KU;  // units per lane (units with the same elements share its steps)
 // gather CTA: 4 warps of 32 units (H) / 128 threads (f)
 constexpr int kGatherThreads = 128;
 
@@ -171,24 +161,6 @@ struct Context {
   int32_t* u_offT = nullptr;      // [n_units] H offset of (J,I) or -1
   int32_t* u_deg = nullptr;       // [n_units] deg(I) | deg(J) << 16
   double* u_m = nullptr;          // [n_units] M_IJ
-  // one-kernel eval plan (tile.cu; single rank, T10 SVK, geometry classes):
-  // node tiles, the elements each stages, per-warp interleaved contribution
-  // lists of the tile's units and per-lane unit metadata
-  int64_t n_tiles = 0, n_tile_visits = 0;
-  int tile_grid = 0;              // persistent grid of k_tile_eval
-  int32_t* t_rec_ptr = nullptr;   // [n_tiles+1]
-  uint16_t* t_rec = nullptr;      // [n_tile_visits][12] local node indices, class id
-  int32_t* t_node_ptr = nullptr;  // [n_tiles+1]
-  int32_t* t_node = nullptr;      // nodes of each tile (owned first)
-  int32_t* t_warp_ptr = nullptr;  // [n_tiles+1]
-  int32_t* w_ent = nullptr;       // [n_warps]
-  int32_t* w_info = nullptr;      // [n_warps] steps | diagonal << 16
-  uint64_t* t_ent = nullptr;      // per (item, step, lane): slot | (a_j << 4 | b_j) << (8 + 8 j)
-  int32_t* l_lane = nullptr;      // [32 n_items] part | diagonal << 8, -1 empty
-  int32_t* l_off = nullptr;       // [32 n_warps]
-  int32_t* l_aux = nullptr;
-  int32_t* l_deg = nullptr;
-  double* l_m = nullptr;
   double* Kscr = nullptr;         // [n_el][n_ublk][9]
   double* fscr = nullptr;         // [n_el][nen][3]
   unsigned long long* err_flag = nullptr;  // min over (e*64+q) with det F <= 0 (MR)
@@ -268,9 +240,6 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
 tlfea_status launch_element_kernel(Context* c, const double* x, const double* v,
                                    bool tangent, cudaStream_t s);
 tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s);
-tlfea_status build_tile_plan(Context* c, const double* X_host);
-tlfea_status launch_tile_eval(Context* c, const double* x, const double* v, const double* vn, const double* fext,
-                              double h, double* g, double* H, double* fint, cudaStream_t s);
 tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, const double* fext,
                              double h, double* g, double* fint, bool partial_only,
                              cudaStream_t s);

@@ -1375,7 +1375,6 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   }
 
   TL_TRY(build_unit_meta(c));
-  TL_TRY(build_tile_plan(c, mesh->X_ref));
 
   // ---- eval scratch
   // element blocks are addressed with 32-bit block positions
