@@ -444,13 +444,16 @@ def incidence(conn_coef: np.ndarray, nodes: np.ndarray):
     return ptr, inc
 
 
-def eval_rows(mesh, mat: dict, rule: int, mass_rule: int, x, v, h, nodes, max_cols: int = 96):
+def eval_rows(mesh, mat: dict, rule: int, mass_rule: int, x, v, h, nodes, max_cols: int = 96, inc=None):
     """Sampled-row oracle: for each coefficient node I in `nodes`, returns
     (cols [n][max_cols] coefficient columns (-1 padded), H [n][3][max_cols][3],
-    f_int [n][3], M [n][max_cols]). Elements visited in ascending order."""
+    f_int [n][3], M [n][max_cols]). Elements visited in ascending order.
+    inc: optional (ptr, elements) incidence of `nodes` (as `incidence` returns)."""
     nodes = np.ascontiguousarray(nodes, np.int64)
-    coef_conn = mesh.coef_conn()
-    ptr, inc = incidence(coef_conn, nodes)
+    if inc is None:
+        ptr, inc = incidence(mesh.coef_conn(), nodes)
+    else:
+        ptr, inc = (np.ascontiguousarray(a, np.int64) for a in inc)
     n = len(nodes)
     while True:
         cols = np.zeros((n, max_cols), np.int64)

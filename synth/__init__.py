@@ -136,6 +136,29 @@ def ancf_plate(n: int, Lx: float = 4.0, Ly: float = 2.0, H: float = 0.1) -> Mesh
     return Mesh(1, X.reshape(-1, 3), conn.astype(np.int32), dims, name=f"ancf{n}x{n}")
 
 
+def ancf_plate_graded(n: int, ratio: float = 1.15, Lx: float = 4.0, Ly: float = 2.0, H: float = 0.1) -> Mesh:
+    """n x n ANCF3443 plate whose element lengths along x grow geometrically
+    by `ratio` (total Lx): n distinct element sizes, so no geometry classes
+    (the per-(e,q) table path). Flat reference as in ancf_plate."""
+    nn = n + 1
+    steps = ratio ** np.arange(n)
+    xs = np.concatenate([[0.0], np.cumsum(steps)]) * (Lx / steps.sum())
+    ys = np.arange(nn) * (Ly / n)
+    gx, gy = np.meshgrid(xs, ys, indexing="ij")
+    X = np.zeros((nn * nn, 4, 3))
+    X[:, 0, 0] = gx.ravel()
+    X[:, 0, 1] = gy.ravel()
+    X[:, 1, 0] = 1.0
+    X[:, 2, 1] = 1.0
+    X[:, 3, 2] = 1.0
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    i, j = i.ravel(), j.ravel()
+    nid = lambda a, b: a * nn + b
+    conn = np.stack([nid(i, j), nid(i + 1, j), nid(i + 1, j + 1), nid(i, j + 1)], axis=1)
+    dims = np.stack([xs[i + 1] - xs[i], np.full(n * n, Ly / n), np.full(n * n, H)], axis=1)
+    return Mesh(1, X.reshape(-1, 3), conn.astype(np.int32), dims, name=f"ancf{n}x{n}_graded")
+
+
 def ancf_beam(n: int, L: float = 0.2, W: float = 0.1, H: float = 0.1) -> Mesh:
     """Chain of n ANCF3243 beam elements along x (§5.3):
     element e spans nodes e and e+1, uniform L, rectangular W x H section.

@@ -173,3 +173,78 @@ def test_config5_many_body_sampled_bodies(T):
     s = np.abs(fb).max()
     assert np.abs(fb.sum(1)).max() < 1e-9 * s * per
     assert np.abs(np.cross(xb, fb).sum(1)).max() < 1e-8 * s * per
+
+
+# ---------------------------------------------- config 3, every row streamed
+_FULL = {}
+
+
+def _full_chunk(args):
+    """Worker (forked): oracle rows of nodes [n0, n1) against the GPU arrays
+    inherited through _FULL; returns squared-difference / norm sums."""
+    n0, n1 = args
+    F = _FULL
+    nodes = np.arange(n0, n1, dtype=np.int64)
+    p0, p1 = F["iptr"][n0], F["iptr"][n1]
+    inc = (F["iptr"][n0:n1 + 1] - p0, F["iinc"][p0:p1])
+    ocols, oH, of, oM = oracle.eval_rows(F["mesh"], F["mat"], F["rule"], 0, F["x"], F["v"], F["h"], nodes, inc=inc)
+    rp, cols, H, f, g = F["rowptr"], F["cols"], F["H"], F["f"], F["g"]
+    out = np.zeros(7)
+    vd = (F["v"] - F["vn"]).reshape(-1, 3)
+    for s, I in enumerate(nodes):
+        c = ocols[s][ocols[s] >= 0]
+        deg = len(c)
+        r0, r1 = rp[3 * I], rp[3 * I + 3]
+        exp_cols = np.tile((3 * c[:, None] + np.arange(3)[None, :]).ravel(), 3)
+        if r1 - r0 != exp_cols.size or not np.array_equal(cols[r0:r1], exp_cols):
+            out[6] += 1
+            continue
+        ov = oH[s][:, :deg, :].reshape(-1)
+        out[0] += np.sum((H[r0:r1] - ov) ** 2)
+        out[1] += np.sum(ov ** 2)
+        out[2] += np.sum((f[3 * I:3 * I + 3] - of[s]) ** 2)
+        out[3] += np.sum(of[s] ** 2)
+        g0 = oM[s][:deg] @ vd[c] / F["h"] + of[s] - F["fext"][3 * I:3 * I + 3]
+        out[4] += np.sum((g[3 * I:3 * I + 3] - g0) ** 2)
+        out[5] += np.sum(g0 ** 2)
+    return out
+
+
+def test_config3_every_row_streamed(T):
+    """the headline mesh checked in full. The GPU evaluates
+    config 3 once (H with 1,384,065,801 values); the oracle then recomputes
+    EVERY node row (pattern bit-exact, H / f_int / g values) in chunks of
+    nodes, fanned out over the host cores (each oracle process is single
+    threaded). Bars as in north_star: normwise 1e-11 per array."""
+    import multiprocessing as mp
+    import os
+    cfg = synth.config(3)
+    mesh = cfg.mesh
+    x, v, vn, fext = synth.t10_state(mesh, with_fext=True)
+    ctx = T.Context.from_mesh(mesh, cfg.material, cfg.quadrature)
+    assert ctx.nnz == 1_384_065_801
+    g, H, f = ctx.empty_outputs()
+    ctx.eval(d(x), d(v), d(vn), d(fext), cfg.h, g, H, f)
+    rowptr, cols = [t.cpu().numpy() for t in ctx.export_pattern()[:2]]
+    Hh, fh, gh = H.cpu().numpy(), f.cpu().numpy(), g.cpu().numpy()
+    del ctx, H, g, f
+    # node -> ascending incident elements (CSR), for the oracle's row loop
+    cc = mesh.coef_conn().astype(np.int64)
+    flat = cc.ravel()
+    order = np.argsort(flat, kind="stable")          # stable: elements ascend within a node
+    iptr = np.zeros(mesh.n_coef + 1, np.int64)
+    np.add.at(iptr, flat + 1, 1)
+    iptr = np.cumsum(iptr)
+    iinc = (order // cc.shape[1]).astype(np.int64)
+    _FULL.update(mesh=mesh, mat=cfg.material, rule=cfg.quadrature, h=cfg.h, x=x, v=v, vn=vn, fext=fext,
+                 rowptr=rowptr.astype(np.int64), cols=cols, H=Hh, f=fh, g=gh, iptr=iptr, iinc=iinc)
+    chunk = 8192
+    jobs = [(n0, min(n0 + chunk, mesh.n_coef)) for n0 in range(0, mesh.n_coef, chunk)]
+    workers = max(1, len(os.sched_getaffinity(0)))
+    with mp.get_context("fork").Pool(workers) as pool:
+        tot = np.sum(pool.map(_full_chunk, jobs, chunksize=1), axis=0)
+    _FULL.clear()
+    assert tot[6] == 0, f"{int(tot[6])} rows with a pattern mismatch"
+    assert np.sqrt(tot[0] / tot[1]) <= TOL, np.sqrt(tot[0] / tot[1])
+    assert np.sqrt(tot[2] / tot[3]) <= TOL, np.sqrt(tot[2] / tot[3])
+    assert np.sqrt(tot[4] / tot[5]) <= TOL, np.sqrt(tot[4] / tot[5])

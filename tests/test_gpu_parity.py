@@ -88,6 +88,12 @@ CASES = {
                                            dict(synth.MR_PAPER), 0),
     "ancf_3x3_svk": lambda: (synth.ancf_plate(3), dict(synth.SVK_PAPER), 2),
     "ancf_5x5_mr_kv": lambda: (synth.ancf_plate(5), dict(synth.MR_PAPER, **synth.KV_TIRE), 2),
+    # ANCF3443 on the per-(e,q) table path (more than 4 element shapes: the
+    # lane-per-node group without classes) and the SVK + KV tangent group
+    "ancf_6x6_graded_svk": lambda: (synth.ancf_plate_graded(6), dict(synth.SVK_PAPER), 2),
+    "ancf_4x4_perturbed_svk": lambda: (synth.perturbed(synth.ancf_plate(4), amp=0.02), dict(synth.SVK_PAPER), 2),
+    "ancf_5x5_graded_svk_kv": lambda: (synth.ancf_plate_graded(5), dict(synth.SVK_PAPER, **synth.KV_TIRE), 2),
+    "ancf_4x4_svk_kv": lambda: (synth.ancf_plate(4), dict(synth.SVK_PAPER, **synth.KV_TIRE), 2),
     # ANCF3243 beam (NEXT-1): 16 elements = one CTA tile; 9 = ragged tile
     "beam_16_svk": lambda: (synth.ancf_beam(16), dict(synth.SVK_PAPER), 3),
     "beam_9_mr_kv": lambda: (synth.ancf_beam(9), dict(synth.MR_PAPER, **synth.KV_TIRE), 3),
@@ -117,7 +123,7 @@ def test_eval_parity(torch_cuda, case):
     check_pattern(ctx, pr)
     # congruent (Kuhn / uniform plate) meshes use shared-memory geometry classes,
     # perturbed meshes the per-(e,q) tables
-    if "perturbed" in case:
+    if "perturbed" in case or "graded" in case:
         assert ctx.info["n_geometry_classes"] == 0
     elif mesh.element == 0 and mesh.n_el >= 6:
         assert ctx.info["n_geometry_classes"] == 6
@@ -192,6 +198,23 @@ def test_constitutive_hook(torch_cuda, model):
     for i in range(n):
         assert rel(P[i], oracle.pk1(model, mat, F[i], Fd[i]).ravel()) <= 1e-13
         assert rel(A[i], oracle.tangent(model, mat, F[i]).ravel()) <= 1e-12
+
+
+@pytest.mark.parametrize("case", ["ancf_6x6_graded_svk", "ancf_4x4_perturbed_svk", "ancf_5x5_graded_svk_kv",
+                                  "ancf_4x4_svk_kv", "ancf_3x3_svk", "t10_100el_perturbed_svk_keast5",
+                                  "t10_5x3x1_svk_keast5_ragged"])
+def test_force_only_parity(torch_cuda, case):
+    """tlfea_force_only (the AdamW inner evaluation) on the class and the
+    per-(e,q) table paths, with and without Kelvin-Voigt."""
+    torch = torch_cuda
+    import paper_2604_10357_b200 as T
+    mesh, mat, rule = CASES[case]()
+    x, v, vn, fext = state(mesh)
+    pr = oracle.Problem(mesh, mat, rule)
+    _, _, f0 = pr.eval(x, v, vn, None, 1e-3, hessian=False)
+    ctx = T.Context.from_mesh(mesh, mat, rule)
+    f = ctx.force_only(dev(torch, x), dev(torch, v)).cpu().numpy()
+    assert rel(f, f0) <= TOL, rel(f, f0)
 
 
 def test_many_body_force_only(torch_cuda):

@@ -148,3 +148,39 @@ def test_virtual_partition_scattered_tangent(torch_cuda, case):
                 assert np.array_equal(r["cols"][a0:a1], pr.cols[b0:b1])
                 H[b0:b1] = r["H"][a0:a1]
     assert rel(g, g0) <= TOL and rel(H, H0) <= TOL
+
+
+@pytest.mark.parametrize("scattered", [False, True])
+def test_partitioned_slot_map_vs_global(torch_cuda, scattered):
+    """Reading Q16 on partitioned contexts: a rank's slot map (its local
+    elements, ascending global id) holds indices into ITS owned-row CSR (the H
+    it writes) and -1 for rows another rank owns. Mapped through the owned
+    rows' global CSR offsets, every entry equals the oracle's global slot map."""
+    import paper_2604_10357_b200 as T
+    mesh, mat, rule = synth.kuhn_t10_box(4, 3, 2, 0.8, 0.6, 0.4), dict(synth.SVK_PAPER), 1
+    P = 3
+    part = ((np.arange(mesh.n_el) % P) if scattered else (np.arange(mesh.n_el) * P // mesh.n_el)).astype(np.int32)
+    pr = oracle.Problem(mesh, mat, rule)
+    sm0 = pr.slot_map()
+    cc = mesh.coef_conn().astype(np.int64)
+    covered = np.zeros(sm0.shape, bool)
+    for r in range(P):
+        ctx = T.Context.from_mesh(mesh, mat, rule, rank=r, nranks=P, elem_part=part)
+        rowptr, _, _, _, owned = [t.cpu().numpy().astype(np.int64) for t in ctx.export_pattern()]
+        local = np.nonzero(part == r)[0]
+        sm = ctx.slot_map().astype(np.int64)
+        assert sm.shape[0] == local.size
+        loc_row = -np.ones(mesh.n_coef, np.int64)
+        loc_row[owned] = np.arange(owned.size)
+        for k, e in enumerate(local):
+            for a in range(10):
+                i = loc_row[cc[e, a]]
+                for d in range(3):
+                    row = sm[k, 3 * a + d]
+                    if i < 0:
+                        assert np.all(row == -1)
+                        continue
+                    glob = pr.rowptr[3 * cc[e, a] + d] + (row - rowptr[3 * i + d])
+                    assert np.array_equal(glob, sm0[e, 3 * a + d])
+                    covered[e, 3 * a + d] = True
+    assert covered.mean() > 0.3   # rows its own rank owns: all on a contiguous partition, fewer when scattered

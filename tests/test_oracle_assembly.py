@@ -320,3 +320,27 @@ def test_paper_sizes():
         assert synth.SVK_PAPER[k] == GOLD["svk_scaling_material"][k]
     for k in ("C10", "C01", "kappa", "rho0"):
         assert synth.MR_PAPER[k] == GOLD["mr_material"][k]
+
+
+def test_pattern_counts_configs_2_and_3():
+    """SURVEY §8(c) pattern pins for the two large Kuhn boxes (config 2:
+    nnz_H = 34,979,121; config 3: 1,384,065,801), without building their
+    patterns: on a Kuhn box every coefficient pair belongs to an interior,
+    face, edge or corner class of the cell lattice, so nnz_c is a trilinear
+    polynomial in the cell counts (nx, ny, nz) once each is >= 2 (no two
+    boundary layers overlap). Fit it exactly on the 8 boxes {3,4}^3 with the
+    oracle's brute-force pattern, check it on boxes outside the fit, evaluate."""
+    def nnz_c(n):
+        return oracle.Problem(synth.kuhn_t10_box(*n, 1.0, 1.0, 1.0), SVK, 1).nnz_c
+
+    def row(n):
+        x, y, z = n
+        return [1, x, y, z, x * y, x * z, y * z, x * y * z]
+
+    fit = [(a, b, c) for a in (3, 4) for b in (3, 4) for c in (3, 4)]
+    coef = np.linalg.solve(np.array([row(n) for n in fit], float), np.array([nnz_c(n) for n in fit], float))
+    coef = np.round(coef * 6) / 6  # the class counts are integers per cell, edge and face
+    for n in ((5, 3, 4), (2, 6, 3), (7, 2, 2)):
+        assert round(float(np.dot(row(n), coef))) == nnz_c(n), n
+    assert 9 * round(float(np.dot(row((42, 28, 14)), coef))) == 34_979_121
+    assert 9 * round(float(np.dot(row((144, 96, 48)), coef))) == 1_384_065_801
