@@ -139,54 +139,44 @@ def workload(cfg_idx: int):
     return cfg, mesh, x, v, vn, fext
 
 
-def bytes_per_element(mesh, info, tangent: bool, kv: bool):
-    """Algorithmic bytes per element of the dominant (element) kernel in the
-    paper's per-(e,q) layout: connectivity,
-    reference gradients + J0 w, the unique gathered coordinates (and
-    velocities), and its outputs (element force + upper tangent blocks)."""
+def alg_bytes_per_element(mesh, info, tangent: bool, kv: bool, layout: str = "paper"):
+    """SURVEY §8(d) algorithmic bytes per element of the whole path (what
+    must cross HBM with no intermediate at all): the unique gathers of x (and
+    v, v_n, f_ext for the residual; v alone when Kelvin-Voigt drives a
+    force-only evaluation), the unique f/g write, the unique full-pattern H
+    write, the connectivity (4 B per physical node), a coefficient-level slot
+    map (4 n_en^2 B, tangent only) and the reference data: per-(e,q) grad N +
+    J0 w ("paper" layout) or the "min" layout (13 fp64 per affine
+    T10 element; one shared table for a uniform ANCF plate or beam). Config 3
+    gives 4,624 (paper) / 3,488 (min) B/el, config 5 1,365 / 229, the 200x200
+    ANCF plate 30,741 / 11,925, as in §8(d)'s table."""
     nen, nq = info["n_en"], info["n_qp"]
-    nub = nen * (nen + 1) // 2
-    coords = 24.0 * mesh.n_coef / mesh.n_el * (2 if kv else 1)
-    # reference data: per-(e,q) tables (paper layout) or, with geometry
-    # classes, one class id per element (tables staged in shared memory)
-    ref = 1 if info.get("n_geometry_classes", 0) > 0 else 8 * nq * (3 * nen + 1)
-    b = 4 * nen + ref + coords + 24 * nen
+    per_coef = mesh.n_coef / mesh.n_el
+    n_phys = {0: 10, 1: 4, 2: 2}[int(mesh.element)]
+    b = 4 * n_phys
+    b += per_coef * 24 * (4 if tangent else (2 if kv else 1))   # x, v, v_n, f_ext | x (, v)
+    b += per_coef * 24                                          # f / g
     if tangent:
-        b += 72 * nub + 4 * nub   # upper blocks + their gather-sorted destinations
+        b += 8 * info["nnz"] / mesh.n_el + 4 * nen * nen          # H values, slot map
+    if layout == "paper":
+        b += 8 * nq * (3 * nen + 1)
+    elif int(mesh.element) == 0:
+        b += 8 * 13
     return b
 
 
-def fused_bytes_per_element(mesh, info, kv: bool):
-    """Algorithmic bytes per element of the fused persistent eval (the whole
-    tangent path in one kernel): what must cross
-    HBM with no intermediate at all — connectivity, one class id, the unique
-    gathers of x (v) and of v, v_n, f_ext for the residual, the unique g and
-    f_int writes, the H values, and the mass row (values + columns) the
-    residual reads. The element scratch round trip is NOT counted: it is the
-    implementation's cost and shows up as `traffic` above these bytes."""
-    nen = info["n_en"]
-    per_node = mesh.n_coef / mesh.n_el
-    b = 4 * nen + 1
-    b += per_node * 24 * 4                 # x, v (also Fdot when KV), v_n, f_ext
-    b += per_node * 24 * 2                 # g, f_int
-    b += 8 * info["nnz"] / mesh.n_el       # H
-    b += 12 * info["nnz_coef"] / mesh.n_el  # M values + column ids
-    return b
-
-
-def path_bytes_per_element(mesh, info, tangent: bool, kv: bool):
-    """Algorithmic bytes per element of the whole path (SURVEY §8(d) 'paper
-    layout' accounting): unique gathers of x, v, v_n, f_ext, the unique f/g
-    write, the unique full-pattern H write, connectivity, a coefficient-level
-    slot map and the per-(e,q) reference data."""
-    nen, nq = info["n_en"], info["n_qp"]
-    per_node = mesh.n_coef / mesh.n_el
-    b = 4 * nen + 8 * nq * (3 * nen + 1) + 4 * nen * nen
-    b += per_node * 24 * (4 if tangent else (2 if kv else 1))   # x, v, v_n, f_ext
-    b += per_node * 24 * (2 if tangent else 1)                   # f_int (+ g)
+def alg_flops_per_element(mesh, info, tangent: bool, model: int):
+    """SURVEY §8(d) flops per element: exact structured-SVK counts per
+    quadrature point (468 force / 4,420 force + symmetric tangent for T10,
+    684 / 10,252 ANCF3443; the beam scaled from them), plus the M/h term of H
+    (0.4 kflop/el T10, 1 kflop/el ANCF); Mooney-Rivlin + KV: §8(d)'s model."""
+    elem = {0: "t10", 1: "ancf", 2: "beam"}[int(mesh.element)]
+    if elem == "t10" and model == 1 and tangent:
+        return float(FLOP_PER_QP_MR_T10 * info["n_qp"])
+    f = FLOP_PER_QP[(elem, tangent)] * info["n_qp"]
     if tangent:
-        b += 8 * info["nnz"] / mesh.n_el                         # H values
-    return b
+        f += 400 if elem == "t10" else 1000
+    return float(f)
 
 
 # ---------------------------------------------------------- CPU oracle --
@@ -222,20 +212,61 @@ def oracle_slice(cfg_idx: int, target_el: int):
     return cfg, m, x, v, vn, fext, f"whole mesh ({m.n_el} elements)"
 
 
-def time_oracle(cfg_idx: int, target_el: int, reps: int = 1):
+def time_oracle(cfg_idx: int, target_el: int, reps: int = 1, all_cores: bool = False):
     import oracle
     cfg, sub, x, v, vn, fext, desc = oracle_slice(cfg_idx, target_el)
     pr = oracle.Problem(sub, cfg.material, cfg.quadrature, with_precompute=False)
     ts = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        pr.eval(x, v, vn, fext, cfg.h, hessian=not cfg.force_only)
+        pr.eval(x, v, vn, fext, cfg.h, hessian=not cfg.force_only, all_cores=all_cores)
         ts.append(time.perf_counter() - t0)
     return sub.n_el, ts, desc
 
 
-def cpu_cores_used():
-    return 1  # the oracle is single-threaded by construction
+def host_info():
+    """CPU model, logical cores available to this process and RAM (GB)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    ram = None
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                ram = round(int(line.split()[1]) / 1024 ** 2, 1)
+    except OSError:
+        pass
+    return {"cpu_model": model, "cores_available": len(os.sched_getaffinity(0)), "ram_gb": ram}
+
+
+def cpu_baseline(cfg_idx: int):
+    """the oracle as it stands on this host. (ii) all cores
+    (OpenMP element loop, thread-private element blocks merged in element
+    order: bitwise the serial oracle) = the CPU-baseline figure; (i) one core
+    beside it. Bounded samples (a few seconds of oracle work each)."""
+    import oracle
+    target_all = {1: 192, 2: 98784, 3: 331776, 4: 10000, 5: 972000, 6: 500000}[cfg_idx]
+    target_one = {1: 192, 2: 13824, 3: 27648, 4: 1600, 5: 97200, 6: 50000}[cfg_idx]
+    cfg, sub, x, v, vn, fext, desc = oracle_slice(cfg_idx, target_all)
+    pr = oracle.Problem(sub, cfg.material, cfg.quadrature, with_precompute=False)
+    t0 = time.perf_counter()
+    pr.eval(x, v, vn, fext, cfg.h, hessian=not cfg.force_only, all_cores=True)
+    t_all = time.perf_counter() - t0
+    cores = oracle.max_threads()
+    cfg1, sub1, x1, v1, vn1, fext1, desc1 = oracle_slice(cfg_idx, target_one)
+    pr1 = oracle.Problem(sub1, cfg1.material, cfg1.quadrature, with_precompute=False)
+    t0 = time.perf_counter()
+    pr1.eval(x1, v1, vn1, fext1, cfg1.h, hessian=not cfg1.force_only)
+    t_one = time.perf_counter() - t0
+    return {"value": sub.n_el / t_all, "unit": "elements/s", "cores": cores, "kind": "oracle",
+            "sample": desc, "seconds": t_all,
+            "one_core": {"value": sub1.n_el / t_one, "sample": desc1, "seconds": t_one},
+            "host": host_info()}
 
 
 # ----------------------------------------------------------- reference arm --
@@ -244,10 +275,10 @@ def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
+    import oracle
     cfg_idx = args.config
-    target = {1: 192, 2: 30000, 3: 40000, 4: 60, 5: 20000, 6: 30000}[cfg_idx]
-    n_el, _, desc = time_oracle(cfg_idx, target, reps=0)
-    _, ts, _ = time_oracle(cfg_idx, target, reps=args.warmup + args.steps)
+    target = {1: 192, 2: 98784, 3: 165888, 4: 10000, 5: 486000, 6: 250000}[cfg_idx]
+    n_el, ts, desc = time_oracle(cfg_idx, target, reps=args.warmup + args.steps, all_cores=True)
     ts = ts[args.warmup:]
     sec = sum(ts) / len(ts)
     value = n_el / sec
@@ -256,8 +287,9 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": cfg.name, "sample": desc},
-            "cpu_baseline": {"value": value, "unit": "elements/s", "cores": cpu_cores_used(), "kind": "oracle",
-                             "sample": desc},
+            "cpu_baseline": {"value": value, "unit": "elements/s", "cores": oracle.max_threads(), "kind": "oracle",
+                             "sample": desc + " (all-core OpenMP element loop, bitwise the serial oracle)",
+                             "host": host_info()},
             "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -292,6 +324,12 @@ def run_ours(args):
     t_setup = time.perf_counter() - t_setup
     info = ctx.info
     dev = torch.device("cuda", local)
+    # accounting on the GLOBAL mesh (a rank's info holds its owned-row nnz)
+    ginfo = dict(info)
+    if world > 1:
+        t_nnz = torch.tensor([float(info["nnz"])], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t_nnz, op=dist.ReduceOp.SUM)
+        ginfo["nnz"] = int(t_nnz.item())
     d = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     xd, vd, vnd, fed = d(x), d(v), d(vn), d(fext)
     g, H, f = ctx.empty_outputs()
@@ -353,51 +391,44 @@ def run_ours(args):
     ms_step = ms_total / args.steps
     value = mesh.n_el / (ms_step / 1e3)
 
-    # --- roofline of the dominant kernel (live CUDA events on its stream)
+    # --- roofline of the dominant kernel (live CUDA events on its stream):
+    # achieved = SURVEY §8(d) algorithmic bytes (flops) per element x the
+    # elements one launch processes / the launch's average duration
     hbm_peak, hbm_src = peaks()
     dom = max(kt, key=lambda k: kt[k][1])
     n_l, ms_l = kt[dom]
     avg_ms = ms_l / max(n_l, 1)
-    elem = {0: "t10", 1: "ancf", 2: "beam"}[int(mesh.element)]
-    if dom == "element":
-        bpe = bytes_per_element(mesh, info, not force_only, kv)
-        bytes_launch = bpe * info["n_elements"]
-        per_qp = FLOP_PER_QP[(elem, not force_only)]
-        if elem == "t10" and cfg.material["model"] == 1 and not force_only:
-            per_qp = FLOP_PER_QP_MR_T10
-        flops_launch = per_qp * info["n_qp"] * info["n_elements"]
-    elif dom == "fused":
-        bytes_launch = fused_bytes_per_element(mesh, info, kv) * info["n_elements"]
-        flops_launch = (FLOP_PER_QP[(elem, True)] * info["n_qp"] * info["n_elements"]
-                        + 9 * info["n_elements"] * info["n_en"] ** 2)
-    elif dom == "gather_H":
-        nnz_c = info["nnz_coef"]
-        contrib = info["n_elements"] * info["n_en"] ** 2
-        bytes_launch = nnz_c * (4 + 4 + 8 + 72) + contrib * (4 + 72) + 4 * info["n_owned_nodes"]
-        flops_launch = 9 * contrib
-    else:
-        bytes_launch = 24 * info["n_elements"] * info["n_en"]
-        flops_launch = 3 * info["n_elements"] * info["n_en"]
+    n_loc = info["n_elements"]
+    model = int(cfg.material["model"])
+    b_paper = alg_bytes_per_element(mesh, ginfo, not force_only, kv, "paper")
+    b_min = alg_bytes_per_element(mesh, ginfo, not force_only, kv, "min")
+    fl_el = alg_flops_per_element(mesh, ginfo, not force_only, model)
+    bytes_launch, flops_launch = b_paper * n_loc, fl_el * n_loc
     gbs = bytes_launch / (avg_ms / 1e3) / 1e9
     tfl = flops_launch / (avg_ms / 1e3) / 1e12
-    fp64_pk, fp64_src = fp64_peak()
-    f_hbm, f_fp64 = gbs / hbm_peak, tfl / fp64_pk
+    fp64_meas, fp64_src = fp64_peak()
+    f_hbm, f_fp64 = gbs / hbm_peak, tfl / FP64_NOMINAL_TFLOPS
+    mode = "force_only" if force_only else "force+tangent"
+    layout = "tables" if info["n_geometry_classes"] == 0 else "classes"
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(f"{cfg.name}:{dom}")
+            traffic = json.load(open(prof)).get(f"{cfg.name}|{mode}|{args.hessian}|{layout}|{dom}")
         except Exception:
             traffic = None
+    common = {"traffic": traffic, "traffic_over_alg": (traffic / bytes_launch if traffic else None),
+              "kernel": dom, "kernel_ms": avg_ms, "alg_bytes_per_el": b_paper, "alg_bytes_per_el_min": b_min,
+              "alg_flops_per_el": fl_el, "hbm_frac": f_hbm, "hbm_frac_min_layout": b_min * n_loc / (avg_ms / 1e3)
+              / 1e9 / hbm_peak, "fp64_frac": f_fp64, "fp64_frac_of_measured": tfl / fp64_meas,
+              "fp64_peak_measured": fp64_meas, "fp64_peak_measured_source": fp64_src}
     if f_hbm >= f_fp64:
         roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": f_hbm,
-                "traffic": traffic, "peak_source": hbm_src}
+                "peak_source": hbm_src, **common}
     else:
-        roof = {"bound": "alu", "achieved": tfl, "peak": fp64_pk, "unit": "TFLOP/s", "frac": f_fp64,
-                "traffic": traffic, "peak_source": fp64_src}
-    roof.update({"kernel": dom, "kernel_ms": avg_ms, "hbm_frac": f_hbm, "fp64_frac": f_fp64,
-                 "alg_bytes_per_launch": bytes_launch, "alg_flops_per_launch": flops_launch})
-    path_b = path_bytes_per_element(mesh, info, not force_only, kv) * mesh.n_el
+        roof = {"bound": "alu", "achieved": tfl, "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s", "frac": f_fp64,
+                "peak_source": "DFMA unit count: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md)", **common}
+    path_b = b_paper * mesh.n_el
     kernels = {k: {"launches": c, "ms_per_launch": (m / c if c else 0.0), "share": (m / ms_total if ms_total else 0)}
                for k, (c, m) in kt.items()}
 
@@ -421,11 +452,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        # ~10-15 s of 1-core oracle work (whole mesh where it is smaller)
-        target = {1: 192, 2: 98784, 3: 250000, 4: 18500, 5: 1944000, 6: 235000}[args.config]
-        n_el_s, ts, desc = time_oracle(args.config, target)
-        cpu = {"value": n_el_s / ts[0], "unit": "elements/s", "cores": cpu_cores_used(), "kind": "oracle",
-               "sample": desc, "seconds": ts[0]}
+        cpu = cpu_baseline(args.config)
 
     if rank == 0:
         line = {
@@ -433,7 +460,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": cfg.name, "n_elements": mesh.n_el, "nnz_H": int(info["nnz"]) if world == 1 else None,
+            "config": {"workload": cfg.name, "n_elements": mesh.n_el, "nnz_H": int(ginfo["nnz"]),
                        "quadrature": ["t10_4pt", "keast5", "gl443", "gl322"][cfg.quadrature],
                        "material": ["svk", "mooney_rivlin"][cfg.material["model"]] + ("+kv" if kv else ""),
                        "path": "force_only" if force_only else "force+tangent+residual (tlfea_eval)",
@@ -441,9 +468,12 @@ def run_ours(args):
                        "parallelism": f"element-partition x{world}" if world > 1 else "1 GPU",
                        "geometry_classes": info["n_geometry_classes"],
                        "l2": "inputs/outputs larger than L2 (no flush needed)",
-                       "nnz_per_s": 9 * info["nnz_coef"] * world / (ms_step / 1e3) if world == 1 else None,
+                       "nnz_per_s": ginfo["nnz"] / (ms_step / 1e3) if not force_only else None,
                        "path_hbm_frac": path_b / (ms_step / 1e3) / 1e9 / hbm_peak,
-                       "path_alg_bytes_per_el": path_b / mesh.n_el, "setup_s": t_setup,
+                       "path_hbm_frac_min_layout": b_min * mesh.n_el / (ms_step / 1e3) / 1e9 / hbm_peak,
+                       "path_alg_bytes_per_el": b_paper, "path_alg_bytes_per_el_min": b_min,
+                       "path_fp64_frac": fl_el * mesh.n_el / (ms_step / 1e3) / 1e12 / FP64_NOMINAL_TFLOPS,
+                       "setup_s": t_setup,
                        "kernels": kernels},
             "roofline": roof,
             "cpu_baseline": cpu,

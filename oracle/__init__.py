@@ -25,20 +25,25 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "tlfea_oracle.cpp")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
 _lock = threading.Lock()
 _lib = None
+_lib_omp = None
 
 MAT_FIELDS = ("E", "nu", "C10", "C01", "kappa", "rho0", "eta_damp", "lambda_damp")
 
 
-def build(force: bool = False) -> str:
-    """Compile the oracle (g++, fp64, no FMA contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
+def build(force: bool = False, openmp: bool = False) -> str:
+    """Compile the oracle (g++, fp64, no FMA contraction). openmp: the same
+    source with -fopenmp (liboracle_omp.so, the all-core CPU baseline: only
+    orc_eval_chunked runs on several threads)."""
+    out = _LIB_OMP if openmp else _LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        tmp = out + f".tmp{os.getpid()}"
         subprocess.check_call(["g++", "-O2", "-ffp-contract=off", "-std=c++17", "-shared",
-                               "-fPIC", "-o", tmp, _SRC])
-        os.replace(tmp, _LIB)
-    return _LIB
+                               "-fPIC", *(["-fopenmp"] if openmp else []), "-o", tmp, _SRC])
+        os.replace(tmp, out)
+    return out
 
 
 def lib():
@@ -48,6 +53,20 @@ def lib():
             _lib = C.CDLL(build())
             _declare(_lib)
     return _lib
+
+
+def lib_omp():
+    """The OpenMP build (all-core element loop of orc_eval_chunked)."""
+    global _lib_omp
+    with _lock:
+        if _lib_omp is None:
+            _lib_omp = C.CDLL(build(openmp=True))
+            _declare(_lib_omp)
+    return _lib_omp
+
+
+def max_threads() -> int:
+    return int(lib_omp().orc_max_threads())
 
 
 _d = C.POINTER(C.c_double)
@@ -89,6 +108,8 @@ def _declare(L):
     L.orc_force_from_stress.argtypes = [i, i, i64, _i32, _d, _d, _d, i64, _d]
     L.orc_eval.argtypes = [i, i, i, _d, i64, _i32, i64, _d, _d, _i64, _i64, _d, _d, _i64, _i64,
                            _d, _d, _d, _d, d, _d, _d, _d]
+    L.orc_eval_chunked.argtypes = L.orc_eval.argtypes
+    L.orc_max_threads.restype = i
     L.orc_eval_rows.argtypes = [i, i, i, i, _d, _i32, _d, _d, _d, _d, d, i64, _i64, _i64, _i64,
                                 i64, _i64, _d, _d, _d]
     L.orc_eval_rows.restype = i64
@@ -345,15 +366,19 @@ class Problem:
                                     _p(self.dims), _p(_f64(P)), self.n_coef, _p(f))
         return f
 
-    def eval(self, x, v, vn=None, fext=None, h=1e-3, hessian=True, use_fff=True, lam=None, rho=0.0):
+    def eval(self, x, v, vn=None, fext=None, h=1e-3, hessian=True, use_fff=True, lam=None, rho=0.0,
+             all_cores=False):
         """Returns (g, H or None, f_int) on the full DOF pattern. With
         constraints: g += h C^T (lam + rho c(x)) (Eq. residual P:101-113,
-        P:484-489) and H += h^2 rho C^T C (Eq. hessian)."""
+        P:484-489) and H += h^2 rho C^T C (Eq. hessian).
+        all_cores: the element loop on every host core (orc_eval_chunked of
+        the OpenMP build; bitwise equal to the serial evaluation)."""
         nd = 3 * self.n_coef
         g = np.zeros(nd)
         fint = np.zeros(nd)
         H = np.zeros(self.nnz) if hessian else None
-        lib().orc_eval(self.elem, self.rule, self.model, _p(self.matv), self.n_el,
+        fn = lib_omp().orc_eval_chunked if all_cores else lib().orc_eval
+        fn(self.elem, self.rule, self.model, _p(self.matv), self.n_el,
                        _p(self.conn, _i32), self.n_coef, _p(self.X), _p(self.dims),
                        _p(self.rowptr_c, _i64), _p(self.cols_c, _i64), _p(self.M),
                        _p(self.fff if use_fff else None), _p(self.rowptr, _i64),

@@ -5,7 +5,9 @@
 // bench.py's cpu_baseline / --impl reference legs may load this library. The
 // product path (paper_2604_10357_b200 / libtlfea.so) never imports, links or
 // calls it, and it shares no code, header, table or helper with the CUDA
-// sources. Build: g++ -O2 -ffp-contract=off -std=c++17 -shared -fPIC.
+// sources. Build: g++ -O2 -ffp-contract=off -std=c++17 -shared -fPIC (the
+// all-core CPU baseline: the same source with -fopenmp, liboracle_omp.so;
+// only orc_eval_chunked then runs its element loop on several threads).
 //
 // Citations: "P:n" = line n of PAPER.md (section / equation named); "Qn" =
 // reading n of DESIGN.md (= SURVEY §8(c) table). Every function follows the
@@ -25,6 +27,9 @@
 #include <cstdint>
 #include <cstring>
 #include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 namespace {
 
@@ -919,6 +924,93 @@ void orc_eval(int elem, int rule, int model, const double* mat, int64_t n_el, co
         const int64_t i = 3 * I + d;
         g[i] = s / h + fint[i] - (fext ? fext[i] : 0.0) - (fff ? fff[i] : 0.0);
       }
+}
+
+// The same evaluation with the element routine run on all host cores
+// (the all-core CPU baseline): elements are computed in
+// chunks, in parallel (OpenMP build liboracle_omp.so; a plain build runs the
+// loop serially), each into its own slot of a chunk buffer (thread-private
+// element blocks), and the chunk is then assembled in ascending element order
+// exactly as orc_eval does. The arithmetic and the summation order are those
+// of orc_eval, so the results are bitwise equal to it.
+void orc_eval_chunked(int elem, int rule, int model, const double* mat, int64_t n_el, const int32_t* conn,
+                      int64_t n_coef, const double* X, const double* dims, const int64_t* rowptr_c,
+                      const int64_t* cols_c, const double* M, const double* fff, const int64_t* rowptr,
+                      const int64_t* cols, const double* x, const double* v, const double* vn,
+                      const double* fext, double h, double* g, double* H, double* fint) {
+  const int nen = n_en_of(elem), nd = 3 * nen;
+  const int64_t ndof = 3 * n_coef, chunk = 2048;
+  for (int64_t i = 0; i < ndof; ++i) fint[i] = 0.0;
+  if (H)
+    for (int64_t p = 0; p < rowptr[ndof]; ++p) H[p] = 0.0;
+  std::vector<double> fe((size_t)chunk * nd), Ke(H ? (size_t)chunk * nd * nd : 0);
+  for (int64_t e0 = 0; e0 < n_el; e0 += chunk) {
+    const int64_t ne = std::min(chunk, n_el - e0);
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t k = 0; k < ne; ++k) {
+      int64_t cf[16];
+      elem_coefs(elem, conn, e0 + k, cf);
+      element_fK(elem, rule, model, mat, X, cf, dims_of(elem, dims, e0 + k), x, v, &fe[(size_t)k * nd],
+                 H ? &Ke[(size_t)k * nd * nd] : nullptr);
+    }
+    // merge: thread th owns the nodes I with I % nt == th and adds the chunk's
+    // element blocks to their rows in ascending element order (the serial order)
+#pragma omp parallel
+    {
+      int nt = 1, th = 0;
+#ifdef _OPENMP
+      nt = omp_get_num_threads();
+      th = omp_get_thread_num();
+#endif
+      for (int64_t k = 0; k < ne; ++k) {
+        int64_t cf[16];
+        elem_coefs(elem, conn, e0 + k, cf);
+        const double* fk = &fe[(size_t)k * nd];
+        const double* Kk = H ? &Ke[(size_t)k * nd * nd] : nullptr;
+        for (int a = 0; a < nen; ++a)
+          for (int d = 0; d < 3; ++d) {
+            const int64_t r = 3 * cf[a] + d;
+            if (cf[a] % nt != th) continue;
+            fint[r] += fk[3 * a + d];
+            if (H)
+              for (int b = 0; b < nen; ++b)
+                for (int f = 0; f < 3; ++f) {
+                  const int64_t p = find_col(cols, rowptr[r], rowptr[r + 1], 3 * cf[b] + f);
+                  H[p] += h * Kk[(3 * a + d) * nd + 3 * b + f];
+                }
+          }
+      }
+    }
+  }
+  if (H)
+#pragma omp parallel for schedule(static)
+    for (int64_t I = 0; I < n_coef; ++I)
+      for (int64_t k = rowptr_c[I]; k < rowptr_c[I + 1]; ++k)
+        for (int d = 0; d < 3; ++d) {
+          const int64_t r = 3 * I + d;
+          const int64_t p = find_col(cols, rowptr[r], rowptr[r + 1], 3 * cols_c[k] + d);
+          H[p] += M[k] / h;
+        }
+  if (g)
+#pragma omp parallel for schedule(static)
+    for (int64_t I = 0; I < n_coef; ++I)
+      for (int d = 0; d < 3; ++d) {
+        double s = 0.0;
+        for (int64_t k = rowptr_c[I]; k < rowptr_c[I + 1]; ++k) {
+          const int64_t J = cols_c[k];
+          s += M[k] * (v[3 * J + d] - (vn ? vn[3 * J + d] : 0.0));
+        }
+        const int64_t i = 3 * I + d;
+        g[i] = s / h + fint[i] - (fext ? fext[i] : 0.0) - (fff ? fff[i] : 0.0);
+      }
+}
+
+int orc_max_threads() {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
 }
 
 // Sampled rows (for parity at sizes the full oracle cannot hold): for each

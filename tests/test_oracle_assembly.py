@@ -344,3 +344,21 @@ def test_pattern_counts_configs_2_and_3():
         assert round(float(np.dot(row(n), coef))) == nnz_c(n), n
     assert 9 * round(float(np.dot(row((42, 28, 14)), coef))) == 34_979_121
     assert 9 * round(float(np.dot(row((144, 96, 48)), coef))) == 1_384_065_801
+
+
+def test_all_core_oracle_equals_serial():
+    """The all-core CPU baseline (OpenMP element loop, thread-private element
+    blocks assembled in element order) is bitwise the serial oracle."""
+    for mesh, mat, rule in ((synth.kuhn_t10_box(4, 3, 2, 0.8, 0.6, 0.4), SVK, 1),
+                            (synth.ancf_plate(3), SVK, 2)):
+        pr = oracle.Problem(mesh, mat, rule)
+        if mesh.element == 0:
+            x, v, vn, fe = synth.t10_state(mesh, with_fext=True)
+        else:
+            x, v, vn = synth.ancf_state(mesh)
+            fe = None
+        a = pr.eval(x, v, vn, fe, 1e-3)
+        b = pr.eval(x, v, vn, fe, 1e-3, all_cores=True)
+        for u, w in zip(a, b):
+            assert np.array_equal(u, w)
+    assert oracle.max_threads() >= 1
