@@ -487,6 +487,99 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# --------------------------------------------------------------- ladder --
+
+LADDER_T10 = ((3, 2, 1), (6, 4, 2), (9, 6, 3), (15, 10, 5), (24, 16, 8), (39, 26, 13))
+LADDER_ANCF = (10, 20, 50, 100, 150, 200)
+LADDER_BEAM = (1000, 10000, 50000, 100000, 200000, 500000)
+RES = ("RES0", "RES2", "RES4", "RES8", "RES16", "RES32")
+
+
+def run_ladder(args):
+    """north_star: throughput on synthetic meshes shaped like the paper's
+    six-resolution ladders (T10 Kuhn beams under both rules, the ANCF3443
+    plates, the ANCF3243 chains), force + tangent (tlfea_eval) and force only,
+    with the all-core oracle on the same rung beside each GPU number."""
+    import torch
+
+    import oracle
+    import paper_2604_10357_b200 as T
+    torch.cuda.set_device(0)
+    hbm_peak, _ = peaks()
+    rows = []
+
+    def measure(name, res, mesh, mat, rule, h, force_only):
+        if mesh.element == 0:
+            x, v, vn, fext = synth.t10_state(mesh, with_fext=True)
+        else:
+            x, v, vn = synth.ancf_state(mesh, length=4.0 if mesh.element == 1 else float(mesh.X[:, 0].max()))
+            fext = None
+        ctx = T.Context.from_mesh(mesh, mat, rule)
+        info = ctx.info
+        d = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        xd, vd, vnd, fed = d(x), d(v), d(vn), d(fext)
+        g, H, f = ctx.empty_outputs()
+        step = (lambda: ctx.force_only(xd, None, f)) if force_only else (lambda: ctx.eval(xd, vd, vnd, fed, h, g, H, f))
+        for _ in range(3):
+            step()
+        k = int(max(10, min(200, 4e6 / mesh.n_el)))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(k):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / k
+        kv = False
+        bp = alg_bytes_per_element(mesh, info, not force_only, kv, "paper")
+        bm = alg_bytes_per_element(mesh, info, not force_only, kv, "min")
+        fl = alg_flops_per_element(mesh, info, not force_only, int(mat["model"]))
+        del ctx, g, H, f
+        torch.cuda.empty_cache()
+        # the oracle on the same rung (all cores; the first elements of the
+        # beam's two largest chains, which take it beyond a few seconds)
+        sub, xs, vs, vns, fes = mesh, x, v, vn, fext
+        if mesh.element == 2 and mesh.n_el > 100000:
+            sub = synth.ancf_beam(100000)
+            xs, vs, vns = synth.ancf_state(sub, length=float(mesh.X[:, 0].max()))
+            fes = None
+        pr = oracle.Problem(sub, mat, rule, with_precompute=False)
+        t0 = time.perf_counter()
+        pr.eval(xs, vs, vns, fes, h, hessian=not force_only, all_cores=True)
+        t_or = time.perf_counter() - t0
+        row = {"family": name, "res": res, "n_elements": mesh.n_el, "quadrature": ["t10_4pt", "keast5", "gl443", "gl322"][rule],
+               "path": "force_only" if force_only else "force+tangent+residual", "ms_per_eval": ms,
+               "elements_per_s": mesh.n_el / (ms / 1e3),
+               "nnz_per_s": (info["nnz"] / (ms / 1e3)) if not force_only else None, "nnz_H": info["nnz"],
+               "hbm_frac_paper_layout": bp * mesh.n_el / (ms / 1e3) / 1e9 / hbm_peak,
+               "hbm_frac_min_layout": bm * mesh.n_el / (ms / 1e3) / 1e9 / hbm_peak,
+               "fp64_frac": fl * mesh.n_el / (ms / 1e3) / 1e12 / FP64_NOMINAL_TFLOPS,
+               "geometry_classes": info["n_geometry_classes"],
+               "oracle_all_core_elements_per_s": sub.n_el / t_or, "oracle_sample_elements": sub.n_el,
+               "gpu_over_oracle": (mesh.n_el / (ms / 1e3)) / (sub.n_el / t_or)}
+        print(json.dumps(row), flush=True)
+        rows.append(row)
+
+    svk = dict(synth.SVK_PAPER)
+    for res, (nx, ny, nz) in zip(RES, LADDER_T10):
+        mesh = synth.kuhn_t10_box(nx, ny, nz, 3.0, 2.0, 1.0)
+        for rule in (synth.Q_T10_4PT, synth.Q_T10_KEAST5):
+            for fo in (False, True):
+                measure("t10_kuhn", res, mesh, svk, rule, synth.H_T10, fo)
+    for res, n in zip(RES, LADDER_ANCF):
+        mesh = synth.ancf_plate(n)
+        for fo in (False, True):
+            measure("ancf3443_plate", res, mesh, svk, synth.Q_GL_443, synth.H_ANCF, fo)
+    for res, n in zip(RES, LADDER_BEAM):
+        mesh = synth.ancf_beam(n)
+        for fo in (False, True):
+            measure("ancf3243_beam", res, mesh, svk, synth.Q_GL_322, synth.H_BEAM, fo)
+    host = host_info()
+    print(json.dumps({"ladder": rows, "host": host, "oracle_threads": oracle.max_threads(),
+                      "hbm_peak_gbs": hbm_peak, "fp64_peak_tflops_nominal": FP64_NOMINAL_TFLOPS}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -498,13 +591,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--hessian", choices=["full", "upper"], default="full",
                     help="H storage (full DOF CSR = the headline; upper = NEXT-4 variant)")
+    ap.add_argument("--ladder", action="store_true",
+                    help="the paper's six-resolution ladders (T10, ANCF3443, ANCF3243), one line per rung")
     ap.add_argument("--tables", action="store_true",
                     help="per-(e,q) reference tables in HBM (the paper's layout, as for a mesh of non-congruent "
                          "elements) instead of the shared-memory geometry classes")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.ladder:
+        run_ladder(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

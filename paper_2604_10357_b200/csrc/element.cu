@@ -502,6 +502,10 @@ struct T10Pre {
   int ce;
   int32_t fd;  // force scratch position of (e, a)
 };
+// CLS: class mode (the class id is loaded); table mode never touches A.cls
+// (a compile-time switch: a run-time null test here changed the scheduling of
+// the store loop and cost 7 % of the element kernel).
+template <bool CLS>
 __device__ __forceinline__ void t10_preload(int64_t grp, const ElArgs& A, T10Pre& p) {
   const int lane = threadIdx.x & 31;
   const int g = lane / 10, a = lane % 10;
@@ -514,7 +518,8 @@ __device__ __forceinline__ void t10_preload(int64_t grp, const ElArgs& A, T10Pre
     const int64_t I = A.conn[e * 10 + a];
 #pragma unroll
     for (int i = 0; i < 3; ++i) p.xa[i] = A.x[3 * I + i];
-    if (a == 0 && A.cls) p.ce = A.cls[e];
+    if constexpr (CLS)
+      if (a == 0) p.ce = A.cls[e];
   }
 }
 
@@ -1601,7 +1606,7 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
   const int64_t grp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);  // this warp's element group
   T10Pre pre;
   if constexpr (T2PH && !CLS) t10_stage_tables_async<NQ>(grp, A, s_tab);
-  if constexpr (T2PH) t10_preload(grp, A, pre);
+  if constexpr (T2PH) t10_preload<CLS>(grp, A, pre);
   if (CLS) {
     // all loads of a thread in flight at once (one L2 round trip, not one per element)
     const int tot = A.n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1);
@@ -1628,7 +1633,7 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
     element_group_beam_svk<NQ>(grp, A, s_tab);
   } else if constexpr (V2PH) {
     T10Pre pv;
-    t10_preload(grp, A, pv);
+    t10_preload<CLS>(grp, A, pv);
     element_group_t10svk<NQ, true>(grp, A, s_tab, pv);
   } else if constexpr (M2PH) {
     if constexpr (!CLS) t10_stage_tables<NQ>(grp, A, s_tab);
