@@ -25,6 +25,7 @@ cpu_baseline = the CPU oracle (oracle/, as is, 1 core) on a bounded slice
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -123,9 +124,14 @@ class ClockSampler:
 
 # ------------------------------------------------------------ workloads --
 
-def workload(cfg_idx: int):
+def workload(cfg_idx: int, variant: str = "kuhn"):
     cfg = synth.config(cfg_idx)
     mesh = cfg.mesh
+    if variant == "straight" and mesh.element == 0 and cfg_idx != 5:
+        # the same mesh with randomly displaced corners (straight-sided, no two
+        # elements congruent): the affine (min) layout path
+        mesh = synth.perturbed_straight(mesh)
+        cfg = dataclasses.replace(cfg, name=cfg.name + "_straight", mesh=mesh)
     if cfg_idx == 5:
         mesh, x, v = synth.many_body()
         vn, fext = v.copy(), None
@@ -314,7 +320,7 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg, mesh, x, v, vn, fext = workload(args.config)
+    cfg, mesh, x, v, vn, fext = workload(args.config, args.mesh)
     force_only = cfg.force_only
     kv = cfg.material.get("eta_damp", 0) > 0 or cfg.material.get("lambda_damp", 0) > 0
     t_setup = time.perf_counter()
@@ -409,7 +415,7 @@ def run_ours(args):
     fp64_meas, fp64_src = fp64_peak()
     f_hbm, f_fp64 = gbs / hbm_peak, tfl / FP64_NOMINAL_TFLOPS
     mode = "force_only" if force_only else "force+tangent"
-    layout = "tables" if info["n_geometry_classes"] == 0 else "classes"
+    layout = ["classes", "tables", "affine"][info.get("reference_layout", 1)]
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -467,6 +473,7 @@ def run_ours(args):
                        "hessian_storage": args.hessian,
                        "parallelism": f"element-partition x{world}" if world > 1 else "1 GPU",
                        "geometry_classes": info["n_geometry_classes"],
+                       "reference_layout": ["classes", "per-(e,q) tables", "affine min layout"][info["reference_layout"]],
                        "l2": "inputs/outputs larger than L2 (no flush needed)",
                        "nnz_per_s": ginfo["nnz"] / (ms_step / 1e3) if not force_only else None,
                        "path_hbm_frac": path_b / (ms_step / 1e3) / 1e9 / hbm_peak,
@@ -591,6 +598,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--hessian", choices=["full", "upper"], default="full",
                     help="H storage (full DOF CSR = the headline; upper = NEXT-4 variant)")
+    ap.add_argument("--mesh", choices=["kuhn", "straight"], default="kuhn",
+                    help="straight: the T10 mesh with randomly displaced corners (straight-sided, non-congruent: "
+                         "the affine min layout instead of geometry classes)")
     ap.add_argument("--ladder", action="store_true",
                     help="the paper's six-resolution ladders (T10, ANCF3443, ANCF3243), one line per rung")
     ap.add_argument("--tables", action="store_true",

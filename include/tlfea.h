@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define TLFEA_ABI_VERSION 4
+#define TLFEA_ABI_VERSION 5
 
 typedef struct tlfea_ctx_s* tlfea_ctx;
 
@@ -157,10 +157,15 @@ typedef struct {
                              UPPER: single rank, no constraints. */
   int32_t reference_layout; /* 0 (default): geometry classes when every element
                              is congruent to one of <= 32 (T10) / 4 (ANCF)
-                             reference shapes, else the per-(e,q) tables of
-                             §4.1; 1: the per-(e,q) tables always
-                             (the paper's layout, on any mesh). Results are
-                             the same either way (to rounding). */
+                             reference shapes; else, for straight-sided T10,
+                             the affine "min" layout (13 fp64 per element:
+                             grad_X z_0..3 and J0); else the
+                             per-(e,q) tables of §4.1.
+                             1: the per-(e,q) tables always (the paper's
+                             layout, on any mesh). 2: the affine layout
+                             whenever the T10 mesh is straight-sided (no
+                             classes), else the tables. Results agree to
+                             rounding whichever is used. */
 } tlfea_options;
 
 /* Sizes of a context (tlfea_info). Rows/DOFs are GLOBAL indices; in a
@@ -186,6 +191,8 @@ typedef struct {
                               gather + f/g gather; DESIGN.md §6 records the
                               one-kernel variants measured). */
   int64_t n_constraints;   /* rows m of the context's constraint set (0: none) */
+  int32_t reference_layout;/* in use: 0 geometry classes, 1 per-(e,q) tables,
+                              2 affine (min) layout */
 } tlfea_info_t;
 
 /* ---------------------------------------------------------------- setup -- */

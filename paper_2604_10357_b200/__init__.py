@@ -20,6 +20,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
+ABI_VERSION = 5  # include/tlfea.h TLFEA_ABI_VERSION (struct layouts of this binding)
 LIB_PATH = os.environ.get("TLFEA_LIB") or os.path.join(_HERE, "libtlfea.so")
 _lib = None
 _lock = threading.Lock()
@@ -67,7 +68,8 @@ class Info(C.Structure):
                 ("n_elements", C.c_int64), ("n_elements_global", C.c_int64), ("n_coef", C.c_int64),
                 ("n_dof", C.c_int64), ("nnz_coef", C.c_int64), ("nnz", C.c_int64), ("n_owned_nodes", C.c_int64),
                 ("affine", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32), ("device_bytes", C.c_int64),
-                ("n_geometry_classes", C.c_int32), ("fused_eval", C.c_int32), ("n_constraints", C.c_int64)]
+                ("n_geometry_classes", C.c_int32), ("fused_eval", C.c_int32), ("n_constraints", C.c_int64),
+                ("reference_layout", C.c_int32)]
 
 class AdamWParams(C.Structure):
     _fields_ = [("alpha", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
@@ -134,6 +136,8 @@ def lib():
             L.tlfea_launch_count.restype = C.c_int64
             L.tlfea_last_error.restype = C.c_char_p
             L.tlfea_abi_version.restype = C.c_int32
+            if L.tlfea_abi_version() != ABI_VERSION:
+                raise RuntimeError(f"{LIB_PATH}: ABI {L.tlfea_abi_version()}, binding expects {ABI_VERSION} (rebuild)")
             _lib = L
     return _lib
 
@@ -213,11 +217,12 @@ class Context:
         (tlfea_constraints; NEXT-3). hessian: "full" or "upper" storage of H
         (options.hessian_upper; NEXT-4). reference_layout: "auto" (geometry
         classes when the mesh allows) or "tables" (the paper's per-(e,q)
-        tables always; options.reference_layout)."""
+        tables always) or "affine" (the min layout of straight-sided T10
+        before classes; options.reference_layout)."""
         if hessian not in ("full", "upper"):
             raise ValueError("hessian must be 'full' or 'upper'")
-        if reference_layout not in ("auto", "tables"):
-            raise ValueError("reference_layout must be 'auto' or 'tables'")
+        if reference_layout not in ("auto", "tables", "affine"):
+            raise ValueError("reference_layout must be 'auto', 'tables' or 'affine'")
         L = lib()
         con = None
         if constraints is not None:
@@ -237,7 +242,7 @@ class Context:
         opts = Options(quadrature, mass_rule, (C.c_double * 3)(*gravity), (C.c_double * 3)(0, 0, 0), rank, nranks,
                        None if self._part is None else self._part.ctypes.data_as(C.POINTER(C.c_int32)), device,
                        None if con is None else C.pointer(con), 1 if hessian == "upper" else 0,
-                       1 if reference_layout == "tables" else 0)
+                       {"auto": 0, "tables": 1, "affine": 2}[reference_layout])
         self.material = dict(mat)
         m = make_material(mat)
         h = C.c_void_p()

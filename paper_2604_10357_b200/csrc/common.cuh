@@ -111,7 +111,7 @@ struct Context {
   int64_t n_own = 0;           // owned coefficient rows
   int64_t nnz_c = 0;           // owned-row coefficient nnz
   int affine = 0;
-  int force_tables = 0;         // options.reference_layout = 1: never use geometry classes
+  int force_tables = 0;         // options.reference_layout: 1 tables always, 2 affine (min) layout first
   // H storage: full DOF CSR (9 nnz_c values) or UPPER (col >= row). UPPER row
   // 3I+d starts at ubase[I] + d (3 + 3 L_I) - d (d - 1) / 2, L_I = blocks
   // J > I of coefficient row I; block (I, J) with rank k among J >= I (k = 0:
@@ -145,6 +145,9 @@ struct Context {
   int n_cls = 0;                  // 0 = per-element tables (gradN / J0w above)
   uint8_t* cls = nullptr;         // [n_el] class id
   double* cls_tab = nullptr;      // [n_cls][nq][nen*3 + 1]  (gradN then J0w)
+  // affine (min) layout of straight-sided T10 without classes: [n_el][13] =
+  // grad_X z_0..3 (barycentric gradients), J0 (SURVEY §8(d) min layout)
+  double* aff = nullptr;
   std::vector<int64_t> cls_rep;   // representative (first) element of each class
   // symmetric H gather units (upper blocks + blocks whose transpose is not owned)
   int64_t n_units = 0;

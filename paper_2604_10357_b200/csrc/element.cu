@@ -120,6 +120,7 @@ struct ElArgs {
   const uint8_t* cls;
   const double* cls_tab;
   int n_cls;
+  const double* aff;  // affine (min) layout: [n_el][13] = grad_X z_0..3, J0 (straight-sided T10)
   const double* x;
   const double* v;
   MatDev mat;
@@ -566,6 +567,79 @@ __device__ __forceinline__ void t10_stage_tables_async(int64_t grp, const ElArgs
     const int g = lane / NQ, q = lane - NQ * g;
     pf_cp8(&s_tab[((wib * EPW + g) * NQ + q) * TABW + 3 * NEN], A.J0w + (e0 + g) * NQ + q);
   }
+}
+
+// Min (affine) layout for straight-sided T10 without geometry classes
+// (SURVEY §8(d) "min layout"; P:312-320 with J constant per element): 13 fp64
+// per element, the barycentric gradients grad_X z_i (i = 0..3) and J0 = det J.
+// The warp's 3 elements' tables are generated in shared memory, rows slot =
+// 3 wib + g as in table mode:
+//   corner i: grad N_i = (4 z_i - 1) grad z_i,
+//   edge (a,b): grad N = 4 (z_a grad z_b + z_b grad z_a),  J0 w_q = J0 * w_q
+// (the T10 basis of reading Q2 at the rule's barycentric points).
+template <int NQ>
+__device__ __forceinline__ void t10_rule_point(int q, double z[4], double& w) {
+  if constexpr (NQ == 5) {  // Keast (reading Q1): centroid -2/15, then z_p = 1/2 at point p + 1
+#pragma unroll
+    for (int i = 0; i < 4; ++i) z[i] = q == 0 ? 0.25 : (i == q - 1 ? 0.5 : 1.0 / 6.0);
+    w = q == 0 ? -2.0 / 15.0 : 3.0 / 40.0;
+  } else {  // 4-point degree-2 rule: z_p = (5 + 3 sqrt 5)/20 at point p, (5 - sqrt 5)/20 elsewhere
+    const double r5 = 2.2360679774997896964;
+    const double alpha = 0.25 + 0.15 * r5, beta = 0.25 - 0.05 * r5;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) z[i] = i == q ? alpha : beta;
+    w = 1.0 / 24.0;
+  }
+}
+
+// Load half: lane (element g, point q) of the warp's 3 x NQ fetches its
+// element's 13 values (issued before the conn -> x loads so both overlap).
+struct T10Aff {
+  double gz[4][3];
+  double J0;
+};
+template <int NQ>
+__device__ __forceinline__ void t10_affine_load(int64_t grp, const ElArgs& A, T10Aff& f) {
+  constexpr int EPW = 3;
+  const int lane = threadIdx.x & 31;
+  const int g = lane / NQ;
+  const int64_t e = grp * EPW + g;
+  const bool ok = lane < EPW * NQ && e < A.n_el;
+  const double* a = A.aff + 13 * (ok ? e : 0);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) f.gz[i][k] = ok ? a[3 * i + k] : 0.0;
+  f.J0 = ok ? a[12] : 0.0;
+}
+// Expand half: the lane's table row (grad N_a of the 10 nodes, J0 w_q).
+template <int NQ>
+__device__ __forceinline__ void t10_affine_expand(const T10Aff& f, double* __restrict__ s_tab) {
+  constexpr int NEN = 10, EPW = 3, TABW = 3 * NEN + 1;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (lane < EPW * NQ) {
+    const int g = lane / NQ, q = lane - NQ * g;
+    double z[4], w;
+    t10_rule_point<NQ>(q, z, w);
+    double* t = s_tab + ((wib * EPW + g) * NQ + q) * TABW;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) t[3 * i + k] = (4.0 * z[i] - 1.0) * f.gz[i][k];
+    const int ea[6] = {0, 1, 2, 0, 1, 2}, eb[6] = {1, 2, 0, 3, 3, 3};
+#pragma unroll
+    for (int m = 0; m < 6; ++m)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) t[3 * (4 + m) + k] = 4.0 * (z[ea[m]] * f.gz[eb[m]][k] + z[eb[m]] * f.gz[ea[m]][k]);
+    t[3 * NEN] = f.J0 * w;
+  }
+  __syncwarp();
+}
+template <int NQ>
+__device__ __forceinline__ void t10_stage_affine(int64_t grp, const ElArgs& A, double* __restrict__ s_tab) {
+  T10Aff f;
+  t10_affine_load<NQ>(grp, A, f);
+  t10_affine_expand<NQ>(f, s_tab);
 }
 
 #ifndef TLFEA_T10_2PH_NPASS
@@ -1593,7 +1667,8 @@ __host__ __device__ constexpr int el_minb_k() {
                                                                             : el_minb<ELEM, MODEL, NPASS>();
 }
 
-template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS>
+// AFF: table mode with the tables generated from the affine (min) layout.
+template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS, bool AFF = false>
 __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV, TAN, CLS>()) k_element(ElArgs A) {
   extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
   // (SVK in table mode measured slower two-phase: config 3 without classes 13.97 vs 12.61 ms, force only
@@ -1605,8 +1680,11 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
   constexpr bool V2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && KV && TAN && CLS;  // SVK + Kelvin-Voigt
   const int64_t grp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);  // this warp's element group
   T10Pre pre;
-  if constexpr (T2PH && !CLS) t10_stage_tables_async<NQ>(grp, A, s_tab);
+  if constexpr (T2PH && !CLS && !AFF) t10_stage_tables_async<NQ>(grp, A, s_tab);
+  T10Aff aff;
+  if constexpr (T2PH && AFF) t10_affine_load<NQ>(grp, A, aff);
   if constexpr (T2PH) t10_preload<CLS>(grp, A, pre);
+  if constexpr (T2PH && AFF) t10_affine_expand<NQ>(aff, s_tab);
   if (CLS) {
     // all loads of a thread in flight at once (one L2 round trip, not one per element)
     const int tot = A.n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1);
@@ -1623,10 +1701,11 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
   }
   if constexpr (T2PH) {
     if constexpr (!CLS) pre.ce = (threadIdx.x >> 5) * 3 + (threadIdx.x & 31) / 10;  // staged slot
+    // (affine tables are written synchronously: no cp.async wait before phase A)
     if constexpr (TAN)
-      element_group_t10svk<NQ, false, !CLS>(grp, A, s_tab, pre);
+      element_group_t10svk<NQ, false, !CLS && !AFF>(grp, A, s_tab, pre);
     else
-      element_group_t10svk_force<NQ, !CLS>(grp, A, s_tab, pre);
+      element_group_t10svk_force<NQ, !CLS && !AFF>(grp, A, s_tab, pre);
   } else if constexpr (A2PH) {
     element_group_ancf_svk<NQ>(grp, A, s_tab);
   } else if constexpr (B2PH) {
@@ -1636,7 +1715,10 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
     t10_preload<CLS>(grp, A, pv);
     element_group_t10svk<NQ, true>(grp, A, s_tab, pv);
   } else if constexpr (M2PH) {
-    if constexpr (!CLS) t10_stage_tables<NQ>(grp, A, s_tab);
+    if constexpr (!CLS && AFF)
+      t10_stage_affine<NQ>(grp, A, s_tab);
+    else if constexpr (!CLS)
+      t10_stage_tables<NQ>(grp, A, s_tab);
     element_group_t10mr<NQ, KV>(grp, A, s_tab, !CLS);
   } else
     element_group<ELEM, NQ, MODEL, KV, TAN, CLS, NPASS, TLFEA_DEST_ASYNC != 0>(grp, A, s_tab);
@@ -1813,6 +1895,7 @@ static ElArgs el_args(const Context* c, const double* x, const double* v) {
   A.cls = c->cls;
   A.cls_tab = c->cls_tab;
   A.n_cls = c->n_cls;
+  A.aff = c->aff;
   A.x = x;
   A.v = v;
   A.mat = c->mat;
@@ -1840,6 +1923,15 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
     // the T10 two-phase groups stage each warp's element tables in dynamic shared memory
     constexpr bool stage = ELEM == 0 && ((TLFEA_MR_2PH && MODEL == 1 && TAN) || (TLFEA_T10_2PH && MODEL == 0 && !KV));
     const size_t smem = stage ? sizeof(double) * kWarps * G::EPW * NQ * (G::NEN * 3 + 1) : 0;
+    if constexpr (stage) {
+      if (c->aff) {  // tables generated from the affine (min) layout
+        auto kern = k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>(), true>;
+        TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
+        kern<<<grid, kWarps * 32, smem, s>>>(A);
+        TL_CHECK_LAUNCH();
+        return TLFEA_OK;
+      }
+    }
     auto kern = k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>()>;
     TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
     kern<<<grid, kWarps * 32, smem, s>>>(A);

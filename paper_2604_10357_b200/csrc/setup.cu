@@ -190,6 +190,42 @@ __global__ void k_affine_check(int64_t n_el, const int32_t* __restrict__ conn,
   if (dev > 1e-12 * h) atomicOr(nonaffine, 1u);
 }
 
+// Affine (min) layout of a straight-sided T10 (P:312-320 with J constant):
+// J = [X1 - X0, X2 - X0, X3 - X0] (columns dX/dxi_c), grad_X z_{c+1} = row c
+// of J^-1, grad_X z_0 = -(sum of the others), J0 = det J.
+__global__ void k_affine_layout(int64_t n_el, const int32_t* __restrict__ conn, const double* __restrict__ X,
+                                double* __restrict__ aff) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n_el) return;
+  const int32_t* c = conn + e * 10;
+  double J[3][3];
+  for (int k = 0; k < 3; ++k)
+    for (int m = 0; m < 3; ++m) J[k][m] = X[3 * (int64_t)c[m + 1] + k] - X[3 * (int64_t)c[0] + k];
+  const double A00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], A01 = J[1][2] * J[2][0] - J[1][0] * J[2][2],
+               A02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  const double det = J[0][0] * A00 + J[0][1] * A01 + J[0][2] * A02;
+  const double r = 1.0 / det;
+  // inverse: Ji[m][k] = cofactor(k, m) / det
+  double Ji[3][3];
+  Ji[0][0] = A00 * r;
+  Ji[1][0] = A01 * r;
+  Ji[2][0] = A02 * r;
+  Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * r;
+  Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * r;
+  Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * r;
+  Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * r;
+  Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * r;
+  Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * r;
+  double* a = aff + 13 * e;
+  for (int k = 0; k < 3; ++k) {
+    a[3 + k] = Ji[0][k];
+    a[6 + k] = Ji[1][k];
+    a[9 + k] = Ji[2][k];
+    a[k] = -(Ji[0][k] + Ji[1][k] + Ji[2][k]);
+  }
+  a[12] = det;
+}
+
 // Pattern keys: (owned row << 32) | column for every element-local pair whose
 // row is owned; non-owned pairs get the sentinel ~0.
 __global__ void k_keys(int64_t n_el, int nen, const int32_t* __restrict__ conn,
@@ -651,7 +687,7 @@ static tlfea_status build_geometry_classes(Context* c, const double* dX) {
   const int max_cls = c->element == TLFEA_T10 ? 32 : 4;
   c->n_cls = 0;
   if (n == 0) return TLFEA_OK;
-  if (c->force_tables) return TLFEA_OK;  // options.reference_layout = 1
+  if (c->force_tables == 1) return TLFEA_OK;  // options.reference_layout = 1: per-(e,q) tables
   TmpArr<unsigned long long> key, key2;
   TmpArr<int64_t> idx, idx2;
   TmpArr<int32_t> flag, run;
@@ -862,8 +898,8 @@ static tlfea_status validate(const tlfea_mesh* mesh, const tlfea_material* mat,
   if (opts->mass_rule != 0 && opts->mass_rule != 1) return fail(TLFEA_E_INVALID, "mass_rule must be 0 or 1");
   if (opts->nranks < 1 || opts->rank < 0 || opts->rank >= opts->nranks)
     return fail(TLFEA_E_INVALID, "bad rank / nranks");
-  if (opts->reference_layout != 0 && opts->reference_layout != 1)
-    return fail(TLFEA_E_INVALID, "reference_layout must be 0 or 1");
+  if (opts->reference_layout < 0 || opts->reference_layout > 2)
+    return fail(TLFEA_E_INVALID, "reference_layout must be 0, 1 or 2");
   if (opts->hessian_upper != 0 && opts->hessian_upper != 1)
     return fail(TLFEA_E_INVALID, "hessian_upper must be 0 or 1");
   if (opts->hessian_upper && (opts->nranks != 1 || (opts->constraints && opts->constraints->m > 0)))
@@ -1165,7 +1201,13 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     TL_CUDA(cudaMemcpy(&na, dna, sizeof(na), cudaMemcpyDeviceToHost));
     c->affine = na ? 0 : 1;
   }
-  TL_TRY(build_geometry_classes(c, dX));
+  if (c->force_tables != 2) TL_TRY(build_geometry_classes(c, dX));
+  // no classes: straight-sided T10 elements take the affine (min) layout
+  if (c->element == TLFEA_T10 && c->affine && c->n_cls == 0 && c->force_tables != 1 && c->n_el > 0) {
+    TL_TRY(c->alloc(&c->aff, (size_t)c->n_el * 13));
+    k_affine_layout<<<grid_for(c->n_el, 256), 256>>>(c->n_el, c->conn, dX, c->aff);
+    TL_CHECK_LAUNCH();
+  }
 
   // ---- a-2 pattern over setup elements (64-bit keys, sort, unique)
   // constraint couplings join the element keys (pattern union)

@@ -106,6 +106,19 @@ def perturbed(mesh: Mesh, amp: float = 0.05, seed: int = SEED_BASE + 7) -> Mesh:
     return Mesh(mesh.element, X, mesh.conn.copy(), mesh.dims, name=mesh.name + "_perturbed")
 
 
+def perturbed_straight(mesh: Mesh, amp: float = 0.2, seed: int = SEED_BASE + 8) -> Mesh:
+    """Straight-sided unstructured T10 variant: the element corners move by
+    U(-amp, amp) x node spacing and every mid-edge node is put back at the
+    middle of its edge, so the elements stay affine but no two are congruent
+    (the affine "min" layout path)."""
+    X = mesh.X.copy()
+    corners = np.unique(mesh.conn[:, :4])
+    X[corners] += np.random.default_rng(seed).uniform(-amp, amp, (corners.size, 3)) * _node_spacing(mesh.X)
+    for m, (a, b) in enumerate(T10_EDGES):
+        X[mesh.conn[:, 4 + m]] = 0.5 * (X[mesh.conn[:, a]] + X[mesh.conn[:, b]])
+    return Mesh(0, X, mesh.conn.copy(), None, name=mesh.name + "_straight")
+
+
 def _morton3(c: np.ndarray) -> np.ndarray:
     code = np.zeros(c.shape[0], dtype=np.int64)
     for bit in range(21):

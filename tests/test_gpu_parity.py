@@ -86,6 +86,16 @@ CASES = {
                                                   dict(synth.SVK_PAPER, **synth.KV_TIRE), 1),
     "t10_3x3x2_perturbed_mr_4pt": lambda: (synth.perturbed(synth.kuhn_t10_box(3, 3, 2, 0.6, 0.6, 0.4)),
                                            dict(synth.MR_PAPER), 0),
+    # straight-sided, non-congruent T10: the affine (min) layout, 13 fp64 per element
+    "t10_5x3x2_straight_svk_keast5": lambda: (synth.perturbed_straight(synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4)),
+                                              dict(synth.SVK_PAPER), 1),
+    "t10_4x3x2_straight_svk_4pt": lambda: (synth.perturbed_straight(synth.kuhn_t10_box(4, 3, 2, 0.8, 0.6, 0.4)),
+                                           dict(synth.SVK_PAPER), 0),
+    "t10_4x3x2_straight_mr_kv_keast5": lambda: (synth.perturbed_straight(synth.kuhn_t10_box(4, 3, 2, 0.8, 0.6, 0.4)),
+                                                dict(synth.MR_PAPER, **synth.KV_TIRE), 1),
+    "t10_100el_straight_svk_keast5": lambda: (synth.perturbed_straight(synth.Mesh(0, synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).X,
+                                                                                  synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).conn[:100])),
+                                              dict(synth.SVK_PAPER), 1),
     "ancf_3x3_svk": lambda: (synth.ancf_plate(3), dict(synth.SVK_PAPER), 2),
     "ancf_5x5_mr_kv": lambda: (synth.ancf_plate(5), dict(synth.MR_PAPER, **synth.KV_TIRE), 2),
     # ANCF3443 on the per-(e,q) table path (more than 4 element shapes: the
@@ -123,7 +133,9 @@ def test_eval_parity(torch_cuda, case):
     check_pattern(ctx, pr)
     # congruent (Kuhn / uniform plate) meshes use shared-memory geometry classes,
     # perturbed meshes the per-(e,q) tables
-    if "perturbed" in case or "graded" in case:
+    if "straight" in case:
+        assert ctx.info["n_geometry_classes"] == 0 and ctx.info["reference_layout"] == 2
+    elif "perturbed" in case or "graded" in case:
         assert ctx.info["n_geometry_classes"] == 0
     elif mesh.element == 0 and mesh.n_el >= 6:
         assert ctx.info["n_geometry_classes"] == 6
@@ -202,6 +214,7 @@ def test_constitutive_hook(torch_cuda, model):
 
 @pytest.mark.parametrize("case", ["ancf_6x6_graded_svk", "ancf_4x4_perturbed_svk", "ancf_5x5_graded_svk_kv",
                                   "ancf_4x4_svk_kv", "ancf_3x3_svk", "t10_100el_perturbed_svk_keast5",
+                                  "t10_5x3x2_straight_svk_keast5", "t10_4x3x2_straight_svk_4pt",
                                   "t10_5x3x1_svk_keast5_ragged"])
 def test_force_only_parity(torch_cuda, case):
     """tlfea_force_only (the AdamW inner evaluation) on the class and the
@@ -266,3 +279,25 @@ def test_errors(torch_cuda):
     assert bad is not None and bad[0] in set(np.nonzero((mesh.conn == mesh.conn[2, 3]).any(1))[0])
     with pytest.raises(T.TlfeaError, match="INVALID"):
         ctx.eval(dev(torch, mesh.X.ravel()), dev(torch, np.zeros(mesh.n_dof)), h=0.0)
+
+
+@pytest.mark.parametrize("case", ["t10_5x3x1_svk_keast5_ragged", "cfg1_svk_4pt", "t10_4x3x2_mr_kv_keast5"])
+def test_affine_layout_on_kuhn_boxes(torch_cuda, case):
+    """options.reference_layout = 2 forces the affine (min) layout on a
+    congruent Kuhn box: same results as the class tables (to rounding) and as
+    the oracle."""
+    import paper_2604_10357_b200 as T
+    torch = torch_cuda
+    mesh, mat, rule = CASES[case]()
+    h = synth.H_T10
+    x, v, vn, fext = state(mesh)
+    ca = T.Context.from_mesh(mesh, mat, rule, reference_layout="affine")
+    assert ca.info["reference_layout"] == 2
+    g, H, f = ca.eval(dev(torch, x), dev(torch, v), dev(torch, vn), dev(torch, fext), h, f_int=ca.empty_outputs()[2])
+    fo = ca.force_only(dev(torch, x), dev(torch, v)).cpu().numpy()
+    torch.cuda.synchronize()
+    pr = oracle.Problem(mesh, mat, rule)
+    g0, H0, f0 = pr.eval(x, v, vn, fext, h)
+    assert rel(g.cpu().numpy(), g0) <= TOL and rel(H.cpu().numpy(), H0) <= TOL and rel(f.cpu().numpy(), f0) <= TOL
+    if not mat.get("eta_damp"):
+        assert rel(fo, f0) <= TOL
