@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define TLFEA_ABI_VERSION 5
+#define TLFEA_ABI_VERSION 6
 
 typedef struct tlfea_ctx_s* tlfea_ctx;
 
@@ -204,7 +204,8 @@ typedef struct {
  * CSR (64-bit keys, radix sort, unique, counts, scan), its DOF lift, the
  * slot map, the mass M, f_ff, and the assembly schedule.
  * Errors: TLFEA_E_INVALID, TLFEA_E_INVERTED_ELEMENT (message names e),
- * TLFEA_E_OVERFLOW (nnz >= 2^31 or n_elements >= 2^24), TLFEA_E_OOM, TLFEA_E_CUDA.
+ * TLFEA_E_OVERFLOW (owned-row nnz >= 2^31, or more than 2^24 elements on one
+ * rank), TLFEA_E_OOM, TLFEA_E_CUDA.
  * Synchronizes the device. On success *out owns all device buffers. */
 tlfea_status tlfea_setup(const tlfea_mesh* mesh, const tlfea_material* mat,
                          const tlfea_options* opts, tlfea_ctx* out);
@@ -385,21 +386,41 @@ tlfea_status tlfea_assemble_hessian(tlfea_ctx ctx, const double* x, double h,
 tlfea_status tlfea_exchange_sizes(tlfea_ctx ctx, int64_t* send_counts,
                                   int64_t* recv_counts);
 
-/* begin: evaluate the local elements, write owned-row partials into H_out /
- * f_int_out-internal state and pack the non-owned partials into send_buf
- * (DEVICE [sum send_counts]). The caller then moves send_buf -> peers'
- * recv_buf (e.g. NCCL send/recv over NVLink), and calls finish, which adds the
- * received partials in ascending peer-rank order (deterministic for a fixed
- * partition) and completes g (and f_int_out if non-NULL). force_only = 1
- * skips H (H_out may be NULL). */
+/* The partitioned evaluation, three calls on one stream (the
+ * exchange overlaps the interior elements, step 3):
+ *  begin    : Stage 1 + 2 of the BOUNDARY elements (local elements with a
+ *             node owned elsewhere; the context orders them first) and the
+ *             pack of the non-owned partials (H 3x3 blocks, nodal forces) into
+ *             send_buf (DEVICE [sum send_counts]). When the stream reaches the
+ *             end of begin, send_buf is complete: the caller then starts the
+ *             transfer send_buf -> peers' recv_buf (e.g. NCCL send/recv over
+ *             NVLink on its own stream).
+ *  interior : Stage 1 + 2 of the remaining local elements (concurrently with
+ *             the transfer), then the owned rows of H (H_out) and of the
+ *             nodal force from all local elements.
+ *  finish   : once recv_buf has arrived (the caller orders its stream after
+ *             the transfer): adds the received partials in ascending peer
+ *             order (deterministic for a fixed partition) and completes g (and
+ *             f_int_out if non-NULL).
+ * force_only = 1 skips H (H_out may be NULL). Calling the three out of order
+ * returns TLFEA_E_INVALID. A single-rank context accepts the same sequence
+ * (no exchange). */
 tlfea_status tlfea_eval_begin(tlfea_ctx ctx, const double* x, const double* v,
                               int32_t force_only, double h, double* H_out,
                               double* send_buf, void* stream);
+tlfea_status tlfea_eval_interior(tlfea_ctx ctx, const double* x, const double* v,
+                                 int32_t force_only, double h, double* H_out,
+                                 void* stream);
 tlfea_status tlfea_eval_finish(tlfea_ctx ctx, const double* recv_buf,
                                const double* v, const double* v_n,
                                const double* f_ext, double h,
                                int32_t force_only, double* g_out,
                                double* H_out, double* f_int_out, void* stream);
+
+/* Global ids of the context's local elements, in its local order (the order
+ * of tlfea_slot_map / tlfea_export_precompute rows; partitioned contexts put
+ * the boundary elements first). out_host HOST int64 [n_elements]. */
+tlfea_status tlfea_local_elements(tlfea_ctx ctx, int64_t* out_host);
 
 /* Host-only partition planner (no GPU needed; used by setup and by the CPU
  * tests of the exchange protocol). Given the GLOBAL mesh connectivity

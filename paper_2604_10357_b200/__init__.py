@@ -20,7 +20,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-ABI_VERSION = 5  # include/tlfea.h TLFEA_ABI_VERSION (struct layouts of this binding)
+ABI_VERSION = 6  # include/tlfea.h TLFEA_ABI_VERSION (struct layouts of this binding)
 LIB_PATH = os.environ.get("TLFEA_LIB") or os.path.join(_HERE, "libtlfea.so")
 _lib = None
 _lock = threading.Lock()
@@ -105,7 +105,9 @@ _SIGS = {
     "tlfea_assemble_hessian": [_vp, _vp, _d, _vp, _vp],
     "tlfea_exchange_sizes": [_vp, _vp, _vp],
     "tlfea_eval_begin": [_vp, _vp, _vp, _i32, _d, _vp, _vp, _vp],
+    "tlfea_eval_interior": [_vp, _vp, _vp, _i32, _d, _vp, _vp],
     "tlfea_eval_finish": [_vp, _vp, _vp, _vp, _vp, _d, _i32, _vp, _vp, _vp, _vp],
+    "tlfea_local_elements": [_vp, _vp],
     "tlfea_plan_partition": [_i64, _i32, _vp, _i64, _vp, _i32, _i32, _vp, C.POINTER(_i64), _vp, _vp,
                              C.POINTER(_i64), _vp, _vp],
     "tlfea_sync_status": [_vp, C.POINTER(_i64), C.POINTER(_i32)],
@@ -465,6 +467,19 @@ class Context:
                                       self._d(H, 0 if force_only else self.nnz, "H"),
                                       self._d(send_buf, int(self.exchange_sizes()[0].sum()), "send_buf"),
                                       _stream(stream)))
+
+    def eval_interior(self, x, v, h, H, force_only=False, stream=None):
+        """tlfea_eval_interior: the elements the exchange overlaps, then the
+        owned rows (call between eval_begin and eval_finish)."""
+        n = self.n_dof
+        _check(lib().tlfea_eval_interior(self.handle, self._d(x, n, "x"), self._d(v, n, "v"), int(force_only),
+                                         float(h), self._d(H, 0 if force_only else self.nnz, "H"), _stream(stream)))
+
+    def local_elements(self):
+        """Global ids of the local elements in the context's local order."""
+        out = np.zeros(self.info["n_elements"], np.int64)
+        _check(lib().tlfea_local_elements(self.handle, _ptr(out)))
+        return out
 
     def eval_finish(self, recv_buf, v, v_n, f_ext, h, g, H, f_int=None, force_only=False, stream=None):
         n, no = self.n_dof, 3 * self.n_own

@@ -451,13 +451,32 @@ tlfea_status tlfea_eval_begin(tlfea_ctx ctx, const double* x, const double* v, i
   TRY(use_device(c));
   const cudaStream_t s = as_stream(stream);
   c.last_stream = s;
-  TIMED(0, launch_element_kernel(&c, x, v, !force_only, s));
-  if (!force_only) TIMED(1, launch_gather_H(&c, h, H_out, s));
-  TIMED(2, launch_gather_f(&c, nullptr, nullptr, nullptr, h, nullptr, c.fpart, true, s));
+  // the boundary elements (local [0, n_el_bnd)) and the send buffer
+  TIMED(0, launch_element_kernel(&c, x, v, !force_only, s, 0, c.nranks > 1 ? c.n_el_bnd : c.n_el));
   if (c.nranks > 1) {
     if (!send_buf) return fail(TLFEA_E_INVALID, "tlfea_eval_begin: NULL send_buf");
     TIMED(3, launch_pack_send(&c, send_buf, force_only != 0, s));
   }
+  c.interior_pending = true;
+  return TLFEA_OK;
+}
+
+tlfea_status tlfea_eval_interior(tlfea_ctx ctx, const double* x, const double* v, int32_t force_only, double h,
+                                 double* H_out, void* stream) {
+  CTX_OR_FAIL(ctx);
+  Context& c = ctx->c;
+  TRY(check_h(h));
+  if (!c.interior_pending) return fail(TLFEA_E_INVALID, "tlfea_eval_interior: call tlfea_eval_begin first");
+  if (!x || (!force_only && !H_out)) return fail(TLFEA_E_INVALID, "tlfea_eval_interior: NULL x or H_out");
+  if (c.mat.kv && !v) return fail(TLFEA_E_INVALID, "tlfea_eval_interior: Kelvin-Voigt damping needs v");
+  TRY(use_device(c));
+  const cudaStream_t s = as_stream(stream);
+  c.last_stream = s;
+  if (c.nranks > 1) TIMED(0, launch_element_kernel(&c, x, v, !force_only, s, c.n_el_bnd, c.n_el));
+  // owned rows from the local elements: H blocks and the partial nodal forces
+  if (!force_only) TIMED(1, launch_gather_H(&c, h, H_out, s));
+  TIMED(2, launch_gather_f(&c, nullptr, nullptr, nullptr, h, nullptr, c.fpart, true, s));
+  c.interior_pending = false;
   return TLFEA_OK;
 }
 
@@ -467,6 +486,7 @@ tlfea_status tlfea_eval_finish(tlfea_ctx ctx, const double* recv_buf, const doub
   CTX_OR_FAIL(ctx);
   Context& c = ctx->c;
   TRY(check_h(h));
+  if (c.interior_pending) return fail(TLFEA_E_INVALID, "tlfea_eval_finish: call tlfea_eval_interior first");
   TRY(use_device(c));
   const cudaStream_t s = as_stream(stream);
   if (c.nranks > 1) {
@@ -479,6 +499,15 @@ tlfea_status tlfea_eval_finish(tlfea_ctx ctx, const double* recv_buf, const doub
   }
   if (f_int_out)
     TL_CUDA(cudaMemcpyAsync(f_int_out, c.fpart, sizeof(double) * 3 * c.n_own, cudaMemcpyDeviceToDevice, s));
+  return TLFEA_OK;
+}
+
+tlfea_status tlfea_local_elements(tlfea_ctx ctx, int64_t* out_host) {
+  CTX_OR_FAIL(ctx);
+  Context& c = ctx->c;
+  if (!out_host) return fail(TLFEA_E_INVALID, "tlfea_local_elements: NULL output");
+  TRY(use_device(c));
+  if (c.n_el > 0) TL_CUDA(cudaMemcpy(out_host, c.elem_gid, sizeof(int64_t) * c.n_el, cudaMemcpyDeviceToHost));
   return TLFEA_OK;
 }
 

@@ -108,6 +108,8 @@ struct Context {
   int rank = 0, nranks = 1;
   int64_t n_el_global = 0, n_coef = 0;
   int64_t n_el = 0;            // local elements
+  int64_t n_el_bnd = 0;        // partitioned: local elements [0, n_el_bnd) are the boundary range
+  bool interior_pending = false;  // tlfea_eval_begin ran, tlfea_eval_interior not yet
   int64_t n_own = 0;           // owned coefficient rows
   int64_t nnz_c = 0;           // owned-row coefficient nnz
   int affine = 0;
@@ -241,7 +243,7 @@ tlfea_status Context::alloc(T** p, size_t count) {
 tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_material* mat,
                            const tlfea_options* opts);
 tlfea_status launch_element_kernel(Context* c, const double* x, const double* v,
-                                   bool tangent, cudaStream_t s);
+                                   bool tangent, cudaStream_t s, int64_t e_begin = 0, int64_t e_end = -1);
 tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s);
 tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, const double* fext,
                              double h, double* g, double* fint, bool partial_only,

@@ -121,6 +121,7 @@ struct ElArgs {
   const double* cls_tab;
   int n_cls;
   const double* aff;  // affine (min) layout: [n_el][13] = grad_X z_0..3, J0 (straight-sided T10)
+  int64_t g0;         // first warp group of the launch (element range [EPW g0, n_el))
   const double* x;
   const double* v;
   MatDev mat;
@@ -1678,7 +1679,7 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
   constexpr bool B2PH = TLFEA_BEAM_2PH && ELEM == 2 && MODEL == 0 && !KV && TAN && CLS;
   constexpr bool M2PH = TLFEA_MR_2PH && ELEM == 0 && MODEL == 1 && TAN;
   constexpr bool V2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && KV && TAN && CLS;  // SVK + Kelvin-Voigt
-  const int64_t grp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);  // this warp's element group
+  const int64_t grp = A.g0 + (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);  // this warp's element group
   T10Pre pre;
   if constexpr (T2PH && !CLS && !AFF) t10_stage_tables_async<NQ>(grp, A, s_tab);
   T10Aff aff;
@@ -1896,6 +1897,7 @@ static ElArgs el_args(const Context* c, const double* x, const double* v) {
   A.cls_tab = c->cls_tab;
   A.n_cls = c->n_cls;
   A.aff = c->aff;
+  A.g0 = 0;
   A.x = x;
   A.v = v;
   A.mat = c->mat;
@@ -1908,12 +1910,16 @@ static ElArgs el_args(const Context* c, const double* x, const double* v) {
 }
 
 template <int ELEM, int NQ, int MODEL, bool KV, bool TAN>
-static tlfea_status launch_el(Context* c, const double* x, const double* v, cudaStream_t s) {
+static tlfea_status launch_el(Context* c, const double* x, const double* v, cudaStream_t s, int64_t e_begin,
+                              int64_t e_end) {
   using G = Geo<ELEM>;
   const int64_t per_cta = (int64_t)kWarps * G::EPW;
-  const unsigned grid = (unsigned)((c->n_el + per_cta - 1) / per_cta);
-  if (grid == 0) return TLFEA_OK;
+  if (e_end <= e_begin) return TLFEA_OK;
+  if (e_begin % per_cta != 0) return fail(TLFEA_E_INVALID, "internal: element range not tile aligned");
+  const unsigned grid = (unsigned)((e_end - e_begin + per_cta - 1) / per_cta);
   ElArgs A = el_args(c, x, v);
+  A.n_el = e_end;
+  A.g0 = e_begin / G::EPW;
   if (c->n_cls > 0) {
     const size_t smem = sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
     auto kern = k_element<ELEM, NQ, MODEL, KV, TAN, true, el_npass<ELEM, MODEL>()>;
@@ -1941,26 +1947,34 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
 }
 
 template <int ELEM, int NQ, int MODEL>
-static tlfea_status launch_el_kv(Context* c, const double* x, const double* v, bool tan, cudaStream_t s) {
+static tlfea_status launch_el_kv(Context* c, const double* x, const double* v, bool tan, cudaStream_t s, int64_t e0,
+                                 int64_t e1) {
   const bool kv = c->mat.kv && v != nullptr;
-  if (tan) return kv ? launch_el<ELEM, NQ, MODEL, true, true>(c, x, v, s) : launch_el<ELEM, NQ, MODEL, false, true>(c, x, v, s);
-  return kv ? launch_el<ELEM, NQ, MODEL, true, false>(c, x, v, s) : launch_el<ELEM, NQ, MODEL, false, false>(c, x, v, s);
+  if (tan)
+    return kv ? launch_el<ELEM, NQ, MODEL, true, true>(c, x, v, s, e0, e1)
+              : launch_el<ELEM, NQ, MODEL, false, true>(c, x, v, s, e0, e1);
+  return kv ? launch_el<ELEM, NQ, MODEL, true, false>(c, x, v, s, e0, e1)
+            : launch_el<ELEM, NQ, MODEL, false, false>(c, x, v, s, e0, e1);
 }
 
 template <int ELEM, int NQ>
-static tlfea_status launch_el_model(Context* c, const double* x, const double* v, bool tan, cudaStream_t s) {
-  if (c->mat.model == TLFEA_SVK) return launch_el_kv<ELEM, NQ, 0>(c, x, v, tan, s);
-  return launch_el_kv<ELEM, NQ, 1>(c, x, v, tan, s);
+static tlfea_status launch_el_model(Context* c, const double* x, const double* v, bool tan, cudaStream_t s, int64_t e0,
+                                    int64_t e1) {
+  if (c->mat.model == TLFEA_SVK) return launch_el_kv<ELEM, NQ, 0>(c, x, v, tan, s, e0, e1);
+  return launch_el_kv<ELEM, NQ, 1>(c, x, v, tan, s, e0, e1);
 }
 
-tlfea_status launch_element_kernel(Context* c, const double* x, const double* v, bool tangent,
-                                   cudaStream_t s) {
+// Local elements [e_begin, e_end) (e_end < 0: all); e_begin a multiple of
+// the element-kernel CTA tile.
+tlfea_status launch_element_kernel(Context* c, const double* x, const double* v, bool tangent, cudaStream_t s,
+                                   int64_t e_begin, int64_t e_end) {
+  if (e_end < 0) e_end = c->n_el;
   if (c->element == TLFEA_T10) {
-    if (c->nq == 4) return launch_el_model<0, 4>(c, x, v, tangent, s);
-    return launch_el_model<0, 5>(c, x, v, tangent, s);
+    if (c->nq == 4) return launch_el_model<0, 4>(c, x, v, tangent, s, e_begin, e_end);
+    return launch_el_model<0, 5>(c, x, v, tangent, s, e_begin, e_end);
   }
-  if (c->element == TLFEA_ANCF3243) return launch_el_model<2, 12>(c, x, v, tangent, s);
-  return launch_el_model<1, 48>(c, x, v, tangent, s);
+  if (c->element == TLFEA_ANCF3243) return launch_el_model<2, 12>(c, x, v, tangent, s, e_begin, e_end);
+  return launch_el_model<1, 48>(c, x, v, tangent, s, e_begin, e_end);
 }
 
 static GatherArgs gather_args(const Context* c, double h, double* H) {

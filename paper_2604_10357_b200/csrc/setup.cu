@@ -904,7 +904,7 @@ static tlfea_status validate(const tlfea_mesh* mesh, const tlfea_material* mat,
     return fail(TLFEA_E_INVALID, "hessian_upper must be 0 or 1");
   if (opts->hessian_upper && (opts->nranks != 1 || (opts->constraints && opts->constraints->m > 0)))
     return fail(TLFEA_E_UNSUPPORTED, "UPPER H storage: single-rank contexts without constraints only");
-  if (mesh->n_elements >= (1ll << 24)) return fail(TLFEA_E_OVERFLOW, "n_elements >= 2^24 (packed gather entries)");
+  if (mesh->n_elements >= (1ll << 31)) return fail(TLFEA_E_OVERFLOW, "n_elements >= 2^31");
   if (3 * mesh->n_coef >= (1ll << 31)) return fail(TLFEA_E_OVERFLOW, "3 n_coef >= 2^31");
   if (const tlfea_constraints* k = opts->constraints) {
     if (k->m < 0) return fail(TLFEA_E_INVALID, "constraints: m < 0");
@@ -1123,8 +1123,29 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     for (int a = 0; a < nen && !touches; ++a) touches = owner[cc[e * nen + a]] == c->rank;
     if (touches) setup_el.push_back(e);
   }
+  // partitioned: boundary elements (a node owned elsewhere: they feed the
+  // send buffer) first, so tlfea_eval_begin can pack them while the interior
+  // elements run next to the exchange; the boundary
+  // range is padded to whole element-kernel CTA tiles
+  c->n_el_bnd = 0;
+  if (c->nranks > 1) {
+    std::vector<int64_t> bnd, inner;
+    for (int64_t e : local) {
+      bool b = false;
+      for (int a = 0; a < nen && !b; ++a) b = owner[cc[e * nen + a]] != c->rank;
+      (b ? bnd : inner).push_back(e);
+    }
+    const int64_t tile = el_per_tile(c->element);
+    c->n_el_bnd = std::min<int64_t>((int64_t)local.size(), ((int64_t)bnd.size() + tile - 1) / tile * tile);
+    local = bnd;
+    local.insert(local.end(), inner.begin(), inner.end());
+  }
   c->n_el = (int64_t)local.size();
   const int64_t NS = (int64_t)setup_el.size();
+  // packed gather entries (e << 8 | a << 4 | b) hold LOCAL element ids
+  if (c->n_el >= (1ll << 24))
+    return fail(TLFEA_E_OVERFLOW, "more than 2^24 elements on one rank (packed gather entries): partition the mesh "
+                                  "over more ranks");
 
   // ---- uploads
   double* dX = nullptr;

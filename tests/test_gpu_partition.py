@@ -40,6 +40,7 @@ def run_partitioned(torch, mesh, mat, rule, P, x, v, vn, fext, h, part=None, for
         outs.append((g, None if force_only else H, f))
     for r, c in enumerate(ctxs):
         c.eval_begin(xd, vd, h, outs[r][1], sbufs[r], force_only=force_only)
+        c.eval_interior(xd, vd, h, outs[r][1], force_only=force_only)
     # the exchange: rank r's block for peer p -> rank p's block from r
     for r in range(P):
         soff = np.concatenate([[0], np.cumsum(sizes[r][0])])
@@ -167,7 +168,8 @@ def test_partitioned_slot_map_vs_global(torch_cuda, scattered):
     for r in range(P):
         ctx = T.Context.from_mesh(mesh, mat, rule, rank=r, nranks=P, elem_part=part)
         rowptr, _, _, _, owned = [t.cpu().numpy().astype(np.int64) for t in ctx.export_pattern()]
-        local = np.nonzero(part == r)[0]
+        local = ctx.local_elements()   # boundary elements first (tlfea_local_elements)
+        assert np.array_equal(np.sort(local), np.nonzero(part == r)[0])
         sm = ctx.slot_map().astype(np.int64)
         assert sm.shape[0] == local.size
         loc_row = -np.ones(mesh.n_coef, np.int64)

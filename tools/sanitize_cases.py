@@ -70,6 +70,7 @@ rb = [torch.zeros(max(1, int(b.sum())), dtype=torch.float64, device="cuda") for 
 outs = [c.empty_outputs() for c in ctxs]
 for r, c in enumerate(ctxs):
     c.eval_begin(d(x), d(v), 1e-3, outs[r][1], sb[r])
+    c.eval_interior(d(x), d(v), 1e-3, outs[r][1])
 for r in range(P):
     so = np.concatenate([[0], np.cumsum(sizes[r][0])])
     for p in range(P):
