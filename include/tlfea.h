@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define TLFEA_ABI_VERSION 6
+#define TLFEA_ABI_VERSION 7
 
 typedef struct tlfea_ctx_s* tlfea_ctx;
 
@@ -218,10 +218,12 @@ tlfea_status tlfea_info(tlfea_ctx ctx, tlfea_info_t* out);
 /* ------------------------------------------------ pattern / slot map -- */
 
 /* DOF-level CSR of H over the owned rows (reading Q14/Q15):
- * rowptr [n_rows+1] (relative: rowptr[0]=0), cols [nnz] GLOBAL DOF columns,
+ * rowptr [n_rows+1] int64 (relative: rowptr[0]=0; 64-bit so H may hold 2^31
+ * or more values, reading Q17), cols [nnz] int32 GLOBAL DOF columns,
  * strictly increasing per row; row r of the block is DOF row
- * 3*owned_node[r/3] + r%3. Pointers are DEVICE, borrowed until destroy. */
-tlfea_status tlfea_pattern(tlfea_ctx ctx, const int32_t** rowptr,
+ * 3*owned_node[r/3] + r%3. Pointers are DEVICE, borrowed until destroy.
+ * Limits: nnz < 3 x 2^31 (FULL), < 2^31 (UPPER); 3 n_coef < 2^31. */
+tlfea_status tlfea_pattern(tlfea_ctx ctx, const int64_t** rowptr,
                            const int32_t** cols);
 
 /* Coefficient-level CSR (the mass / adjacency pattern of §4.2):
@@ -235,19 +237,20 @@ tlfea_status tlfea_coef_pattern(tlfea_ctx ctx, const int32_t** rowptr,
 tlfea_status tlfea_owned_nodes(tlfea_ctx ctx, const int32_t** nodes);
 
 /* Copies of the patterns into caller DEVICE buffers (any may be NULL):
- * rowptr_out [3 n_owned+1], cols_out [nnz], rowptr_c_out [n_owned+1],
- * cols_c_out [nnz_coef], owned_out [n_owned]. Asynchronous on stream. */
-tlfea_status tlfea_export_pattern(tlfea_ctx ctx, int32_t* rowptr_out, int32_t* cols_out,
+ * rowptr_out int64 [3 n_owned+1], cols_out int32 [nnz], rowptr_c_out int32
+ * [n_owned+1], cols_c_out int32 [nnz_coef], owned_out int32 [n_owned].
+ * Asynchronous on stream. */
+tlfea_status tlfea_export_pattern(tlfea_ctx ctx, int64_t* rowptr_out, int32_t* cols_out,
                                   int32_t* rowptr_c_out, int32_t* cols_c_out,
                                   int32_t* owned_out, void* stream);
 
-/* Canonical slot map (reading Q16): out_host int32 [e_count][3n_en][3n_en],
+/* Canonical slot map (reading Q16): out_host int64 [e_count][3n_en][3n_en],
  * entry [e][3a+d][3b+f] = index into the DOF CSR values of the entry
  * (row 3*conn[e][a]+d, column 3*conn[e][b]+f), or -1 when that row is not
  * owned by this context. e indexes the context's LOCAL element list.
  * HOST output; synchronizes. */
 tlfea_status tlfea_slot_map(tlfea_ctx ctx, int64_t e_begin, int64_t e_count,
-                            int32_t* out_host);
+                            int64_t* out_host);
 
 /* ------------------------------------------------ setup exports (a-1,a-2) -- */
 

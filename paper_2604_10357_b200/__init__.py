@@ -20,7 +20,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-ABI_VERSION = 6  # include/tlfea.h TLFEA_ABI_VERSION (struct layouts of this binding)
+ABI_VERSION = 7  # include/tlfea.h TLFEA_ABI_VERSION (struct layouts of this binding)
 LIB_PATH = os.environ.get("TLFEA_LIB") or os.path.join(_HERE, "libtlfea.so")
 _lib = None
 _lock = threading.Lock()
@@ -314,13 +314,13 @@ class Context:
 
     # -- exports
     def export_pattern(self, stream=None):
-        """Copies (rowptr [3 n_own+1], cols [nnz], rowptr_c [n_own+1], cols_c [nnz_coef],
-        owned [n_own]) as int32 CUDA tensors (tlfea_export_pattern)."""
+        """Copies (rowptr [3 n_own+1] int64, cols [nnz], rowptr_c [n_own+1], cols_c [nnz_coef],
+        owned [n_own] int32) as CUDA tensors (tlfea_export_pattern)."""
         torch = self._torch()
         dev = torch.device("cuda", self.device)
         i = self.info
-        out = [torch.empty(n, dtype=torch.int32, device=dev) for n in
-               (3 * self.n_own + 1, self.nnz, self.n_own + 1, i["nnz_coef"], self.n_own)]
+        out = [torch.empty(n, dtype=torch.int64 if k == 0 else torch.int32, device=dev) for k, n in
+               enumerate((3 * self.n_own + 1, self.nnz, self.n_own + 1, i["nnz_coef"], self.n_own))]
         _check(lib().tlfea_export_pattern(self.handle, *[_ptr(t) for t in out], _stream(stream)))
         return tuple(out)
 
@@ -329,7 +329,7 @@ class Context:
         if e_count is None:
             e_count = n - e_begin
         nd = 3 * self.info["n_en"]
-        out = np.zeros((e_count, nd, nd), np.int32)
+        out = np.zeros((e_count, nd, nd), np.int64)
         _check(lib().tlfea_slot_map(self.handle, e_begin, e_count, _ptr(out)))
         return out
 

@@ -121,7 +121,7 @@ tlfea_status tlfea_info(tlfea_ctx ctx, tlfea_info_t* o) {
   return TLFEA_OK;
 }
 
-tlfea_status tlfea_pattern(tlfea_ctx ctx, const int32_t** rowptr, const int32_t** cols) {
+tlfea_status tlfea_pattern(tlfea_ctx ctx, const int64_t** rowptr, const int32_t** cols) {
   CTX_OR_FAIL(ctx);
   if (rowptr) *rowptr = ctx->c.rowptr;
   if (cols) *cols = ctx->c.cols;
@@ -141,14 +141,14 @@ tlfea_status tlfea_owned_nodes(tlfea_ctx ctx, const int32_t** nodes) {
   return TLFEA_OK;
 }
 
-tlfea_status tlfea_export_pattern(tlfea_ctx ctx, int32_t* rowptr_out, int32_t* cols_out, int32_t* rowptr_c_out,
+tlfea_status tlfea_export_pattern(tlfea_ctx ctx, int64_t* rowptr_out, int32_t* cols_out, int32_t* rowptr_c_out,
                                   int32_t* cols_c_out, int32_t* owned_out, void* stream) {
   CTX_OR_FAIL(ctx);
   Context& c = ctx->c;
   TRY(use_device(c));
   const cudaStream_t s = as_stream(stream);
   const cudaMemcpyKind k = cudaMemcpyDeviceToDevice;
-  if (rowptr_out) TL_CUDA(cudaMemcpyAsync(rowptr_out, c.rowptr, sizeof(int32_t) * (3 * c.n_own + 1), k, s));
+  if (rowptr_out) TL_CUDA(cudaMemcpyAsync(rowptr_out, c.rowptr, sizeof(int64_t) * (3 * c.n_own + 1), k, s));
   if (cols_out) TL_CUDA(cudaMemcpyAsync(cols_out, c.cols, sizeof(int32_t) * c.nnz_H, k, s));
   if (rowptr_c_out) TL_CUDA(cudaMemcpyAsync(rowptr_c_out, c.rowptr_c, sizeof(int32_t) * (c.n_own + 1), k, s));
   if (cols_c_out) TL_CUDA(cudaMemcpyAsync(cols_c_out, c.cols_c, sizeof(int32_t) * c.nnz_c, k, s));
@@ -156,7 +156,7 @@ tlfea_status tlfea_export_pattern(tlfea_ctx ctx, int32_t* rowptr_out, int32_t* c
   return TLFEA_OK;
 }
 
-tlfea_status tlfea_slot_map(tlfea_ctx ctx, int64_t e_begin, int64_t e_count, int32_t* out_host) {
+tlfea_status tlfea_slot_map(tlfea_ctx ctx, int64_t e_begin, int64_t e_count, int64_t* out_host) {
   CTX_OR_FAIL(ctx);
   Context& c = ctx->c;
   if (!out_host || e_begin < 0 || e_count < 0 || e_begin + e_count > c.n_el)
@@ -206,9 +206,9 @@ tlfea_status tlfea_slot_map(tlfea_ctx ctx, int64_t e_begin, int64_t e_count, int
         const int32_t s = sc[(e * nen + a) * nen + b];
         for (int d = 0; d < 3; ++d)
           for (int f = 0; f < 3; ++f) {
-            int32_t v = -1;
+            int64_t v = -1;
             if (s >= 0 && i >= 0) {
-              const int32_t b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0;
+              const int64_t b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0;
               v = 9 * b0 + 3 * d * deg + 3 * (s - b0) + f;
             }
             out_host[(e * nd + 3 * a + d) * nd + 3 * b + f] = v;

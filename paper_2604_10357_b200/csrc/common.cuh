@@ -133,7 +133,7 @@ struct Context {
   int32_t* rowptr_c = nullptr;    // [n_own+1]
   int32_t* cols_c = nullptr;      // [nnz_c]
   int32_t* blk_row = nullptr;     // [nnz_c] owned row of each coefficient block
-  int32_t* rowptr = nullptr;      // [3 n_own + 1]  DOF level
+  int64_t* rowptr = nullptr;      // [3 n_own + 1]  DOF level (64-bit: H may exceed 2^31 values)
   int32_t* cols = nullptr;        // [9 nnz_c]
   double* M = nullptr;            // [nnz_c]
   double* fff = nullptr;          // [3 n_own]
@@ -162,8 +162,8 @@ struct Context {
   int32_t* unit_ptr = nullptr;    // [n_units+1]
   int32_t* fdest = nullptr;       // [n_el][nen] position of f_a in the node-sorted force scratch
   // flattened per-unit output metadata (no dependent index chains in the gather)
-  int32_t* u_off = nullptr;       // [n_units] H offset of block (I,J): 9 rowptr_c[i] + 3 k
-  int32_t* u_offT = nullptr;      // [n_units] H offset of (J,I) or -1
+  int32_t* u_off = nullptr;       // [n_units] H offset of block (I,J) / 3 = 3 rowptr_c[i] + k (UPPER: the offset)
+  int32_t* u_offT = nullptr;      // [n_units] H offset of (J,I) / 3, or -1
   int32_t* u_deg = nullptr;       // [n_units] deg(I) | deg(J) << 16
   double* u_m = nullptr;          // [n_units] M_IJ
   double* Kscr = nullptr;         // [n_el][n_ublk][9]

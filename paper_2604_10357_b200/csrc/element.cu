@@ -1848,13 +1848,13 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
     return;
   }
   const int deg = dg & 0xffff, degT = dg >> 16;
-  double* out = H + off;
+  double* out = H + 3 * (int64_t)off;  // FULL offsets are stored / 3 (k_unit_meta)
 #pragma unroll
   for (int d = 0; d < 3; ++d)
 #pragma unroll
     for (int f = 0; f < 3; ++f) h_store(out + 3 * d * deg + f, fma(h, acc[3 * d + f], d == f ? mh : 0.0));
   if (offT >= 0) {
-    double* o2 = H + offT;
+    double* o2 = H + 3 * (int64_t)offT;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll

@@ -252,17 +252,18 @@ __global__ void k_split_keys(int64_t nnz, const unsigned long long* __restrict__
 }
 
 // DOF lift: row 3i+d holds 3J+e for the sorted coefficient columns J.
+// DOF-level positions are 64-bit: H may hold 2^31 or more values (reading Q17)
 __global__ void k_lift(int64_t n_own, int64_t nnz_c, const int32_t* __restrict__ rowptr_c,
                        const int32_t* __restrict__ cols_c, const int32_t* __restrict__ blk_row,
-                       int32_t* __restrict__ rowptr, int32_t* __restrict__ cols) {
+                       int64_t* __restrict__ rowptr, int32_t* __restrict__ cols) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p < n_own) {
-    const int32_t b = rowptr_c[p], deg = rowptr_c[p + 1] - b;
+    const int64_t b = rowptr_c[p], deg = rowptr_c[p + 1] - b;
     for (int d = 0; d < 3; ++d) rowptr[3 * p + d] = 9 * b + 3 * d * deg;
-    if (p == n_own - 1) rowptr[3 * n_own] = (int32_t)(9 * nnz_c);
+    if (p == n_own - 1) rowptr[3 * n_own] = 9 * nnz_c;
   }
   if (p >= nnz_c) return;
-  const int32_t i = blk_row[p], b = rowptr_c[i], deg = rowptr_c[i + 1] - b, k = (int32_t)p - b;
+  const int64_t i = blk_row[p], b = rowptr_c[i], deg = rowptr_c[i + 1] - b, k = p - b;
   const int32_t J = cols_c[p];
   for (int d = 0; d < 3; ++d)
     for (int e = 0; e < 3; ++e) cols[9 * b + 3 * d * deg + 3 * k + e] = 3 * J + e;
@@ -299,7 +300,7 @@ __host__ __device__ __forceinline__ int64_t upper_pos(int32_t base, int32_t k, i
 __global__ void k_lift_upper(int64_t n_own, int64_t nnz_c, const int32_t* __restrict__ rowptr_c,
                              const int32_t* __restrict__ cols_c, const int32_t* __restrict__ blk_row,
                              const int32_t* __restrict__ own_nodes, const int32_t* __restrict__ ubase,
-                             int32_t* __restrict__ rowptr, int32_t* __restrict__ cols) {
+                             int64_t* __restrict__ rowptr, int32_t* __restrict__ cols) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p < n_own) {
     const int32_t deg = rowptr_c[p + 1] - rowptr_c[p];
@@ -594,12 +595,14 @@ __global__ void k_unit_meta(int64_t n_units, const int32_t* __restrict__ unit_p,
   if (u >= n_units) return;
   const int32_t p = unit_p[u], pT = unit_pT[u];
   const int32_t i = blk_row[p], b0 = rowptr_c[i], deg = rowptr_c[i + 1] - b0;
-  u_off[u] = 9 * b0 + 3 * (p - b0);
+  // FULL storage: block offsets 9 b0 + 3 k are multiples of 3; kept / 3 so
+  // 32 bits address up to 3 x 2^31 H values (the gather multiplies back)
+  u_off[u] = 3 * b0 + (p - b0);
   int32_t degT = 0, offT = -1;
   if (pT >= 0) {
     const int32_t j = blk_row[pT], c0 = rowptr_c[j];
     degT = rowptr_c[j + 1] - c0;
-    offT = 9 * c0 + 3 * (pT - c0);
+    offT = 3 * c0 + (pT - c0);
   }
   u_offT[u] = offT;
   u_deg[u] = deg | (degT << 16);
@@ -1264,8 +1267,10 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     unsigned long long last = 0;
     if (nu > 0) TL_CUDA(cudaMemcpy(&last, keys.p + nu - 1, sizeof(last), cudaMemcpyDeviceToHost));
     c->nnz_c = nu - (nu > 0 && last == ~0ull ? 1 : 0);
-    if (9 * c->nnz_c >= (1ll << 31))
-      return fail(TLFEA_E_OVERFLOW, "DOF-level nnz = " + std::to_string(9 * c->nnz_c) + " >= 2^31");
+    // 32-bit coefficient-level indices and block offsets / 3 (k_unit_meta):
+    // H up to 3 x 2^31 values (51 GB), the DOF rowptr and slots are 64-bit
+    if (3 * c->nnz_c >= (1ll << 31))
+      return fail(TLFEA_E_OVERFLOW, "DOF-level nnz = " + std::to_string(9 * c->nnz_c) + " >= 3 x 2^31");
     TL_TRY(c->alloc(&c->cols_c, (size_t)c->nnz_c));
     TL_TRY(c->alloc(&c->blk_row, (size_t)c->nnz_c));
     TL_TRY(c->alloc(&c->rowptr_c, (size_t)c->n_own + 1));
@@ -1302,6 +1307,8 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     count_launch();
     int32_t nu = 0;
     TL_CUDA(cudaMemcpy(&nu, c->ubase + c->n_own, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (4.5 * (double)c->nnz_c + 3.0 * (double)c->n_own >= 2147483647.0)
+      return fail(TLFEA_E_OVERFLOW, "UPPER storage: more than 2^31 values (32-bit offsets)");
     c->nnz_H = nu;
   }
   TL_TRY(c->alloc(&c->rowptr, (size_t)3 * c->n_own + 1));
@@ -1315,7 +1322,7 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
                                                                 c->blk_row, c->rowptr, c->cols);
     TL_CHECK_LAUNCH();
   } else {
-    TL_CUDA(cudaMemset(c->rowptr, 0, sizeof(int32_t)));
+    TL_CUDA(cudaMemset(c->rowptr, 0, sizeof(int64_t)));
   }
   TL_TRY(setup_constraints(c, opts->constraints));
 

@@ -248,3 +248,40 @@ def test_config3_every_row_streamed(T):
     assert np.sqrt(tot[0] / tot[1]) <= TOL, np.sqrt(tot[0] / tot[1])
     assert np.sqrt(tot[2] / tot[3]) <= TOL, np.sqrt(tot[2] / tot[3])
     assert np.sqrt(tot[4] / tot[5]) <= TOL, np.sqrt(tot[4] / tot[5])
+
+
+def test_more_than_2_31_values(T):
+    """Reading Q17 (index width): a single-GPU mesh whose H holds 2^31 or more
+    values (Kuhn 168 x 112 x 56, 6,322,176 T10 elements, nnz_H = 2,195,456,265,
+    the count of the trilinear fit pinned in test_oracle_assembly): the 64-bit
+    DOF row pointers, slots and H offsets. Pattern and values on sampled rows
+    (rows beyond 2^31 values included) against the oracle."""
+    mesh = synth.kuhn_t10_box(168, 112, 56, 3.0, 2.0, 1.0)
+    mat, rule, h = dict(synth.SVK_PAPER), 1, synth.H_T10
+    x, v, vn, fext = synth.t10_state(mesh, with_fext=True)
+    ctx = T.Context.from_mesh(mesh, mat, rule)
+    assert ctx.nnz == 2_195_456_265 > 2 ** 31
+    g, H, f = ctx.empty_outputs()
+    ctx.eval(d(x), d(v), d(vn), d(fext), h, g, H, f)
+    rowptr = ctx.export_pattern()[0].cpu().numpy()
+    assert rowptr.dtype == np.int64 and rowptr[-1] == ctx.nnz
+    # the last nodes' rows live past 2^31 values
+    rng = np.random.default_rng(synth.SEED_BASE + 117)
+    nodes = np.unique(np.concatenate([rng.choice(mesh.n_coef, 24, replace=False),
+                                      np.arange(mesh.n_coef - 8, mesh.n_coef)]))
+    assert rowptr[3 * nodes.max()] > 2 ** 31
+    rp, gcols, gvals = gpu_rows(T, ctx, H, nodes)
+    fg = f.cpu().numpy()
+    del ctx, H
+    ocols, oH, of, oM = oracle.eval_rows(mesh, mat, rule, 0, x, v, h, nodes)
+    num = den = fn = fd = 0.0
+    for s, I in enumerate(nodes):
+        c = ocols[s][ocols[s] >= 0]
+        exp_cols = np.tile((3 * c[:, None] + np.arange(3)[None, :]).ravel(), 3)
+        assert np.array_equal(gcols[s].astype(np.int64), exp_cols), I
+        ov = oH[s][:, :len(c), :].reshape(-1)
+        num += np.sum((gvals[s] - ov) ** 2)
+        den += np.sum(ov ** 2)
+        fn += np.sum((fg[3 * I:3 * I + 3] - of[s]) ** 2)
+        fd += np.sum(of[s] ** 2)
+    assert np.sqrt(num / den) <= TOL and np.sqrt(fn / fd) <= TOL
