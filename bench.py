@@ -539,6 +539,30 @@ def run_ladder(args):
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / k
+        # the same evaluations replayed from a CUDA graph (no host launch path):
+        # the device time of the library's kernels alone
+        ms_graph = None
+        try:
+            kg = int(min(k, 50))
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                step()
+            torch.cuda.current_stream().wait_stream(side)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for _ in range(kg):
+                    step()
+            graph.replay()
+            torch.cuda.synchronize()
+            e0.record()
+            graph.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ms_graph = e0.elapsed_time(e1) / kg
+            del graph
+        except Exception as ex:  # capture unsupported: report the stream timing only
+            print(f"graph capture failed: {ex}", file=sys.stderr)
         kv = False
         bp = alg_bytes_per_element(mesh, info, not force_only, kv, "paper")
         bm = alg_bytes_per_element(mesh, info, not force_only, kv, "min")
@@ -558,6 +582,8 @@ def run_ladder(args):
         t_or = time.perf_counter() - t0
         row = {"family": name, "res": res, "n_elements": mesh.n_el, "quadrature": ["t10_4pt", "keast5", "gl443", "gl322"][rule],
                "path": "force_only" if force_only else "force+tangent+residual", "ms_per_eval": ms,
+               "ms_per_eval_graph": ms_graph,
+               "elements_per_s_graph": mesh.n_el / (ms_graph / 1e3) if ms_graph else None,
                "elements_per_s": mesh.n_el / (ms / 1e3),
                "nnz_per_s": (info["nnz"] / (ms / 1e3)) if not force_only else None, "nnz_H": info["nnz"],
                "hbm_frac_paper_layout": bp * mesh.n_el / (ms / 1e3) / 1e9 / hbm_peak,
