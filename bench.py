@@ -404,7 +404,7 @@ def run_ours(args):
     hbm_peak, hbm_src = peaks()
     dom = max(kt, key=lambda k: kt[k][1])
     n_l, ms_l = kt[dom]
-    avg_ms = ms_l / max(n_l, 1)
+    avg_ms = ms_l / max(n_l, 1) if ms_l > 0 else float("nan")
     n_loc = info["n_elements"]
     model = int(cfg.material["model"])
     b_paper = alg_bytes_per_element(mesh, ginfo, not force_only, kv, "paper")
