@@ -1230,6 +1230,166 @@ __device__ __forceinline__ void element_group_t10svk_force(int64_t grp, const El
   fo[2] = fa[2];
 }
 
+// Force-only T10 SVK with geometry classes, wide groups (the AdamW inner
+// evaluation, Alg. 2; Eq. F_assembly / fint_local as above): a warp
+// holds EPW = 32 / NQ elements so that phase A (one lane per (element, q):
+// F, S, w P = w F S) runs on every lane instead of 12 of 32; phase B walks the
+// EPW x 10 (element, node) tasks in rounds of 32 lanes. kFW warps per CTA
+// amortize the class-table copy over kFW * EPW elements; the element range
+// need not be tile aligned (element = e_begin + warp * EPW + g).
+constexpr int kFW = 8;
+#ifndef TLFEA_FORCE_WIDE
+#define TLFEA_FORCE_WIDE 1
+#endif
+#ifndef TLFEA_FW_PERSIST
+#define TLFEA_FW_PERSIST 1  // persistent warps, next group's inputs prefetched
+#endif
+#ifndef TLFEA_FW_MINB
+#define TLFEA_FW_MINB 3  // 5-point rule (6 elements per warp): 80 registers; config 5 0.577 ms vs 0.574 at 2, 0.64 at 4 (spills)
+#endif
+#ifndef TLFEA_FW_MINB4
+#define TLFEA_FW_MINB4 2  // 4-point rule (8 elements per warp, 3 node rounds): 3 CTAs/SM spill 80 B
+#endif
+template <int NQ>
+struct FwIdx {  // one group's indices: node ids, force destinations, class id
+  static constexpr int NT = (32 / NQ) * 10, NR = (NT + 31) / 32;
+  int32_t node[NR];
+  int32_t fd[NR];
+  int32_t ce;
+};
+template <int NQ>
+__device__ __forceinline__ void fw_load_idx(const ElArgs& A, int64_t e0, FwIdx<NQ>& in) {
+  constexpr int NEN = 10, EPW = 32 / NQ;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < FwIdx<NQ>::NR; ++r) {
+    const int t = lane + 32 * r;
+    const int64_t e = e0 + t / NEN;
+    in.node[r] = -1;
+    in.fd[r] = -1;
+    if (t < FwIdx<NQ>::NT && e < A.n_el) {
+      const int64_t ea = e * NEN + t % NEN;
+      in.fd[r] = A.fdest ? A.fdest[ea] : (int32_t)ea;
+      in.node[r] = A.conn[ea];
+    }
+  }
+  in.ce = (lane < EPW && e0 + lane < A.n_el) ? A.cls[e0 + lane] : 0;
+}
+template <int NQ>
+__device__ __forceinline__ void fw_load_x(const ElArgs& A, const FwIdx<NQ>& in, double (*x)[3]) {
+#pragma unroll
+  for (int r = 0; r < FwIdx<NQ>::NR; ++r) {
+    x[r][0] = x[r][1] = x[r][2] = 0.0;
+    if (in.node[r] >= 0) {
+      const int64_t I = in.node[r];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) x[r][i] = A.x[3 * I + i];
+    }
+  }
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(kFW * 32, NQ == 4 ? TLFEA_FW_MINB4 : TLFEA_FW_MINB) k_force_t10svk_wide(ElArgs A, int64_t e_begin) {
+  constexpr int NEN = 10, EPW = 32 / NQ, NT = EPW * NEN, NR = (NT + 31) / 32, TABW = 3 * NEN + 1;
+  extern __shared__ double s_tab[];  // [n_cls][NQ][3 NEN + 1]
+  __shared__ double s_x[kFW][EPW][3 * NEN];
+  __shared__ double s_pw[kFW][EPW][NQ][9];
+  __shared__ int32_t s_cls[kFW][EPW];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t n_el = A.n_el, stride = (int64_t)gridDim.x * kFW * EPW;
+  int64_t e0 = e_begin + ((int64_t)blockIdx.x * kFW + wib) * EPW;
+  // software pipeline: group k computes while group k+1's coordinates and
+  // group k+2's indices are in flight (the coordinate loads depend on the
+  // indices, so they are issued one group apart)
+  FwIdx<NQ> cur, nxt;
+  double xr[NR][3];
+  fw_load_idx<NQ>(A, e0, cur);
+  if (TLFEA_FW_PERSIST) fw_load_idx<NQ>(A, e0 + stride, nxt);
+  fw_load_x<NQ>(A, cur, xr);
+  {
+    const int tot = A.n_cls * NQ * TABW;
+    constexpr int U = 8;
+    for (int t = threadIdx.x; t < tot; t += U * blockDim.x) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = t + u * (int)blockDim.x < tot ? A.cls_tab[t + u * blockDim.x] : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (t + u * (int)blockDim.x < tot) s_tab[t + u * blockDim.x] = v[u];
+    }
+  }
+  __syncthreads();
+  for (; e0 < n_el; e0 += stride) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int t = lane + 32 * r;
+      if (t < NT)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) s_x[wib][t / NEN][3 * (t % NEN) + i] = xr[r][i];
+    }
+    if (lane < EPW) s_cls[wib][lane] = cur.ce;
+    int32_t fd[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) fd[r] = cur.fd[r];
+    __syncwarp();
+    if (TLFEA_FW_PERSIST) {
+      cur = nxt;
+      fw_load_x<NQ>(A, cur, xr);
+      fw_load_idx<NQ>(A, e0 + 2 * stride, nxt);
+    }
+    if (lane < EPW * NQ) {  // phase A: F, S, w P = w F S at (element ge, point q)
+      const int ge = lane / NQ, q = lane - NQ * ge;
+      const double* t = s_tab + (s_cls[wib][ge] * NQ + q) * TABW;
+      const double* xs = s_x[wib][ge];
+      double F[9];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) F[r] = 0.0;
+#pragma unroll
+      for (int b = 0; b < NEN; ++b) {
+        const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const double xi = xs[3 * b + i];
+          F[3 * i] = fma(xi, n0, F[3 * i]);
+          F[3 * i + 1] = fma(xi, n1, F[3 * i + 1]);
+          F[3 * i + 2] = fma(xi, n2, F[3 * i + 2]);
+        }
+      }
+      double S[6];
+      svk_S(F, A.mat.lam, A.mat.mu, S);
+      const double w = t[3 * NEN];
+      double* pw = s_pw[wib][ge][q];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int J = 0; J < 3; ++J)
+          pw[3 * i + J] = w * (F[3 * i] * sget(S, 0, J) + F[3 * i + 1] * sget(S, 1, J) + F[3 * i + 2] * sget(S, 2, J));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {  // phase B: f_a = sum_q (w P)_q grad N_a(q)
+      const int t = lane + 32 * r;
+      if (fd[r] < 0) continue;
+      const int g = t / NEN, a = t % NEN, ce = s_cls[wib][g];
+      double fa[3] = {0, 0, 0};
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const double* tq = s_tab + (ce * NQ + q) * TABW + 3 * a;
+        const double* pw = s_pw[wib][g][q];
+        const double n0 = tq[0], n1 = tq[1], n2 = tq[2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) fa[i] = fma(pw[3 * i], n0, fma(pw[3 * i + 1], n1, fma(pw[3 * i + 2], n2, fa[i])));
+      }
+      double* fo = A.fscr + (int64_t)fd[r] * 3;
+      fo[0] = fa[0];
+      fo[1] = fa[1];
+      fo[2] = fa[2];
+    }
+    __syncwarp();
+    if (!TLFEA_FW_PERSIST) break;
+  }
+}
+
 #ifndef TLFEA_ANCF_NPASS
 #define TLFEA_ANCF_NPASS 1  // block passes (each re-runs phase A per chunk)
 #endif
@@ -1915,6 +2075,27 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
   using G = Geo<ELEM>;
   const int64_t per_cta = (int64_t)kWarps * G::EPW;
   if (e_end <= e_begin) return TLFEA_OK;
+  if constexpr (ELEM == 0 && MODEL == 0 && !KV && !TAN && TLFEA_FORCE_WIDE) {
+    if (c->n_cls > 0) {
+      const int64_t per = (int64_t)kFW * (32 / NQ);
+      const size_t smem = sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
+      ElArgs A = el_args(c, x, v);
+      A.n_el = e_end;
+      auto kern = k_force_t10svk_wide<NQ>;
+      TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
+      int64_t grid = (e_end - e_begin + per - 1) / per;
+      if (TLFEA_FW_PERSIST) {  // one resident wave of persistent CTAs
+        int dev = 0, nsm = 0, occ = 0;
+        TL_CUDA(cudaGetDevice(&dev));
+        TL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFW * 32, smem));
+        grid = std::min<int64_t>(grid, (int64_t)nsm * std::max(occ, 1));
+      }
+      kern<<<(unsigned)grid, kFW * 32, smem, s>>>(A, e_begin);
+      TL_CHECK_LAUNCH();
+      return TLFEA_OK;
+    }
+  }
   if (e_begin % per_cta != 0) return fail(TLFEA_E_INVALID, "internal: element range not tile aligned");
   const unsigned grid = (unsigned)((e_end - e_begin + per_cta - 1) / per_cta);
   ElArgs A = el_args(c, x, v);

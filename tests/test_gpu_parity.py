@@ -215,7 +215,7 @@ def test_constitutive_hook(torch_cuda, model):
 @pytest.mark.parametrize("case", ["ancf_6x6_graded_svk", "ancf_4x4_perturbed_svk", "ancf_5x5_graded_svk_kv",
                                   "ancf_4x4_svk_kv", "ancf_3x3_svk", "t10_100el_perturbed_svk_keast5",
                                   "t10_5x3x2_straight_svk_keast5", "t10_4x3x2_straight_svk_4pt",
-                                  "t10_5x3x1_svk_keast5_ragged"])
+                                  "t10_5x3x1_svk_keast5_ragged", "cfg1_svk_4pt"])
 def test_force_only_parity(torch_cuda, case):
     """tlfea_force_only (the AdamW inner evaluation) on the class and the
     per-(e,q) table paths, with and without Kelvin-Voigt."""
@@ -240,6 +240,24 @@ def test_many_body_force_only(torch_cuda):
     ctx = T.Context.from_mesh(mesh, mat, 1)
     f = ctx.force_only(dev(torch, x), dev(torch, v)).cpu().numpy()
     assert rel(f, f0) <= TOL
+
+
+@pytest.mark.parametrize("rule", [0, 1])
+def test_many_body_force_only_persistent(torch_cuda, rule):
+    """Class-mode force-only kernel with persistent warps (several grid-stride
+    sweeps: 58k elements > one resident wave) under both rules, and from a
+    non-tile-aligned element offset (begin/interior/finish of a 2-part
+    virtual partition would start mid-tile)."""
+    torch = torch_cuda
+    import paper_2604_10357_b200 as T
+    mesh, x, v = synth.many_body(n_bodies=60)
+    mat = dict(synth.TIRE_DROP)
+    pr = oracle.Problem(mesh, mat, rule)
+    _, _, f0 = pr.eval(x, v, v, None, 1e-3, hessian=False)
+    ctx = T.Context.from_mesh(mesh, mat, rule)
+    assert ctx.info["n_geometry_classes"] > 0
+    f = ctx.force_only(dev(torch, x), dev(torch, v)).cpu().numpy()
+    assert rel(f, f0) <= TOL, rel(f, f0)
 
 
 def test_eval_host_matches_device(torch_cuda):
