@@ -61,61 +61,6 @@ static FArgs f_args(const Context* c, const double* fscr, const double* fpart_in
   return A;
 }
 
-// f_int and the residual g = (1/h) M (v - v_n) + f_int - f_ext - f_ff
-// (Eq. residual / grad_L), one thread per owned node.
-__global__ void k_gather_f(int64_t n_own, int nen, const int32_t* __restrict__ node_ptr,
-                           const uint32_t* __restrict__ node_ent, const double* __restrict__ fscr,
-                           const double* __restrict__ fpart_in, const int32_t* __restrict__ own_nodes,
-                           const int32_t* __restrict__ rowptr_c, const int32_t* __restrict__ cols_c,
-                           const double* __restrict__ M, const double* __restrict__ fff,
-                           const double* __restrict__ v, const double* __restrict__ vn,
-                           const double* __restrict__ fext, double h, int mode, int sorted,
-                           double* __restrict__ g, double* __restrict__ fint) {
-  // mode 0: full (f from scratch + residual); 1: f only -> fint; 2: residual from fpart_in
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n_own) return;
-  double f0 = 0.0, f1 = 0.0, f2 = 0.0;
-  if (mode == 2) {
-    f0 = fpart_in[3 * i];
-    f1 = fpart_in[3 * i + 1];
-    f2 = fpart_in[3 * i + 2];
-  } else {
-#pragma unroll 4
-    for (int32_t t = node_ptr[i]; t < node_ptr[i + 1]; ++t) {
-      const double* s;
-      if (sorted) {
-        s = fscr + (int64_t)t * 3;  // node-sorted force scratch
-      } else {
-        const uint32_t en = node_ent[t];
-        s = fscr + ((int64_t)(en >> 4) * nen + (en & 15)) * 3;
-      }
-      f0 += s[0];
-      f1 += s[1];
-      f2 += s[2];
-    }
-  }
-  if (fint) {
-    fint[3 * i] = f0;
-    fint[3 * i + 1] = f1;
-    fint[3 * i + 2] = f2;
-  }
-  if (mode == 1 || !g) return;
-  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
-#pragma unroll 4
-  for (int32_t p = rowptr_c[i]; p < rowptr_c[i + 1]; ++p) {
-    const int64_t J = cols_c[p];
-    const double mm = M[p];
-    m0 += mm * (v[3 * J] - (vn ? vn[3 * J] : 0.0));
-    m1 += mm * (v[3 * J + 1] - (vn ? vn[3 * J + 1] : 0.0));
-    m2 += mm * (v[3 * J + 2] - (vn ? vn[3 * J + 2] : 0.0));
-  }
-  const int64_t I = own_nodes[i];
-  const double r = 1.0 / h;
-  g[3 * i] = m0 * r + f0 - (fext ? fext[3 * I] : 0.0) - fff[3 * i];
-  g[3 * i + 1] = m1 * r + f1 - (fext ? fext[3 * I + 1] : 0.0) - fff[3 * i + 1];
-  g[3 * i + 2] = m2 * r + f2 - (fext ? fext[3 * I + 2] : 0.0) - fff[3 * i + 2];
-}
-
 // ------------------------------------------------ Stage 1 / Stage 2 alone
 
 template <int MODEL>
@@ -230,15 +175,8 @@ __global__ void k_constitutive(int64_t n, MatDev m, const double* __restrict__ F
 tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, const double* fext, double h,
                              double* g, double* fint, bool partial_only, cudaStream_t s) {
   if (c->n_own == 0) return TLFEA_OK;
-  if (c->fdest) {
-    k_gather_f_dof<<<grid_for(3 * c->n_own, kFgBlock), kFgBlock, 0, s>>>(
-        f_args(c, c->fscr, nullptr, v, vn, fext, h, partial_only ? 1 : 0, g, fint));
-    TL_CHECK_LAUNCH();
-    return TLFEA_OK;
-  }
-  k_gather_f<<<grid_for(c->n_own, 256), 256, 0, s>>>(c->n_own, c->nen, c->node_ptr, c->node_ent, c->fscr, nullptr,
-                                                     c->own_nodes, c->rowptr_c, c->cols_c, c->M, c->fff, v, vn,
-                                                     fext, h, partial_only ? 1 : 0, c->fdest != nullptr, g, fint);
+  k_gather_f_dof<<<grid_for(3 * c->n_own, kFgBlock), kFgBlock, 0, s>>>(
+      f_args(c, c->fscr, nullptr, v, vn, fext, h, partial_only ? 1 : 0, g, fint));
   TL_CHECK_LAUNCH();
   return TLFEA_OK;
 }
@@ -415,15 +353,9 @@ tlfea_status launch_norms2(Context* c, const double* a, const double* b, double*
 tlfea_status launch_residual(Context* c, const double* fint, const double* v, const double* vn,
                              const double* fext, double h, double* g, cudaStream_t s) {
   if (c->n_own == 0) return TLFEA_OK;
-  if (g) {
-    k_gather_f_dof<<<grid_for(3 * c->n_own, kFgBlock), kFgBlock, 0, s>>>(
-        f_args(c, c->fscr, fint, v, vn, fext, h, 2, g, nullptr));
-    TL_CHECK_LAUNCH();
-    return TLFEA_OK;
-  }
-  k_gather_f<<<grid_for(c->n_own, 256), 256, 0, s>>>(c->n_own, c->nen, c->node_ptr, c->node_ent, c->fscr, fint,
-                                                     c->own_nodes, c->rowptr_c, c->cols_c, c->M, c->fff, v, vn,
-                                                     fext, h, 2, c->fdest != nullptr, g, nullptr);
+  if (!g) return TLFEA_OK;  // nothing to write
+  k_gather_f_dof<<<grid_for(3 * c->n_own, kFgBlock), kFgBlock, 0, s>>>(
+      f_args(c, c->fscr, fint, v, vn, fext, h, 2, g, nullptr));
   TL_CHECK_LAUNCH();
   return TLFEA_OK;
 }

@@ -1,5 +1,4 @@
-// fgather.cuh — the per-DOF force gather / residual of libtlfea, shared by the
-// stand-alone gather kernel (eval.cu) and the fused persistent eval (element.cu).
+// fgather.cuh — the per-DOF force gather / residual of libtlfea (eval.cu).
 //
 //   f_int[3i+d] = sum of the node's element forces (ascending element order)
 //   g[3i+d]     = (1/h) sum_J M_IJ (v - v_n)_{3J+d} + f_int - f_ext - f_ff
