@@ -109,6 +109,9 @@ def _declare(L):
     L.orc_eval.argtypes = [i, i, i, _d, i64, _i32, i64, _d, _d, _i64, _i64, _d, _d, _i64, _i64,
                            _d, _d, _d, _d, d, _d, _d, _d]
     L.orc_eval_chunked.argtypes = L.orc_eval.argtypes
+    L.orc_eval_kvc.argtypes = L.orc_eval.argtypes
+    L.orc_element_force_local.argtypes = [i, i, i, _d, _i32, _d, _d, _d, _d, _d]
+    L.orc_element_kvc.argtypes = [i, i, i, _d, _i32, _d, _d, _d, _d, d, _d]
     L.orc_max_threads.restype = i
     L.orc_eval_rows.argtypes = [i, i, i, i, _d, _i32, _d, _d, _d, _d, d, i64, _i64, _i64, _i64,
                                 i64, _i64, _d, _d, _d]
@@ -248,6 +251,24 @@ def element(elem, rule, model, mat, conn_e, X, x, v=None, LWH=None, tangent=True
     return fe, (Ke.reshape(nd, nd) if tangent else None)
 
 
+def element_force_local(elem, rule, model, mat, conn_e, X, xe, ve, LWH=None):
+    """f_e [3 n_en] from LOCAL coordinates xe and velocities ve [3 n_en]."""
+    fe = np.zeros(3 * n_en(elem))
+    lib().orc_element_force_local(elem, rule, model, _p(mat_array(mat)), _p(_i32a(conn_e), _i32), _p(_f64(X)),
+                                  _p(_f64(LWH)), _p(_f64(xe)), _p(_f64(ve)), _p(fe))
+    return fe
+
+
+def element_kvc(elem, rule, model, mat, conn_e, X, x, v, h, LWH=None):
+    """Consistent Kelvin-Voigt element tangent Kc = h df/dx + df/dv [3n_en, 3n_en]
+    (NEXT-4; complex step of the element force with x = q_n + h v)."""
+    nd = 3 * n_en(elem)
+    Kc = np.zeros(nd * nd)
+    lib().orc_element_kvc(elem, rule, model, _p(mat_array(mat)), _p(_i32a(conn_e), _i32), _p(_f64(X)),
+                          _p(_f64(LWH)), _p(_f64(x)), _p(_f64(v)), float(h), _p(Kc))
+    return Kc.reshape(nd, nd)
+
+
 def element_energy(elem, rule, model, mat, conn_e, X, xe, LWH=None) -> float:
     return float(lib().orc_element_energy(elem, rule, model, _p(mat_array(mat)),
                                           _p(_i32a(conn_e), _i32), _p(_f64(X)), _p(_f64(LWH)),
@@ -367,17 +388,21 @@ class Problem:
         return f
 
     def eval(self, x, v, vn=None, fext=None, h=1e-3, hessian=True, use_fff=True, lam=None, rho=0.0,
-             all_cores=False):
+             all_cores=False, kv_consistent=False):
         """Returns (g, H or None, f_int) on the full DOF pattern. With
         constraints: g += h C^T (lam + rho c(x)) (Eq. residual P:101-113,
         P:484-489) and H += h^2 rho C^T C (Eq. hessian).
         all_cores: the element loop on every host core (orc_eval_chunked of
-        the OpenMP build; bitwise equal to the serial evaluation)."""
+        the OpenMP build; bitwise equal to the serial evaluation).
+        kv_consistent (NEXT-4): H = M/h + sum_e (h df_e/dx + df_e/dv), the
+        consistent Kelvin-Voigt tangent dg/dv (orc_eval_kvc), non-symmetric."""
         nd = 3 * self.n_coef
         g = np.zeros(nd)
         fint = np.zeros(nd)
         H = np.zeros(self.nnz) if hessian else None
         fn = lib_omp().orc_eval_chunked if all_cores else lib().orc_eval
+        if kv_consistent and hessian:
+            fn = lib().orc_eval_kvc
         fn(self.elem, self.rule, self.model, _p(self.matv), self.n_el,
                        _p(self.conn, _i32), self.n_coef, _p(self.X), _p(self.dims),
                        _p(self.rowptr_c, _i64), _p(self.cols_c, _i64), _p(self.M),

@@ -448,6 +448,68 @@ void element_fK(int elem, int rule, int model, const double* mat, const double* 
   }
 }
 
+// Element internal force f_e[3 nen] (Eq. fint_local) from LOCAL
+// coordinates xe and velocities ve [3 nen], generic in the scalar type so the
+// complex step can differentiate it: F = sum_a x_a (x) grad N_a, Fdot =
+// sum_a v_a (x) grad N_a, P = P_el(F) + P_v(F, Fdot) (Q7, Q9).
+template <class T>
+void element_force_t(int elem, int rule, int model, const double* mat, const double* X,
+                     const int64_t* cf, const double* LWH, const T* xe, const T* ve, T* fe) {
+  double pts[48][3], w[48];
+  const int nq = quadrature(rule, pts, w);
+  const int nen = n_en_of(elem);
+  for (int r = 0; r < 3 * nen; ++r) fe[r] = T(0.0);
+  for (int q = 0; q < nq; ++q) {
+    double gN[16][3];
+    const double J0w = geom_at(elem, X, cf, LWH, pts[q], gN, nullptr) * w[q];
+    T F[9], Fd[9];
+    for (int i = 0; i < 9; ++i) F[i] = Fd[i] = T(0.0);
+    for (int a = 0; a < nen; ++a)
+      for (int i = 0; i < 3; ++i)
+        for (int J = 0; J < 3; ++J) {
+          F[3 * i + J] += xe[3 * a + i] * gN[a][J];
+          Fd[3 * i + J] += ve[3 * a + i] * gN[a][J];
+        }
+    T P[9], Pv[9];
+    pk1_elastic(model, mat, F, P);
+    pk1_kv(F, Fd, mat[6], mat[7], Pv);
+    for (int i = 0; i < 9; ++i) P[i] += Pv[i];
+    for (int a = 0; a < nen; ++a)
+      for (int i = 0; i < 3; ++i) {
+        T s = T(0.0);
+        for (int J = 0; J < 3; ++J) s += P[3 * i + J] * gN[a][J];
+        fe[3 * a + i] += s * J0w;
+      }
+  }
+}
+
+// Consistent Kelvin-Voigt element tangent (SURVEY §8(f) NEXT-4, P:497-501,
+// P:526): the derivative of the element force of the velocity residual
+// g(v) = M (v - v_n)/h + f_int(q_n + h v, v) - ... (Eq. residual P:101-113,
+// reading Q9) with respect to the element's velocities, x and v moving
+// together (dx = h dv):
+//   Kc[r][s] = d f_e[r] / d v_e[s] = h df/dx + df/dv
+//            = Im f_e(x + i h eps e_s, v + i eps e_s) / eps   (complex step).
+// With eta = lambda_d = 0 it is h K_e (the elastic tangent of element_fK).
+void element_Kc_csd(int elem, int rule, int model, const double* mat, const double* X,
+                    const int64_t* cf, const double* LWH, const double* x, const double* v,
+                    double h, double* Kc) {
+  const int nen = n_en_of(elem), nd = 3 * nen;
+  const double eps = 1e-30;
+  std::vector<cplx> xe(nd), ve(nd), fe(nd);
+  for (int s = 0; s < nd; ++s) {
+    for (int a = 0; a < nen; ++a)
+      for (int i = 0; i < 3; ++i) {
+        xe[3 * a + i] = cplx(x[3 * cf[a] + i], 0.0);
+        ve[3 * a + i] = cplx(v ? v[3 * cf[a] + i] : 0.0, 0.0);
+      }
+    xe[s] += cplx(0.0, h * eps);
+    ve[s] += cplx(0.0, eps);
+    element_force_t<cplx>(elem, rule, model, mat, X, cf, LWH, xe.data(), ve.data(), fe.data());
+    for (int r = 0; r < nd; ++r) Kc[r * nd + s] = fe[r].imag() / eps;
+  }
+}
+
 // Element strain energy Pi_e = sum_q W(F) J0 w_q (Eq. cost), generic
 // in the coordinate scalar type so complex-step d(Pi)/dx can pin the force.
 template <class T>
@@ -802,6 +864,23 @@ void orc_element(int elem, int rule, int model, const double* mat, const int32_t
   element_fK(elem, rule, model, mat, X, cf, LWH, x, v, fe, Ke);
 }
 
+// Element force from LOCAL xe, ve [3 nen] (for FD pins of the consistent tangent).
+void orc_element_force_local(int elem, int rule, int model, const double* mat, const int32_t* conn_e,
+                             const double* X, const double* LWH, const double* xe, const double* ve,
+                             double* fe) {
+  int64_t cf[16];
+  elem_coefs(elem, conn_e, 0, cf);
+  element_force_t<double>(elem, rule, model, mat, X, cf, LWH, xe, ve, fe);
+}
+// Consistent Kelvin-Voigt element tangent Kc [3 nen][3 nen] (x, v global).
+void orc_element_kvc(int elem, int rule, int model, const double* mat, const int32_t* conn_e,
+                     const double* X, const double* LWH, const double* x, const double* v, double h,
+                     double* Kc) {
+  int64_t cf[16];
+  elem_coefs(elem, conn_e, 0, cf);
+  element_Kc_csd(elem, rule, model, mat, X, cf, LWH, x, v, h, Kc);
+}
+
 // Element energy with LOCAL coordinates xe [3 nen] (for FD / CSD pins).
 double orc_element_energy(int elem, int rule, int model, const double* mat, const int32_t* conn_e,
                           const double* X, const double* LWH, const double* xe) {
@@ -923,6 +1002,44 @@ void orc_eval(int elem, int rule, int model, const double* mat, int64_t n_el, co
         }
         const int64_t i = 3 * I + d;
         g[i] = s / h + fint[i] - (fext ? fext[i] : 0.0) - (fff ? fff[i] : 0.0);
+      }
+}
+
+// The evaluation with the CONSISTENT Kelvin-Voigt tangent (NEXT-4): g and
+// f_int exactly as orc_eval, and
+//   H = M/h + sum_e Kc_e,   Kc_e = h df_e/dx + df_e/dv   (element_Kc_csd),
+// i.e. H = dg/dv of Eq. residual with x = q_n + h v; in general
+// non-symmetric. Element order, full DOF CSR (rowptr, cols).
+void orc_eval_kvc(int elem, int rule, int model, const double* mat, int64_t n_el, const int32_t* conn,
+                  int64_t n_coef, const double* X, const double* dims, const int64_t* rowptr_c,
+                  const int64_t* cols_c, const double* M, const double* fff, const int64_t* rowptr,
+                  const int64_t* cols, const double* x, const double* v, const double* vn,
+                  const double* fext, double h, double* g, double* H, double* fint) {
+  orc_eval(elem, rule, model, mat, n_el, conn, n_coef, X, dims, rowptr_c, cols_c, M, fff, rowptr, cols,
+           x, v, vn, fext, h, g, nullptr, fint);
+  const int nen = n_en_of(elem), nd = 3 * nen;
+  const int64_t ndof = 3 * n_coef;
+  for (int64_t p = 0; p < rowptr[ndof]; ++p) H[p] = 0.0;
+  std::vector<double> Kc((size_t)nd * nd);
+  for (int64_t e = 0; e < n_el; ++e) {
+    int64_t cf[16];
+    elem_coefs(elem, conn, e, cf);
+    element_Kc_csd(elem, rule, model, mat, X, cf, dims_of(elem, dims, e), x, v, h, Kc.data());
+    for (int a = 0; a < nen; ++a)
+      for (int d = 0; d < 3; ++d)
+        for (int b = 0; b < nen; ++b)
+          for (int f = 0; f < 3; ++f) {
+            const int64_t r = 3 * cf[a] + d;
+            const int64_t p = find_col(cols, rowptr[r], rowptr[r + 1], 3 * cf[b] + f);
+            H[p] += Kc[(3 * a + d) * nd + 3 * b + f];
+          }
+  }
+  for (int64_t I = 0; I < n_coef; ++I)
+    for (int64_t k = rowptr_c[I]; k < rowptr_c[I + 1]; ++k)
+      for (int d = 0; d < 3; ++d) {
+        const int64_t r = 3 * I + d;
+        const int64_t p = find_col(cols, rowptr[r], rowptr[r + 1], 3 * cols_c[k] + d);
+        H[p] += M[k] / h;
       }
 }
 
