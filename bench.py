@@ -325,7 +325,8 @@ def run_ours(args):
     kv = cfg.material.get("eta_damp", 0) > 0 or cfg.material.get("lambda_damp", 0) > 0
     t_setup = time.perf_counter()
     ctx = T.Context.from_mesh(mesh, cfg.material, cfg.quadrature, rank=rank, nranks=world, device=local,
-                              hessian=args.hessian, reference_layout="tables" if args.tables else "auto")
+                              hessian=args.hessian, reference_layout="tables" if args.tables else "auto",
+                              kv_consistent=args.kv_consistent)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
     info = ctx.info
@@ -472,6 +473,7 @@ def run_ours(args):
                        "material": ["svk", "mooney_rivlin"][cfg.material["model"]] + ("+kv" if kv else ""),
                        "path": "force_only" if force_only else "force+tangent+residual (tlfea_eval)",
                        "hessian_storage": args.hessian,
+                       "tangent": "consistent_kv (NEXT-4)" if info.get("kv_consistent_tangent") else "elastic (Q8)",
                        "parallelism": f"element-partition x{world}" if world > 1 else "1 GPU",
                        "geometry_classes": info["n_geometry_classes"],
                        "reference_layout": ["classes", "per-(e,q) tables", "affine min layout"][info["reference_layout"]],
@@ -628,6 +630,8 @@ def main():
     ap.add_argument("--mesh", choices=["kuhn", "straight"], default="kuhn",
                     help="straight: the T10 mesh with randomly displaced corners (straight-sided, non-congruent: "
                          "the affine min layout instead of geometry classes)")
+    ap.add_argument("--kv-consistent", action="store_true",
+                    help="H = the consistent Kelvin-Voigt tangent dg/dv (NEXT-4; configs with damping, e.g. 2)")
     ap.add_argument("--ladder", action="store_true",
                     help="the paper's six-resolution ladders (T10, ANCF3443, ANCF3243), one line per rung")
     ap.add_argument("--tables", action="store_true",

@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define TLFEA_ABI_VERSION 7
+#define TLFEA_ABI_VERSION 8
 
 typedef struct tlfea_ctx_s* tlfea_ctx;
 
@@ -166,6 +166,24 @@ typedef struct {
                              whenever the T10 mesh is straight-sided (no
                              classes), else the tables. Results agree to
                              rounding whichever is used. */
+  int32_t kv_consistent_tangent; /* 0 (default): H = M/h + h K_t with the
+                             elastic tangent only (Eq. hessian, K_t
+                             "from F" P:526; reading Q8). 1 (SURVEY §8(f)
+                             NEXT-4): with Kelvin-Voigt damping, H is the
+                             consistent tangent of the velocity residual,
+                             H = dg/dv = M/h + h df_int/dx + df_int/dv with
+                             x = q_n + h v (Eq. residual, reading Q9):
+                             per element block K_ab = h K_ab^el + eta w (g_b ga^T
+                             + d_ab F F^T) + lambda_d w g_a g_b^T (from Fdot's
+                             dependence on v) + h w (s^v_ab I + eta d_ab F Fdot^T
+                             + eta g_b gdot_a^T + lambda_d g_a gdot_b^T) (from
+                             F's, with S_v fixed), g = F grad N, gdot = Fdot grad N,
+                             s^v_ab = grad N_a . S_v grad N_b, d_ab = grad N_a .
+                             grad N_b, summed over q with w = J0 w_q. NOT
+                             symmetric: FULL storage, single rank only
+                             (TLFEA_E_INVALID with hessian_upper or nranks > 1);
+                             tlfea_assemble_hessian (no velocities) then
+                             returns TLFEA_E_INVALID. No effect without damping. */
 } tlfea_options;
 
 /* Sizes of a context (tlfea_info). Rows/DOFs are GLOBAL indices; in a
@@ -193,6 +211,9 @@ typedef struct {
   int64_t n_constraints;   /* rows m of the context's constraint set (0: none) */
   int32_t reference_layout;/* in use: 0 geometry classes, 1 per-(e,q) tables,
                               2 affine (min) layout */
+  int32_t kv_consistent_tangent; /* 1 if H is the consistent Kelvin-Voigt
+                              tangent (options.kv_consistent_tangent with
+                              damping), else 0 */
 } tlfea_info_t;
 
 /* ---------------------------------------------------------------- setup -- */

@@ -20,7 +20,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-ABI_VERSION = 7  # include/tlfea.h TLFEA_ABI_VERSION (struct layouts of this binding)
+ABI_VERSION = 8  # include/tlfea.h TLFEA_ABI_VERSION (struct layouts of this binding)
 LIB_PATH = os.environ.get("TLFEA_LIB") or os.path.join(_HERE, "libtlfea.so")
 _lib = None
 _lock = threading.Lock()
@@ -60,7 +60,7 @@ class Options(C.Structure):
                 ("ancf_dims", C.c_double * 3), ("rank", C.c_int32), ("nranks", C.c_int32),
                 ("elem_part", C.POINTER(C.c_int32)), ("device", C.c_int32),
                 ("constraints", C.POINTER(Constraints)), ("hessian_upper", C.c_int32),
-                ("reference_layout", C.c_int32)]
+                ("reference_layout", C.c_int32), ("kv_consistent_tangent", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -69,7 +69,7 @@ class Info(C.Structure):
                 ("n_dof", C.c_int64), ("nnz_coef", C.c_int64), ("nnz", C.c_int64), ("n_owned_nodes", C.c_int64),
                 ("affine", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32), ("device_bytes", C.c_int64),
                 ("n_geometry_classes", C.c_int32), ("fused_eval", C.c_int32), ("n_constraints", C.c_int64),
-                ("reference_layout", C.c_int32)]
+                ("reference_layout", C.c_int32), ("kv_consistent_tangent", C.c_int32)]
 
 class AdamWParams(C.Structure):
     _fields_ = [("alpha", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
@@ -214,13 +214,15 @@ class Context:
     def __init__(self, element: int, conn: np.ndarray, X: np.ndarray, mat: dict, quadrature: int,
                  dims: np.ndarray | None = None, mass_rule: int = 0, gravity=(0.0, 0.0, 0.0),
                  rank: int = 0, nranks: int = 1, elem_part=None, device: int = 0, constraints: dict | None = None,
-                 hessian: str = "full", reference_layout: str = "auto"):
+                 hessian: str = "full", reference_layout: str = "auto", kv_consistent: bool = False):
         """constraints: dict rowptr, cols (DOF ids), vals, b of c(q) = C q - b
         (tlfea_constraints; NEXT-3). hessian: "full" or "upper" storage of H
         (options.hessian_upper; NEXT-4). reference_layout: "auto" (geometry
         classes when the mesh allows) or "tables" (the paper's per-(e,q)
         tables always) or "affine" (the min layout of straight-sided T10
-        before classes; options.reference_layout)."""
+        before classes; options.reference_layout). kv_consistent: H is the
+        consistent Kelvin-Voigt tangent dg/dv (options.kv_consistent_tangent;
+        NEXT-4; non-symmetric, FULL storage, single rank)."""
         if hessian not in ("full", "upper"):
             raise ValueError("hessian must be 'full' or 'upper'")
         if reference_layout not in ("auto", "tables", "affine"):
@@ -244,7 +246,7 @@ class Context:
         opts = Options(quadrature, mass_rule, (C.c_double * 3)(*gravity), (C.c_double * 3)(0, 0, 0), rank, nranks,
                        None if self._part is None else self._part.ctypes.data_as(C.POINTER(C.c_int32)), device,
                        None if con is None else C.pointer(con), 1 if hessian == "upper" else 0,
-                       {"auto": 0, "tables": 1, "affine": 2}[reference_layout])
+                       {"auto": 0, "tables": 1, "affine": 2}[reference_layout], 1 if kv_consistent else 0)
         self.material = dict(mat)
         m = make_material(mat)
         h = C.c_void_p()

@@ -118,6 +118,7 @@ tlfea_status tlfea_info(tlfea_ctx ctx, tlfea_info_t* o) {
   o->fused_eval = 0;
   o->n_constraints = c.n_con;
   o->reference_layout = c.n_cls > 0 ? 0 : (c.aff ? 2 : 1);
+  o->kv_consistent_tangent = c.kvc;
   return TLFEA_OK;
 }
 
@@ -254,6 +255,7 @@ tlfea_status tlfea_eval(tlfea_ctx ctx, const double* x, const double* v, const d
   TRY(use_device(c));
   const cudaStream_t s = as_stream(stream);
   c.last_stream = s;
+  c.kvc_inv_h = 1.0 / h;
   TIMED(0, launch_element_kernel(&c, x, v, true, s));
   TIMED(1, launch_gather_H(&c, h, H_out, s));
   TIMED(2, launch_gather_f(&c, v, v_n, f_ext, h, g_out, f_int_out, false, s));
@@ -422,6 +424,7 @@ tlfea_status tlfea_assemble_hessian(tlfea_ctx ctx, const double* x, double h, do
   TRY(check_h(h));
   if (c.nranks > 1) return fail(TLFEA_E_INVALID, "single-rank contexts only");
   if (!x || !H_out) return fail(TLFEA_E_INVALID, "NULL x or H_out");
+  if (c.kvc) return fail(TLFEA_E_INVALID, "kv_consistent_tangent context: the tangent needs v (use tlfea_eval)");
   // the tangent is elastic only (reading Q8): evaluated without velocities
   TRY(use_device(c));
   const cudaStream_t s = as_stream(stream);
@@ -451,6 +454,7 @@ tlfea_status tlfea_eval_begin(tlfea_ctx ctx, const double* x, const double* v, i
   TRY(use_device(c));
   const cudaStream_t s = as_stream(stream);
   c.last_stream = s;
+  c.kvc_inv_h = 1.0 / h;
   // the boundary elements (local [0, n_el_bnd)) and the send buffer
   TIMED(0, launch_element_kernel(&c, x, v, !force_only, s, 0, c.nranks > 1 ? c.n_el_bnd : c.n_el));
   if (c.nranks > 1) {

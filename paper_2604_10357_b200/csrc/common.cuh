@@ -120,6 +120,13 @@ struct Context {
   // the diagonal) has entry (d, f) at ubase[I] + 3 k + f + d (2 + 3 L_I)
   // - d (d - 1) / 2 (f >= d when k = 0).
   int upper = 0;
+  // consistent Kelvin-Voigt tangent (options.kv_consistent_tangent with damping,
+  // NEXT-4): each gather-sorted scratch slot holds 18 values, the unit's (I,J)
+  // and (J,I) contributions in their own orientation (non-symmetric blocks);
+  // kvc_inv_h = 1/h of the evaluation in flight (the element kernel scales the
+  // df/dv part by 1/h so the gather's h * acc + M/h gives h df/dx + df/dv).
+  int kvc = 0;
+  double kvc_inv_h = 0.0;
   int64_t nnz_H = 0;           // values of H as stored
   int32_t* ubase = nullptr;    // [n_own + 1] UPPER offsets of coefficient rows
 

@@ -130,6 +130,7 @@ struct ElArgs {
   const int32_t* dest;
   const int32_t* fdest;
   unsigned long long* err;
+  double inv_h;  // consistent KV tangent only: 1/h of the evaluation (k_element_kvc)
 };
 
 __device__ __forceinline__ void pf_cp4(void* smem, const void* gmem) {
@@ -1886,6 +1887,312 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
 }
 
 
+// ------------------------------------------------- consistent KV tangent
+// SURVEY §8(f) NEXT-4 (options.kv_consistent_tangent): H = dg/dv of the
+// velocity residual (Eq. residual, x = q_n + h v, reading Q9) with
+// Kelvin-Voigt damping, H = M/h + h (K^el + K^vx + K^vv / h), where per
+// quadrature point (w = J0 w_q, g = F grad N, gd = Fdot grad N, d_ab =
+// grad N_a . grad N_b, s^v_ab = grad N_a . S_v grad N_b):
+//   K^vv_ab = w (eta g_b g_a^T + eta d_ab F F^T + lam_d g_a g_b^T)   (dP_v/dFdot)
+//   K^vx_ab = w (s^v_ab I + eta d_ab F Fdot^T + eta g_b gd_a^T + lam_d g_a gd_b^T)
+// (dP_v/dF at fixed Fdot; DESIGN.md §9a derives both). K^vv and K^el are
+// symmetric, K^vx is not, so every element pair (a, b), a <= b, yields two
+// blocks: lane a accumulates KA = K_ab and KB = K_ba for each of its partners.
+// The gather-sorted scratch slot of an element upper block holds 18 values:
+// the contribution to the unit's H(I,J) then to H(J,I), each in its own
+// orientation (no transposes). One lane per element node as in element_group
+// (T10: 3 elements per warp, ANCF3443: 2 lanes per node, beam: 4 elements per
+// warp); three block passes keep the 2 x 9 accumulators per partner in
+// registers. A variant path: it is not tuned like the symmetric kernels.
+template <int ELEM, int NQ, int MODEL, bool CLS>
+__device__ __forceinline__ void element_group_kvc(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab) {
+  using G = Geo<ELEM>;
+  constexpr int NEN = G::NEN, GROUP = G::GROUP, EPW = G::EPW, NUB = G::NUB, NB = G::NB;
+  constexpr int TABW = NEN * 3 + 1;
+  constexpr int NPASS = 3, NBP = (NB + NPASS - 1) / NPASS;
+  constexpr bool MULTI = ELEM != 1;
+  __shared__ double s_part[kWarps][18][kLD];
+  __shared__ double s_F[kWarps][EPW][18];
+  __shared__ double s_node[kWarps][9][kLD];  // g, gd, grad N per lane
+  __shared__ double s_C[kWarps][EPW][MODEL == 1 ? 36 : 1];
+  __shared__ int32_t s_pos[kWarps][32];
+  const int64_t n_el = A.n_el;
+  const MatDev& mat = A.mat;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const bool lane_active = MULTI ? (lane < EPW * GROUP) : true;
+  const int g = (MULTI && lane_active) ? lane / GROUP : 0;
+  const int a = MULTI ? (lane_active ? lane % GROUP : 0) : (lane & 15);
+  const int half = MULTI ? 0 : (lane >> 4);
+  const int64_t e = grp * EPW + g;
+  const bool valid = lane_active && e < n_el;
+  const int gbase = g * GROUP;
+  const double ih = A.inv_h;
+
+  double xa[3] = {0, 0, 0}, va[3] = {0, 0, 0};
+  int ce = 0;
+  if (valid) {
+    const int64_t I = A.conn[e * NEN + a];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      xa[i] = A.x[3 * I + i];
+      va[i] = A.v[3 * I + i];
+    }
+    if (CLS) ce = A.cls[e];
+  }
+  double fa[3] = {0, 0, 0};
+  double KA[NBP][9], KB[NBP][9];
+#pragma unroll 1
+  for (int pass = 0; pass < NPASS; ++pass) {
+#pragma unroll
+    for (int j = 0; j < NBP; ++j)
+#pragma unroll
+      for (int r = 0; r < 9; ++r) KA[j][r] = KB[j][r] = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < NQ; ++q) {
+      double gN[3] = {0, 0, 0}, w = 0.0;
+      if (valid) {
+        if (CLS) {
+          const double* t = s_tab + (ce * NQ + q) * TABW;
+          gN[0] = t[3 * a];
+          gN[1] = t[3 * a + 1];
+          gN[2] = t[3 * a + 2];
+          w = t[3 * NEN];
+        } else {
+          const double* src = A.gradN + ((e * NQ + q) * NEN + a) * 3;
+          gN[0] = src[0];
+          gN[1] = src[1];
+          gN[2] = src[2];
+          w = A.J0w[e * NQ + q];
+        }
+      }
+      // F, Fdot = sum_a (x_a, v_a) (x) grad N_a over the element's lanes
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int J = 0; J < 3; ++J) {
+          s_part[wib][3 * i + J][lane] = xa[i] * gN[J];
+          s_part[wib][9 + 3 * i + J][lane] = va[i] * gN[J];
+        }
+      __syncwarp();
+      if (MULTI) {
+        if (lane_active) {
+          for (int comp = a; comp < 18; comp += GROUP) {
+            const double* p = &s_part[wib][comp][gbase];
+            double sum = 0.0;
+#pragma unroll
+            for (int b = 0; b < NEN; ++b) sum += p[b];
+            s_F[wib][g][comp] = sum;
+          }
+        }
+      } else {
+        const int comp = lane & 15;
+        if (comp < 9) {
+          const double* p = &s_part[wib][9 * half + comp][0];
+          double sum = 0.0;
+#pragma unroll
+          for (int b = 0; b < 16; ++b) sum += p[b];
+          s_F[wib][0][9 * half + comp] = sum;
+        }
+      }
+      __syncwarp();
+      double F[9], Fd[9];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) {
+        F[r] = s_F[wib][g][r];
+        Fd[r] = s_F[wib][g][9 + r];
+      }
+      double S[6], Sv[6];
+      MRState ms;
+      if (MODEL == 0) {
+        svk_S(F, mat.lam, mat.mu, S);
+      } else {
+        mr_state(F, ms);
+        if (valid && !(ms.J > 0.0) && a == 0 && half == 0) atomicMin(A.err, (unsigned long long)(e * 64 + q));
+        mr_S(ms, mat.C10, mat.C01, mat.kappa, S);
+      }
+      kv_S(F, Fd, mat.eta, mat.lamd, Sv);
+      double tw[3], twv[3];  // w S grad N_a, w S_v grad N_a
+#pragma unroll
+      for (int I = 0; I < 3; ++I) {
+        tw[I] = w * (sget(S, I, 0) * gN[0] + sget(S, I, 1) * gN[1] + sget(S, I, 2) * gN[2]);
+        twv[I] = w * (sget(Sv, I, 0) * gN[0] + sget(Sv, I, 1) * gN[1] + sget(Sv, I, 2) * gN[2]);
+      }
+      if (pass == 0) {  // f_a += F (w (S + S_v) grad N_a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          fa[i] = fma(F[3 * i], tw[0] + twv[0], fma(F[3 * i + 1], tw[1] + twv[1], fma(F[3 * i + 2], tw[2] + twv[2], fa[i])));
+      }
+      double ga[3], gda[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        ga[i] = F[3 * i] * gN[0] + F[3 * i + 1] * gN[1] + F[3 * i + 2] * gN[2];
+        gda[i] = Fd[3 * i] * gN[0] + Fd[3 * i + 1] * gN[1] + Fd[3 * i + 2] * gN[2];
+      }
+      double B[6], Cd[9];  // F F^T (Voigt), F Fdot^T
+#pragma unroll
+      for (int vv = 0; vv < 6; ++vv) {
+        int i, k;
+        voigt_pair(vv, i, k);
+        B[vv] = F[3 * i] * F[3 * k] + F[3 * i + 1] * F[3 * k + 1] + F[3 * i + 2] * F[3 * k + 2];
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) Cd[3 * i + k] = F[3 * i] * Fd[3 * k] + F[3 * i + 1] * Fd[3 * k + 1] + F[3 * i + 2] * Fd[3 * k + 2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        s_node[wib][i][lane] = ga[i];
+        s_node[wib][3 + i][lane] = gda[i];
+        s_node[wib][6 + i][lane] = gN[i];
+      }
+      double CB[MODEL == 1 ? 6 : 1][3];
+      if (MODEL == 1) {
+        if (lane_active && (MULTI || half == 0)) {
+          const int col = MULTI ? a : lane;
+          if (col < 6) {
+            double cc[6];
+            mr_Cv_column_dispatch(ms, mat.C10, mat.C01, mat.kappa, col, cc);
+#pragma unroll
+            for (int vv = 0; vv < 6; ++vv) s_C[wib][g][6 * vv + col] = w * cc[vv];
+          }
+        }
+      }
+      __syncwarp();
+      if constexpr (MODEL == 1) {
+        double Ba[6][3];
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv) {
+          int I, J;
+          voigt_pair(vv, I, J);
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+            Ba[vv][i] = (I == J) ? F[3 * i + I] * gN[I] : F[3 * i + I] * gN[J] + F[3 * i + J] * gN[I];
+        }
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv)
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < 6; ++ww) sacc = fma(s_C[wib][g][6 * vv + ww], Ba[ww][i], sacc);
+            CB[vv][i] = sacc;
+          }
+      }
+      // symmetric part coefficients: SVK folds K^vv / h into the Lame pair
+      const double lwe = MODEL == 0 ? w * (mat.lam + mat.lamd * ih) : w * mat.lamd * ih;
+      const double mwe = MODEL == 0 ? w * (mat.mu + mat.eta * ih) : w * mat.eta * ih;
+      const double ew = w * mat.eta, ldw = w * mat.lamd;
+#pragma unroll
+      for (int jj = 0; jj < NBP; ++jj) {
+        const int j = pass * NBP + jj;
+        const int b = j < NB ? partner<ELEM>(a, half, j) : -1;
+        if (b < 0) continue;
+        const int lb = gbase + b;
+        double gb[3], gdb[3], nb[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          gb[i] = s_node[wib][i][lb];
+          gdb[i] = s_node[wib][3 + i][lb];
+          nb[i] = s_node[wib][6 + i][lb];
+        }
+        const double s = tw[0] * nb[0] + tw[1] * nb[1] + tw[2] * nb[2];
+        const double sv = twv[0] * nb[0] + twv[1] * nb[1] + twv[2] * nb[2];
+        const double dd = gN[0] * nb[0] + gN[1] * nb[1] + gN[2] * nb[2];
+        double E[9];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            E[3 * i + k] = lwe * ga[i] * gb[k] + mwe * gb[i] * ga[k] + mwe * dd * B[vidx(i, k)] + (i == k ? s : 0.0);
+        if constexpr (MODEL == 1) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            double bb[6];
+#pragma unroll
+            for (int vv = 0; vv < 6; ++vv) {
+              int I, J;
+              voigt_pair(vv, I, J);
+              bb[vv] = (I == J) ? F[3 * k + I] * nb[I] : F[3 * k + I] * nb[J] + F[3 * k + J] * nb[I];
+            }
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              double acc = 0.0;
+#pragma unroll
+              for (int vv = 0; vv < 6; ++vv) acc = fma(CB[vv][i], bb[vv], acc);
+              E[3 * i + k] += acc;
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const double c = ew * dd * Cd[3 * i + k] + (i == k ? sv : 0.0);
+            KA[jj][3 * i + k] += E[3 * i + k] + c + ew * gb[i] * gda[k] + ldw * ga[i] * gdb[k];
+            KB[jj][3 * i + k] += E[3 * k + i] + c + ew * ga[i] * gdb[k] + ldw * gb[i] * gda[k];
+          }
+      }
+      __syncwarp();
+    }
+    if (valid && pass == 0 && (MULTI || half == 0)) {
+      const int64_t fp = A.fdest ? (int64_t)A.fdest[e * NEN + a] : e * NEN + a;
+      double* fo = A.fscr + fp * 3;
+      fo[0] = fa[0];
+      fo[1] = fa[1];
+      fo[2] = fa[2];
+    }
+    // blocks -> 18-value scratch slots: [H(I,J) part | H(J,I) part]
+    constexpr int NLB = MULTI ? EPW * GROUP : 32;
+    constexpr int NIT = (NLB + 2) / 3;
+    const int bi = lane / 9, rr = lane - 9 * (lane / 9);
+#pragma unroll
+    for (int jj = 0; jj < NBP; ++jj) {
+      const int j = pass * NBP + jj;
+      const int b = (valid && j < NB) ? partner<ELEM>(a, half, j) : -1;
+      int32_t pos = -1;
+      bool flip = false;
+      if (b >= 0) {
+        const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
+        const int32_t d = A.dest[e * NUB + ub];
+        pos = d >> 1;
+        // KA = K_ab; the unit's (I,J) block is K_{lo,hi} unless the dest bit flips it
+        flip = a != b && ((a > b) != ((d & 1) != 0));
+      }
+      s_pos[wib][lane] = pos;
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        if (b >= 0) {
+#pragma unroll
+          for (int r = 0; r < 9; ++r) s_part[wib][r][lane] = (flip != (part == 1)) ? KB[jj][r] : KA[jj][r];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+          const int blk = 3 * it + bi;
+          if (lane < 27 && blk < NLB) {
+            const int32_t p = s_pos[wib][blk];
+            if (p >= 0) k_store(A.Kscr + (int64_t)p * 18 + 9 * part + rr, s_part[wib][rr][blk]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+template <int ELEM, int NQ, int MODEL, bool CLS>
+__global__ void __launch_bounds__(kWarps * 32, 2) k_element_kvc(ElArgs A) {
+  extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
+  if (CLS) {
+    const int tot = A.n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1);
+    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_tab[t] = A.cls_tab[t];
+    __syncthreads();
+  }
+  const int64_t grp = A.g0 + (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  element_group_kvc<ELEM, NQ, MODEL, CLS>(grp, A, s_tab);
+}
+
+
 // ------------------------------------------------------------------ gather
 
 // v3: TMA bulk copies (cp.async.bulk global->shared, mbarrier completion),
@@ -2045,6 +2352,82 @@ __global__ void __launch_bounds__(kG3Warps * 32) k_gather_units_v3(GatherArgs A)
   gather_units_warp(((int64_t)blockIdx.x * kG3Warps + (threadIdx.x >> 5)) * 32, A, W);
 }
 
+
+// Consistent KV tangent gather (NEXT-4): as gather_units_warp, but each
+// scratch slot holds 18 values (the unit's H(I,J) part, then its H(J,I) part,
+// both in their own orientation) and the two blocks are written untransposed.
+constexpr int kG3WB2 = kG3WB / 2;  // 18-value blocks per window (same buffer)
+__device__ __forceinline__ void gather_units_warp_kvc(int64_t u0, const GatherArgs& A, G3Warp& W) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_units = A.n_units;
+  const double* __restrict__ Kscr = A.Kscr;
+  double* __restrict__ H = A.H;
+  if (u0 >= n_units) return;
+  const int64_t u = u0 + lane;
+  const bool valid = u < n_units;
+  const int64_t uend = min(u0 + 32, n_units);
+  const int64_t P0 = A.unit_ptr[u0], P1 = A.unit_ptr[uend];
+  int32_t my0 = 0, my1 = 0, off = 0, offT = -1, dg = 0;
+  double m = 0.0;
+  if (valid) {
+    my0 = A.unit_ptr[u];
+    my1 = A.unit_ptr[u + 1];
+    off = A.u_off[u];
+    offT = A.u_offT[u];
+    dg = A.u_deg[u];
+    m = A.u_m[u];
+  }
+  const int nwin = (int)((P1 - P0 + kG3WB2 - 1) / kG3WB2);
+  const uint32_t wk0 = W.wk;
+  auto issue = [&](int k) {
+    const int64_t w0 = P0 + (int64_t)k * kG3WB2, w1 = min(w0 + (int64_t)kG3WB2, P1);
+    const uint32_t wi = wk0 + k;  // 144-byte slots: always 16-byte aligned
+    bulk_load(W.buf[wi & 1], (const void*)(Kscr + w0 * 18), (unsigned)((w1 - w0) * 144), &W.bar[wi & 1]);
+  };
+  if (lane == 0 && nwin > 0) issue(0);
+  double acc[18];
+#pragma unroll
+  for (int r = 0; r < 18; ++r) acc[r] = 0.0;
+  for (int k = 0; k < nwin; ++k) {
+    if (lane == 0 && k + 1 < nwin) issue(k + 1);
+    const uint32_t wi = wk0 + k;
+    mbar_wait(&W.bar[wi & 1], (wi >> 1) & 1);
+    const int64_t w0 = P0 + (int64_t)k * kG3WB2, w1 = min(w0 + (int64_t)kG3WB2, P1);
+    const double* buf = W.buf[wi & 1];
+    const int64_t a0 = max((int64_t)my0, w0), a1 = min((int64_t)my1, w1);
+    for (int64_t t = a0; t < a1; ++t) {
+      const double* sb = buf + (t - w0) * 18;
+#pragma unroll
+      for (int r = 0; r < 18; ++r) acc[r] += sb[r];
+    }
+    __syncwarp();
+  }
+  W.wk = wk0 + nwin;
+  if (!valid) return;
+  const double h = A.h, mh = m / h;
+  const int deg = dg & 0xffff, degT = dg >> 16;
+  double* out = H + 3 * (int64_t)off;
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int f = 0; f < 3; ++f) h_store(out + 3 * d * deg + f, fma(h, acc[3 * d + f], d == f ? mh : 0.0));
+  if (offT >= 0) {
+    double* o2 = H + 3 * (int64_t)offT;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int f = 0; f < 3; ++f) h_store(o2 + 3 * d * degT + f, fma(h, acc[9 + 3 * d + f], d == f ? mh : 0.0));
+  }
+}
+
+__global__ void __launch_bounds__(kG3Warps * 32) k_gather_units_kvc(GatherArgs A) {
+  __shared__ __align__(16) double s_buf[kG3Warps][2][kG3Buf];
+  __shared__ __align__(8) uint64_t s_bar[kG3Warps][2];
+  G3Warp W;
+  g3_init(s_buf, s_bar, W);
+  gather_units_warp_kvc(((int64_t)blockIdx.x * kG3Warps + (threadIdx.x >> 5)) * 32, A, W);
+}
+
 // ------------------------------------------------------------- launchers
 
 static ElArgs el_args(const Context* c, const double* x, const double* v) {
@@ -2066,6 +2449,7 @@ static ElArgs el_args(const Context* c, const double* x, const double* v) {
   A.dest = c->dest;
   A.fdest = c->fdest;
   A.err = c->err_flag;
+  A.inv_h = c->kvc_inv_h;
   return A;
 }
 
@@ -2127,10 +2511,39 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
   return TLFEA_OK;
 }
 
+// Consistent KV tangent (NEXT-4): k_element_kvc, class tables or per-(e,q) tables.
+template <int ELEM, int NQ, int MODEL>
+static tlfea_status launch_el_kvc(Context* c, const double* x, const double* v, cudaStream_t s, int64_t e_begin,
+                                  int64_t e_end) {
+  using G = Geo<ELEM>;
+  const int64_t per_cta = (int64_t)kWarps * G::EPW;
+  if (e_end <= e_begin) return TLFEA_OK;
+  if (e_begin % per_cta != 0) return fail(TLFEA_E_INVALID, "internal: element range not tile aligned");
+  if (!c->dest) return fail(TLFEA_E_INVALID, "internal: consistent KV tangent needs the gather-sorted scratch");
+  const unsigned grid = (unsigned)((e_end - e_begin + per_cta - 1) / per_cta);
+  ElArgs A = el_args(c, x, v);
+  A.n_el = e_end;
+  A.g0 = e_begin / G::EPW;
+  if (c->n_cls > 0) {
+    const size_t smem = sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
+    auto kern = k_element_kvc<ELEM, NQ, MODEL, true>;
+    TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
+    kern<<<grid, kWarps * 32, smem, s>>>(A);
+  } else {
+    k_element_kvc<ELEM, NQ, MODEL, false><<<grid, kWarps * 32, 0, s>>>(A);
+  }
+  TL_CHECK_LAUNCH();
+  return TLFEA_OK;
+}
+
 template <int ELEM, int NQ, int MODEL>
 static tlfea_status launch_el_kv(Context* c, const double* x, const double* v, bool tan, cudaStream_t s, int64_t e0,
                                  int64_t e1) {
   const bool kv = c->mat.kv && v != nullptr;
+  if (tan && c->kvc) {
+    if (!v) return fail(TLFEA_E_INVALID, "consistent KV tangent: NULL v");
+    return launch_el_kvc<ELEM, NQ, MODEL>(c, x, v, s, e0, e1);
+  }
   if (tan)
     return kv ? launch_el<ELEM, NQ, MODEL, true, true>(c, x, v, s, e0, e1)
               : launch_el<ELEM, NQ, MODEL, false, true>(c, x, v, s, e0, e1);
@@ -2176,6 +2589,11 @@ static GatherArgs gather_args(const Context* c, double h, double* H) {
 tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
   if (c->n_units == 0) return TLFEA_OK;
   const int64_t per = (int64_t)kG3Warps * 32;
+  if (c->kvc) {
+    k_gather_units_kvc<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(gather_args(c, h, H));
+    TL_CHECK_LAUNCH();
+    return TLFEA_OK;
+  }
   k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(gather_args(c, h, H));
   TL_CHECK_LAUNCH();
   return TLFEA_OK;

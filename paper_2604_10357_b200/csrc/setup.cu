@@ -907,6 +907,11 @@ static tlfea_status validate(const tlfea_mesh* mesh, const tlfea_material* mat,
     return fail(TLFEA_E_INVALID, "hessian_upper must be 0 or 1");
   if (opts->hessian_upper && (opts->nranks != 1 || (opts->constraints && opts->constraints->m > 0)))
     return fail(TLFEA_E_UNSUPPORTED, "UPPER H storage: single-rank contexts without constraints only");
+  if (opts->kv_consistent_tangent != 0 && opts->kv_consistent_tangent != 1)
+    return fail(TLFEA_E_INVALID, "kv_consistent_tangent must be 0 or 1");
+  if (opts->kv_consistent_tangent && (opts->hessian_upper || opts->nranks != 1))
+    return fail(TLFEA_E_UNSUPPORTED,
+                "kv_consistent_tangent: the consistent tangent is non-symmetric (FULL storage, single rank)");
   if (mesh->n_elements >= (1ll << 31)) return fail(TLFEA_E_OVERFLOW, "n_elements >= 2^31");
   if (3 * mesh->n_coef >= (1ll << 31)) return fail(TLFEA_E_OVERFLOW, "3 n_coef >= 2^31");
   if (const tlfea_constraints* k = opts->constraints) {
@@ -1056,6 +1061,7 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   c->nq = n_qp_of(opts->quadrature);
   c->mass_rule = opts->mass_rule;
   c->force_tables = opts->reference_layout;
+  c->kvc = opts->kv_consistent_tangent && (mat->eta_damp > 0.0 || mat->lambda_damp > 0.0);
   c->mat_in = *mat;
   c->mat = make_matdev(*mat);
   for (int k = 0; k < 3; ++k) c->gravity[k] = opts->gravity[k];
@@ -1451,7 +1457,7 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   if (c->n_el * (int64_t)n_ublk_of(nen) >= (int64_t(1) << 31))
     return fail(TLFEA_E_OVERFLOW, "element tangent scratch exceeds 2^31 blocks: partition the mesh over more ranks");
   // +4 doubles: the bulk-copy gather rounds its windows out to 16-byte bounds
-  TL_TRY(c->alloc(&c->Kscr, (size_t)c->n_el * n_ublk_of(nen) * 9 + 4));
+  TL_TRY(c->alloc(&c->Kscr, (size_t)c->n_el * n_ublk_of(nen) * (c->kvc ? 18 : 9) + 4));
   TL_TRY(c->alloc(&c->fscr, (size_t)c->n_el * nen * 3));
   TL_TRY(c->alloc(&c->fpart, (size_t)3 * std::max<int64_t>(c->n_own, 1)));
 

@@ -44,7 +44,7 @@ def test_sm100a_code_in_library(T):
 
 
 def test_abi_version_and_no_cpu_fallback(T):
-    assert T.lib().tlfea_abi_version() == 7
+    assert T.lib().tlfea_abi_version() == 8
     torch = pytest.importorskip("torch")
     if torch.cuda.is_available():
         pytest.skip("a GPU is present; the no-device path is exercised on CPU hosts")
