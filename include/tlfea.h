@@ -85,7 +85,8 @@ typedef enum { TLFEA_SVK = 0, TLFEA_MOONEY_RIVLIN = 1 } tlfea_model;
  *  MR : W = C10(I1b-3) + C01(I2b-3) + kappa/2 (J-1)^2 (reading Q6).
  *  Kelvin-Voigt (active when eta_damp>0 or lambda_damp>0):
  *       Edot = (Fdot^T F + F^T Fdot)/2, S_v = 2 eta Edot + lambda_d tr(Edot) I,
- *       P_v = F S_v (reading Q7). Its tangent is NOT in H (Eq. hessian, Q8). */
+ *       P_v = F S_v (reading Q7). Its tangent is NOT in H (Eq. hessian, Q8)
+ *       unless options.kv_consistent_tangent asks for dg/dv (NEXT-4). */
 typedef struct {
   int32_t model; /* tlfea_model */
   double E, nu;            /* SVK */
@@ -296,7 +297,8 @@ tlfea_status tlfea_export_mass(tlfea_ctx ctx, double* M_out, double* fff_out,
  *   f_ext external nodal forces, or NULL (= 0)
  *   h   time step (> 0, else TLFEA_E_INVALID)
  * Outputs (DEVICE, owned rows): g_out [3*n_owned_nodes] residual;
- *   H_out [nnz] values of M/h + h K_t on tlfea_pattern (elastic tangent only;
+ *   H_out [nnz] values of M/h + h K_t on tlfea_pattern (elastic tangent, or the
+ *         consistent Kelvin-Voigt tangent per options.kv_consistent_tangent;
  *         full or UPPER storage per options.hessian_upper, info.nnz entries);
  *   f_int_out [3*n_owned_nodes] or NULL.
  * In a partitioned context (nranks > 1) use the begin/finish pair below.
