@@ -2299,33 +2299,42 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
     __syncwarp();
   }
   W.wk = wk0 + nwin;
-  if (!valid) return;
+  // Warp-cooperative stores: the 32 unit blocks (h K + M/h) are staged in the
+  // drained TMA window, then lane t % 32 writes value t = 3 u + f of DOF row d
+  // of unit u. Consecutive units of one row I have consecutive block offsets,
+  // so a direct store instruction covers 256 contiguous bytes (per-lane 72-byte
+  // blocks touched 24 sectors per instruction); the transposed (J,I) blocks keep
+  // each unit's 24-byte row piece on three adjacent lanes. Config 3 gather:
+  // 7.55 vs 7.98 ms.
+  double* st = W.buf[0];
   const double mh = m / h;
-  if (A.upper) {
-    // UPPER storage (common.cuh): entry (d, f) at off + f + d (2 + 3 L) - d (d-1)/2,
-    // the diagonal block keeps f >= d only; no transposed copy
-    const int L = dg & 0xffff;
-    const bool diag = (dg >> 16) != 0;
-    double* out = H + off;
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-#pragma unroll
-      for (int f = 0; f < 3; ++f)
-        if (!diag || f >= d) out[f + d * (2 + 3 * L) - d * (d - 1) / 2] = fma(h, acc[3 * d + f], d == f ? mh : 0.0);
-    return;
-  }
-  const int deg = dg & 0xffff, degT = dg >> 16;
-  double* out = H + 3 * (int64_t)off;  // FULL offsets are stored / 3 (k_unit_meta)
 #pragma unroll
   for (int d = 0; d < 3; ++d)
 #pragma unroll
-    for (int f = 0; f < 3; ++f) h_store(out + 3 * d * deg + f, fma(h, acc[3 * d + f], d == f ? mh : 0.0));
-  if (offT >= 0) {
-    double* o2 = H + 3 * (int64_t)offT;
+    for (int f = 0; f < 3; ++f) st[lane * 9 + 3 * d + f] = fma(h, acc[3 * d + f], d == f ? mh : 0.0);
+  __syncwarp();
 #pragma unroll
-    for (int d = 0; d < 3; ++d)
+  for (int k = 0; k < 3; ++k) {
+    const int t = 32 * k + lane, sl = t / 3, f = t - 3 * (t / 3);
+    const int32_t o = __shfl_sync(0xffffffffu, off, sl), oT = __shfl_sync(0xffffffffu, offT, sl);
+    const int32_t dgl = __shfl_sync(0xffffffffu, dg, sl);
+    const bool vl = u0 + sl < n_units;
+    if (A.upper) {
+      // UPPER storage (common.cuh): entry (d, f) at off + f + d (2 + 3 L) - d (d-1)/2,
+      // the diagonal block keeps f >= d only; no transposed copy
+      const int L = dgl & 0xffff;
+      const bool diag = (dgl >> 16) != 0;
 #pragma unroll
-      for (int f = 0; f < 3; ++f) h_store(o2 + 3 * d * degT + f, fma(h, acc[3 * f + d], d == f ? mh : 0.0));
+      for (int d = 0; d < 3; ++d)
+        if (vl && (!diag || f >= d)) H[o + f + d * (2 + 3 * L) - d * (d - 1) / 2] = st[sl * 9 + 3 * d + f];
+    } else {
+      const int dl = dgl & 0xffff, dT = dgl >> 16;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        if (vl) h_store(H + 3 * (int64_t)o + 3 * d * dl + f, st[sl * 9 + 3 * d + f]);
+        if (vl && oT >= 0) h_store(H + 3 * (int64_t)oT + 3 * d * dT + f, st[sl * 9 + 3 * f + d]);
+      }
+    }
   }
 }
 
@@ -2403,20 +2412,24 @@ __device__ __forceinline__ void gather_units_warp_kvc(int64_t u0, const GatherAr
     __syncwarp();
   }
   W.wk = wk0 + nwin;
-  if (!valid) return;
+  // warp-cooperative stores as in gather_units_warp (18 staged values per unit)
   const double h = A.h, mh = m / h;
-  const int deg = dg & 0xffff, degT = dg >> 16;
-  double* out = H + 3 * (int64_t)off;
+  double* st = W.buf[0];
 #pragma unroll
-  for (int d = 0; d < 3; ++d)
+  for (int r = 0; r < 18; ++r) st[lane * 18 + r] = fma(h, acc[r], (r % 9) % 4 == 0 ? mh : 0.0);
+  __syncwarp();
 #pragma unroll
-    for (int f = 0; f < 3; ++f) h_store(out + 3 * d * deg + f, fma(h, acc[3 * d + f], d == f ? mh : 0.0));
-  if (offT >= 0) {
-    double* o2 = H + 3 * (int64_t)offT;
+  for (int k = 0; k < 3; ++k) {
+    const int t = 32 * k + lane, sl = t / 3, f = t - 3 * (t / 3);
+    const int32_t o = __shfl_sync(0xffffffffu, off, sl), oT = __shfl_sync(0xffffffffu, offT, sl);
+    const int32_t dgl = __shfl_sync(0xffffffffu, dg, sl);
+    const bool vl = u0 + sl < n_units;
+    const int dl = dgl & 0xffff, dT = dgl >> 16;
 #pragma unroll
-    for (int d = 0; d < 3; ++d)
-#pragma unroll
-      for (int f = 0; f < 3; ++f) h_store(o2 + 3 * d * degT + f, fma(h, acc[9 + 3 * d + f], d == f ? mh : 0.0));
+    for (int d = 0; d < 3; ++d) {
+      if (vl) h_store(H + 3 * (int64_t)o + 3 * d * dl + f, st[sl * 18 + 3 * d + f]);
+      if (vl && oT >= 0) h_store(H + 3 * (int64_t)oT + 3 * d * dT + f, st[sl * 18 + 9 + 3 * d + f]);
+    }
   }
 }
 
