@@ -157,6 +157,7 @@ struct Context {
   // affine (min) layout of straight-sided T10 without classes: [n_el][13] =
   // grad_X z_0..3 (barycentric gradients), J0 (SURVEY §8(d) min layout)
   double* aff = nullptr;
+  double* cls_aff = nullptr;      // [n_cls][13] the same per class (straight-sided T10 with classes)
   std::vector<int64_t> cls_rep;   // representative (first) element of each class
   // symmetric H gather units (upper blocks + blocks whose transpose is not owned)
   int64_t n_units = 0;

@@ -1391,6 +1391,161 @@ __global__ void __launch_bounds__(kFW * 32, NQ == 4 ? TLFEA_FW_MINB4 : TLFEA_FW_
   }
 }
 
+
+// ------------------------------------------ T10 SVK force only, affine form
+// Straight-sided T10 (every mesh with the affine min layout, and congruent
+// meshes whose classes are straight-sided): grad N is linear in the
+// barycentric coordinates z, so with the four constant gradients grad z_k
+// (SURVEY §8(d) min layout, P:312-320 with J constant) the element needs no
+// per-point tables:
+//   F(z) = sum_k z_k G_k,  G_k = 4 (x_k (x) grad z_k + sum_{j != k} x_kj (x) grad z_j) - C,
+//   C = sum_i x_i (x) grad z_i   (x_kj: the mid-edge node of edge (k, j); sum z = 1)
+// is the T10 deformation gradient of Eq. F_assembly at any point, and
+// with wP_q = J0 w_q F_q S_q (reading Q5), Q_i = sum_q z_qi wP_q, R = sum_q wP_q:
+//   corner i: f_i = sum_q wP_q grad N_i(z_q) = (4 Q_i - R) grad z_i,
+//   edge (a,b): f = 4 (Q_a grad z_b + Q_b grad z_a)          (Eq. fint_local).
+// The rules' points are permutations, so F_q and Q_i cost a few FMAs each
+// (Keast-5: F_0 = T/4, F_q = T/6 + G_{q-1}/3 with T = sum_k G_k; 4-point:
+// F_q = beta T + (alpha - beta) G_q). One thread per element, all in registers:
+// no shared-memory traffic (the two-phase kernels above are bound by it).
+#ifndef TLFEA_FORCE_AFF
+#define TLFEA_FORCE_AFF 1
+#endif
+#ifndef TLFEA_FA_MINB
+#define TLFEA_FA_MINB 3  // config 5: 0.263 ms at 3 CTAs/SM (166 registers) vs 0.283 at 4 (128, spills), 0.320 at 2
+#endif
+constexpr int kFABlock = 128;
+template <int NQ, bool CLS>
+__global__ void __launch_bounds__(kFABlock, TLFEA_FA_MINB) k_force_t10_aff(ElArgs A, int64_t e_begin,
+                                                                           const double* __restrict__ cls_aff) {
+  extern __shared__ double s_aff[];  // CLS: [n_cls][13]
+  if (CLS) {
+    for (int t = threadIdx.x; t < A.n_cls * 13; t += blockDim.x) s_aff[t] = cls_aff[t];
+    __syncthreads();
+  }
+  const int64_t e = e_begin + (int64_t)blockIdx.x * kFABlock + threadIdx.x;
+  if (e >= A.n_el) return;
+  const double* af = CLS ? s_aff + 13 * A.cls[e] : A.aff + 13 * e;
+  double gz[4][3];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) gz[i][k] = af[3 * i + k];
+  const double J0 = af[12];
+  int32_t nd[10];
+#pragma unroll
+  for (int a = 0; a < 10; ++a) nd[a] = A.conn[e * 10 + a];
+  double x[10][3];
+#pragma unroll
+  for (int a = 0; a < 10; ++a)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) x[a][i] = A.x[3 * (int64_t)nd[a] + i];
+  // edge node of (k, j) in the local order of reading Q2: 4 (0,1) 5 (1,2) 6 (2,0) 7 (0,3) 8 (1,3) 9 (2,3)
+  constexpr int EDGE[4][4] = {{-1, 4, 6, 7}, {4, -1, 5, 8}, {6, 5, -1, 9}, {7, 8, 9, -1}};
+  double C[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      C[3 * r + c] = x[0][r] * gz[0][c] + x[1][r] * gz[1][c] + x[2][r] * gz[2][c] + x[3][r] * gz[3][c];
+  double G[4][9], T[9];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double h = x[k][r] * gz[k][c];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j != k) h = fma(x[EDGE[k][j]][r], gz[j][c], h);
+        G[k][3 * r + c] = fma(4.0, h, -C[3 * r + c]);
+      }
+#pragma unroll
+  for (int r = 0; r < 9; ++r) T[r] = (G[0][r] + G[1][r]) + (G[2][r] + G[3][r]);
+  const double lam = A.mat.lam, mu = A.mat.mu;
+  // wP at one point: J0 w F S
+  auto wP_at = [&](const double F[9], double jw, double out[9]) {
+    double S[6];
+    svk_S(F, lam, mu, S);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int J = 0; J < 3; ++J)
+        out[3 * i + J] = jw * (F[3 * i] * sget(S, 0, J) + F[3 * i + 1] * sget(S, 1, J) + F[3 * i + 2] * sget(S, 2, J));
+  };
+  double P4[4][9], base[9], R[9];  // per-permutation-point wP, and the parts shared by all Q_i
+  double ca, cr;                   // Q_i = base + ca P4[i];  4 Q_i - R = 4 base - R + 4 ca P4[i]
+  if constexpr (NQ == 5) {  // Keast (reading Q1): centroid w = -2/15; z_{q-1} = 1/2, others 1/6, w = 3/40
+    double F[9], P0[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) F[r] = 0.25 * T[r];
+    wP_at(F, J0 * (-2.0 / 15.0), P0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int r = 0; r < 9; ++r) F[r] = fma(1.0 / 3.0, G[k][r], T[r] * (1.0 / 6.0));
+      wP_at(F, J0 * (3.0 / 40.0), P4[k]);
+    }
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      const double U = (P4[0][r] + P4[1][r]) + (P4[2][r] + P4[3][r]);
+      base[r] = fma(0.25, P0[r], U * (1.0 / 6.0));
+      R[r] = P0[r] + U;
+    }
+    ca = 1.0 / 3.0;
+  } else {  // 4-point degree 2: z_q = alpha at q, beta elsewhere, w = 1/24
+    const double r5 = 2.2360679774997896964;
+    const double alpha = 0.25 + 0.15 * r5, beta = 0.25 - 0.05 * r5;
+    double F[9];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int r = 0; r < 9; ++r) F[r] = fma(alpha - beta, G[k][r], beta * T[r]);
+      wP_at(F, J0 * (1.0 / 24.0), P4[k]);
+    }
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      R[r] = (P4[0][r] + P4[1][r]) + (P4[2][r] + P4[3][r]);
+      base[r] = beta * R[r];
+    }
+    ca = alpha - beta;
+  }
+  (void)cr;
+  double f[10][3];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)  // corners: (4 Q_i - R) grad z_i
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) s = fma(fma(4.0, fma(ca, P4[i][3 * r + c], base[3 * r + c]), -R[3 * r + c]), gz[i][c], s);
+      f[i][r] = s;
+    }
+  constexpr int EA[6] = {0, 1, 2, 0, 1, 2}, EB[6] = {1, 2, 0, 3, 3, 3};
+#pragma unroll
+  for (int m = 0; m < 6; ++m)  // edges: 4 (Q_a grad z_b + Q_b grad z_a)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double qa = fma(ca, P4[EA[m]][3 * r + c], base[3 * r + c]);
+        const double qb = fma(ca, P4[EB[m]][3 * r + c], base[3 * r + c]);
+        s = fma(qa, gz[EB[m]][c], fma(qb, gz[EA[m]][c], s));
+      }
+      f[4 + m][r] = 4.0 * s;
+    }
+#pragma unroll
+  for (int a = 0; a < 10; ++a) {
+    const int64_t fp = A.fdest ? (int64_t)A.fdest[e * 10 + a] : e * 10 + a;
+    double* fo = A.fscr + 3 * fp;
+    fo[0] = f[a][0];
+    fo[1] = f[a][1];
+    fo[2] = f[a][2];
+  }
+}
+
 #ifndef TLFEA_ANCF_NPASS
 #define TLFEA_ANCF_NPASS 1  // block passes (each re-runs phase A per chunk)
 #endif
@@ -2353,7 +2508,11 @@ __device__ __forceinline__ void g3_init(double (*s_buf)[2][kG3Buf], uint64_t (*s
   W.wk = 0;
 }
 
+#ifdef TLFEA_G3_MINB
+__global__ void __launch_bounds__(kG3Warps * 32, TLFEA_G3_MINB) k_gather_units_v3(GatherArgs A) {
+#else
 __global__ void __launch_bounds__(kG3Warps * 32) k_gather_units_v3(GatherArgs A) {
+#endif
   __shared__ __align__(16) double s_buf[kG3Warps][2][kG3Buf];
   __shared__ __align__(8) uint64_t s_bar[kG3Warps][2];
   G3Warp W;
@@ -2472,6 +2631,21 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
   using G = Geo<ELEM>;
   const int64_t per_cta = (int64_t)kWarps * G::EPW;
   if (e_end <= e_begin) return TLFEA_OK;
+  if constexpr (ELEM == 0 && MODEL == 0 && !KV && !TAN && TLFEA_FORCE_AFF) {
+    if ((c->n_cls > 0 && c->cls_aff) || (c->n_cls == 0 && c->aff)) {
+      ElArgs A = el_args(c, x, v);
+      A.n_el = e_end;
+      const unsigned grid = (unsigned)((e_end - e_begin + kFABlock - 1) / kFABlock);
+      if (c->n_cls > 0) {
+        const size_t smem = sizeof(double) * c->n_cls * 13;
+        k_force_t10_aff<NQ, true><<<grid, kFABlock, smem, s>>>(A, e_begin, c->cls_aff);
+      } else {
+        k_force_t10_aff<NQ, false><<<grid, kFABlock, 0, s>>>(A, e_begin, nullptr);
+      }
+      TL_CHECK_LAUNCH();
+      return TLFEA_OK;
+    }
+  }
   if constexpr (ELEM == 0 && MODEL == 0 && !KV && !TAN && TLFEA_FORCE_WIDE) {
     if (c->n_cls > 0) {
       const int64_t per = (int64_t)kFW * (32 / NQ);

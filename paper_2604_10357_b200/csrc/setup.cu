@@ -193,11 +193,13 @@ __global__ void k_affine_check(int64_t n_el, const int32_t* __restrict__ conn,
 // Affine (min) layout of a straight-sided T10 (P:312-320 with J constant):
 // J = [X1 - X0, X2 - X0, X3 - X0] (columns dX/dxi_c), grad_X z_{c+1} = row c
 // of J^-1, grad_X z_0 = -(sum of the others), J0 = det J.
+// idx (optional): output row r is element idx[r] (the per-class rows of a
+// mesh with geometry classes), else element r.
 __global__ void k_affine_layout(int64_t n_el, const int32_t* __restrict__ conn, const double* __restrict__ X,
-                                double* __restrict__ aff) {
+                                double* __restrict__ aff, const int64_t* __restrict__ idx = nullptr) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n_el) return;
-  const int32_t* c = conn + e * 10;
+  const int32_t* c = conn + (idx ? idx[e] : e) * 10;
   double J[3][3];
   for (int k = 0; k < 3; ++k)
     for (int m = 0; m < 3; ++m) J[k][m] = X[3 * (int64_t)c[m + 1] + k] - X[3 * (int64_t)c[0] + k];
@@ -1232,6 +1234,17 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
     c->affine = na ? 0 : 1;
   }
   if (c->force_tables != 2) TL_TRY(build_geometry_classes(c, dX));
+  // straight-sided T10 with geometry classes: the affine layout of each class
+  // representative (the force-only kernel evaluates the T10 basis from it)
+  if (c->element == TLFEA_T10 && c->affine && c->n_cls > 0) {
+    const int64_t nr = (int64_t)c->cls_rep.size();
+    TmpArr<int64_t> drep;
+    TL_TRY(drep.get(nr));
+    TL_CUDA(cudaMemcpy(drep.p, c->cls_rep.data(), sizeof(int64_t) * nr, cudaMemcpyHostToDevice));
+    TL_TRY(c->alloc(&c->cls_aff, (size_t)nr * 13));
+    k_affine_layout<<<grid_for(nr, 128), 128>>>(nr, c->conn, dX, c->cls_aff, drep.p);
+    TL_CHECK_LAUNCH();
+  }
   // no classes: straight-sided T10 elements take the affine (min) layout
   if (c->element == TLFEA_T10 && c->affine && c->n_cls == 0 && c->force_tables != 1 && c->n_el > 0) {
     TL_TRY(c->alloc(&c->aff, (size_t)c->n_el * 13));
