@@ -347,6 +347,10 @@ def run_ours(args):
         scount, rcount = ctx.exchange_sizes()
         sbuf = torch.empty(max(1, int(scount.sum())), dtype=torch.float64, device=dev)
         rbuf = torch.empty(max(1, int(rcount.sum())), dtype=torch.float64, device=dev)
+        if args.transport == "lib":
+            uid = [T.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ctx.nccl_attach(uid[0])
         soff = np.concatenate([[0], np.cumsum(scount)])
         roff = np.concatenate([[0], np.cumsum(rcount)])
 
@@ -361,9 +365,13 @@ def run_ours(args):
             # boundary elements + pack; the exchange (NCCL stream) overlaps the
             # interior elements; finish adds the received partials
             ctx.eval_begin(xd, vd, cfg.h, H, sbuf, force_only=force_only)
-            works = tdist.exchange_start(sbuf, rbuf, scount, rcount, host_staging=backend == "gloo")
-            ctx.eval_interior(xd, vd, cfg.h, H, force_only=force_only)
-            tdist.exchange_wait(works)
+            if args.transport == "lib":   # the library's NCCL transport (tlfea_eval_exchange)
+                ctx.eval_exchange(sbuf, rbuf)
+                ctx.eval_interior(xd, vd, cfg.h, H, force_only=force_only)
+            else:
+                works = tdist.exchange_start(sbuf, rbuf, scount, rcount, host_staging=backend == "gloo")
+                ctx.eval_interior(xd, vd, cfg.h, H, force_only=force_only)
+                tdist.exchange_wait(works)
             ctx.eval_finish(rbuf, vd, vnd, fed, cfg.h, None if force_only else g, H, f, force_only=force_only)
 
     for _ in range(args.warmup):
@@ -474,7 +482,7 @@ def run_ours(args):
                        "path": "force_only" if force_only else "force+tangent+residual (tlfea_eval)",
                        "hessian_storage": args.hessian,
                        "tangent": "consistent_kv (NEXT-4)" if info.get("kv_consistent_tangent") else "elastic (Q8)",
-                       "parallelism": f"element-partition x{world}" if world > 1 else "1 GPU",
+                       "parallelism": f"element-partition x{world} ({args.transport} transport)" if world > 1 else "1 GPU",
                        "geometry_classes": info["n_geometry_classes"],
                        "reference_layout": ["classes", "per-(e,q) tables", "affine min layout"][info["reference_layout"]],
                        "l2": "inputs/outputs larger than L2 (no flush needed)",
@@ -630,6 +638,9 @@ def main():
     ap.add_argument("--mesh", choices=["kuhn", "straight"], default="kuhn",
                     help="straight: the T10 mesh with randomly displaced corners (straight-sided, non-congruent: "
                          "the affine min layout instead of geometry classes)")
+    ap.add_argument("--transport", choices=["torch", "lib"], default="torch",
+                    help="N>1 exchange: torch.distributed P2P (NCCL) or the library's own NCCL transport "
+                         "(tlfea_nccl_attach / tlfea_eval_exchange)")
     ap.add_argument("--kv-consistent", action="store_true",
                     help="H = the consistent Kelvin-Voigt tangent dg/dv (NEXT-4; configs with damping, e.g. 2)")
     ap.add_argument("--ladder", action="store_true",

@@ -61,7 +61,8 @@ typedef enum {
   TLFEA_E_OVERFLOW = 4,         /* an index exceeds the int32 build limits    */
   TLFEA_E_OOM = 5,              /* device allocation failed                   */
   TLFEA_E_CUDA = 6,             /* CUDA runtime error / no device             */
-  TLFEA_E_UNSUPPORTED = 7       /* valid request this build does not provide  */
+  TLFEA_E_UNSUPPORTED = 7,      /* valid request this build does not provide  */
+  TLFEA_E_NCCL = 8              /* NCCL unavailable or an NCCL call failed    */
 } tlfea_status;
 
 typedef enum { TLFEA_T10 = 0, TLFEA_ANCF3443 = 1, TLFEA_ANCF3243 = 2 } tlfea_element;
@@ -442,6 +443,29 @@ tlfea_status tlfea_eval_finish(tlfea_ctx ctx, const double* recv_buf,
                                const double* f_ext, double h,
                                int32_t force_only, double* g_out,
                                double* H_out, double* f_int_out, void* stream);
+
+/* The library's own NCCL transport of the exchange (SURVEY §8(b) / §8(e)
+ * steps 2-4), an alternative to moving send_buf / recv_buf yourself.
+ * libnccl.so.2 is loaded at run time (TLFEA_E_NCCL if it cannot be).
+ *  tlfea_nccl_get_unique_id: id_out HOST [TLFEA_NCCL_ID_BYTES], an ncclUniqueId
+ *    made on one rank (rank 0) and handed to every rank out of band (e.g. a
+ *    torch.distributed broadcast of the bytes).
+ *  tlfea_nccl_attach: every rank of the partition, with the same id, creates
+ *    the context's communicator (ncclCommInitRank over options.nranks,
+ *    options.rank; collective: all ranks must call it), a communication stream
+ *    and two events. Destroyed with the context.
+ *  tlfea_eval_exchange: between tlfea_eval_begin and tlfea_eval_interior on
+ *    the same stream: sends send_buf's per-peer segments and receives
+ *    recv_buf's (DEVICE, tlfea_exchange_sizes layout) as one NCCL group of
+ *    ncclSend / ncclRecv on the communication stream, which an event orders
+ *    after begin's pack; tlfea_eval_interior then overlaps the transfer, and
+ *    tlfea_eval_finish makes the stream wait for it (events only, no host
+ *    synchronization). A single-rank context without a communicator: no-op. */
+#define TLFEA_NCCL_ID_BYTES 128
+tlfea_status tlfea_nccl_get_unique_id(void* id_out);
+tlfea_status tlfea_nccl_attach(tlfea_ctx ctx, const void* id);
+tlfea_status tlfea_eval_exchange(tlfea_ctx ctx, const double* send_buf,
+                                 double* recv_buf, void* stream);
 
 /* Global ids of the context's local elements, in its local order (the order
  * of tlfea_slot_map / tlfea_export_precompute rows; partitioned contexts put

@@ -29,7 +29,7 @@ T10, ANCF3443 = 0, 1
 Q_T10_4PT, Q_T10_KEAST5, Q_GL_4x4x3 = 0, 1, 2
 SVK, MOONEY_RIVLIN = 0, 1
 STATUS = {0: "OK", 1: "INVALID", 2: "INVERTED_ELEMENT", 3: "INVERTED_STATE", 4: "OVERFLOW", 5: "OOM",
-          6: "CUDA", 7: "UNSUPPORTED"}
+          6: "CUDA", 7: "UNSUPPORTED", 8: "NCCL"}
 
 
 class TlfeaError(RuntimeError):
@@ -107,6 +107,9 @@ _SIGS = {
     "tlfea_eval_begin": [_vp, _vp, _vp, _i32, _d, _vp, _vp, _vp],
     "tlfea_eval_interior": [_vp, _vp, _vp, _i32, _d, _vp, _vp],
     "tlfea_eval_finish": [_vp, _vp, _vp, _vp, _vp, _d, _i32, _vp, _vp, _vp, _vp],
+    "tlfea_nccl_get_unique_id": [_vp],
+    "tlfea_nccl_attach": [_vp, _vp],
+    "tlfea_eval_exchange": [_vp, _vp, _vp, _vp],
     "tlfea_local_elements": [_vp, _vp],
     "tlfea_plan_partition": [_i64, _i32, _vp, _i64, _vp, _i32, _i32, _vp, C.POINTER(_i64), _vp, _vp,
                              C.POINTER(_i64), _vp, _vp],
@@ -206,6 +209,14 @@ def tlfea_plan_partition(conn_coef: np.ndarray, n_coef: int, elem_part, nranks: 
     _check(L.tlfea_plan_partition(n_el, nen, _ptr(conn_coef), n_coef, _ptr(part), nranks, rank, _ptr(owner),
                                   C.byref(nb), _ptr(sb), _ptr(sbp), C.byref(nn), _ptr(sn), _ptr(snp)))
     return owner, sb, sbp, sn, snp
+
+
+def nccl_unique_id() -> bytes:
+    """tlfea_nccl_get_unique_id: the 128-byte NCCL unique id (made on one rank,
+    handed to every rank of the partition out of band)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().tlfea_nccl_get_unique_id(buf))
+    return buf.raw
 
 
 class Context:
@@ -476,6 +487,21 @@ class Context:
         n = self.n_dof
         _check(lib().tlfea_eval_interior(self.handle, self._d(x, n, "x"), self._d(v, n, "v"), int(force_only),
                                          float(h), self._d(H, 0 if force_only else self.nnz, "H"), _stream(stream)))
+
+    def nccl_attach(self, uid: bytes):
+        """tlfea_nccl_attach (collective over the partition's ranks): the
+        context's own NCCL communicator for eval_exchange."""
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id: 128 bytes")
+        _check(lib().tlfea_nccl_attach(self.handle, C.create_string_buffer(uid, 128)))
+
+    def eval_exchange(self, send_buf, recv_buf, stream=None):
+        """tlfea_eval_exchange: the library's NCCL transfer of the packed
+        partials (between eval_begin and eval_interior on the same stream;
+        eval_finish waits for it)."""
+        s, r = self.exchange_sizes()
+        _check(lib().tlfea_eval_exchange(self.handle, self._d(send_buf, int(s.sum()), "send_buf"),
+                                         self._d(recv_buf, int(r.sum()), "recv_buf"), _stream(stream)))
 
     def local_elements(self):
         """Global ids of the local elements in the context's local order."""

@@ -493,6 +493,7 @@ tlfea_status tlfea_eval_finish(tlfea_ctx ctx, const double* recv_buf, const doub
   if (c.interior_pending) return fail(TLFEA_E_INVALID, "tlfea_eval_finish: call tlfea_eval_interior first");
   TRY(use_device(c));
   const cudaStream_t s = as_stream(stream);
+  TRY(nccl_wait(&c, s));  // a library exchange (tlfea_eval_exchange) in flight
   if (c.nranks > 1) {
     if (!recv_buf) return fail(TLFEA_E_INVALID, "tlfea_eval_finish: NULL recv_buf");
     TIMED(3, launch_unpack_recv(&c, recv_buf, h, H_out, force_only != 0, s));
@@ -504,6 +505,34 @@ tlfea_status tlfea_eval_finish(tlfea_ctx ctx, const double* recv_buf, const doub
   if (f_int_out)
     TL_CUDA(cudaMemcpyAsync(f_int_out, c.fpart, sizeof(double) * 3 * c.n_own, cudaMemcpyDeviceToDevice, s));
   return TLFEA_OK;
+}
+
+tlfea_status tlfea_nccl_get_unique_id(void* id_out) {
+  if (!id_out) return fail(TLFEA_E_INVALID, "NULL id_out");
+  return nccl_get_unique_id(id_out);
+}
+
+tlfea_status tlfea_nccl_attach(tlfea_ctx ctx, const void* id) {
+  CTX_OR_FAIL(ctx);
+  if (!id) return fail(TLFEA_E_INVALID, "NULL NCCL unique id");
+  Context& c = ctx->c;
+  TRY(use_device(c));
+  return nccl_attach(&c, id);
+}
+
+tlfea_status tlfea_eval_exchange(tlfea_ctx ctx, const double* send_buf, double* recv_buf, void* stream) {
+  CTX_OR_FAIL(ctx);
+  Context& c = ctx->c;
+  if (!c.interior_pending) return fail(TLFEA_E_INVALID, "tlfea_eval_exchange: call tlfea_eval_begin first");
+  int64_t ns = 0, nr = 0;
+  for (int p = 0; p < c.nranks && c.nranks > 1; ++p) {
+    ns += c.send_counts[p];
+    nr += c.recv_counts[p];
+  }
+  if ((ns > 0 && !send_buf) || (nr > 0 && !recv_buf)) return fail(TLFEA_E_INVALID, "tlfea_eval_exchange: NULL buffer");
+  TRY(use_device(c));
+  if (c.nranks == 1 && !c.nccl_comm) return TLFEA_OK;  // nothing to move
+  return nccl_exchange(&c, send_buf, recv_buf, as_stream(stream));
 }
 
 tlfea_status tlfea_local_elements(tlfea_ctx ctx, int64_t* out_host) {

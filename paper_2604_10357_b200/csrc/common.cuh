@@ -180,6 +180,11 @@ struct Context {
 
   // partition exchange (nranks > 1)
   std::vector<int64_t> send_counts, recv_counts;     // fp64 values per peer
+  // the library's NCCL transport (tlfea_nccl_attach / tlfea_eval_exchange, nccl.cu)
+  void* nccl_comm = nullptr;                 // ncclComm_t
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_packed = nullptr, ev_exchanged = nullptr;
+  bool exchange_pending = false;
   int64_t n_send_blk = 0, n_recv_blk = 0, n_send_node = 0, n_recv_node = 0;
   int32_t* sblk_ptr = nullptr;   // [n_send_blk+1] contribution lists of sent blocks
   uint32_t* sblk_ent = nullptr;
@@ -270,6 +275,11 @@ tlfea_status launch_constraint_terms(Context* c, const double* q, const double* 
 tlfea_status launch_dual_update(Context* c, const double* q, double rho, double* lam, double* c_out,
                                 cudaStream_t st);
 tlfea_status launch_pack_send(Context* c, double* send, bool force_only, cudaStream_t s);
+tlfea_status nccl_get_unique_id(void* id_out);
+tlfea_status nccl_attach(Context* c, const void* id);
+void nccl_detach(Context* c);
+tlfea_status nccl_exchange(Context* c, const double* send_buf, double* recv_buf, cudaStream_t s);
+tlfea_status nccl_wait(Context* c, cudaStream_t s);
 tlfea_status launch_unpack_recv(Context* c, const double* recv, double h, double* H,
                                 bool force_only, cudaStream_t s);
 tlfea_status launch_test_constitutive(const MatDev& m, int64_t n, const double* F,

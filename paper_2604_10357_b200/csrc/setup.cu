@@ -46,6 +46,7 @@ const char* last_error() { return g_err.c_str(); }
 int64_t launch_count() { return g_launches.load(); }
 
 Context::~Context() {
+  nccl_detach(this);
   for (auto& t : timed) {
     cudaEventDestroy(t.start);
     cudaEventDestroy(t.stop);

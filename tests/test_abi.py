@@ -72,3 +72,12 @@ def test_plan_partition_host_only(T):
     # rank 0 sends nothing (it owns every node it touches)
     _, sb0, _, sn0, _ = T.tlfea_plan_partition(mesh.conn, mesh.n_coef, part, 2, 0)
     assert len(sb0) == 0 and len(sn0) == 0
+
+
+def test_nccl_unique_id_host_only(T):
+    """tlfea_nccl_get_unique_id loads libnccl.so.2 at run time (no link-time
+    NCCL dependency) and returns a 128-byte ncclUniqueId without a GPU."""
+    uid = T.nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128 and any(uid)
+    out = subprocess.run(["ldd", T.LIB_PATH], capture_output=True, text=True).stdout
+    assert "libnccl" not in out

@@ -4,7 +4,9 @@ partitioned context on GPU 0 (the ranks share it), runs
 eval_begin -> dist.exchange_start -> eval_interior -> exchange_wait ->
 eval_finish with the gloo transport (host-staged: NCCL refuses two ranks on one
 device), and rank 0 checks the gathered owned rows against the oracle
-(pattern bit-exact, values <= 1e-11). Prints one JSON line on rank 0."""
+(pattern bit-exact, values <= 1e-11). Prints one JSON line on rank 0.
+--transport lib: the library's own NCCL transport instead (tlfea_nccl_attach +
+tlfea_eval_exchange; rank r on GPU r, so it needs as many GPUs as ranks)."""
 import json
 import os
 import sys
@@ -21,12 +23,18 @@ from paper_2604_10357_b200 import dist as tdist  # noqa: E402
 
 
 def main():
+    lib_transport = "--transport" in sys.argv and sys.argv[sys.argv.index("--transport") + 1] == "lib"
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
-    torch.cuda.set_device(0)
+    dev = rank if lib_transport else 0
+    torch.cuda.set_device(dev)
     mesh, mat, rule, h = synth.kuhn_t10_box(6, 3, 2, 1.2, 0.6, 0.4), dict(synth.SVK_PAPER), 1, 1e-3
     x, v, vn, fext = synth.t10_state(mesh, with_fext=True)
-    ctx = T.Context.from_mesh(mesh, mat, rule, rank=rank, nranks=world)
+    ctx = T.Context.from_mesh(mesh, mat, rule, rank=rank, nranks=world, device=dev)
+    if lib_transport:
+        uid = [T.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.nccl_attach(uid[0])
     d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     xd, vd, vnd, fed = d(x), d(v), d(vn), d(fext)
     sc, rc = ctx.exchange_sizes()
@@ -34,9 +42,13 @@ def main():
     rbuf = torch.zeros(max(1, int(rc.sum())), dtype=torch.float64, device="cuda")
     g, H, f = ctx.empty_outputs()
     ctx.eval_begin(xd, vd, h, H, sbuf)
-    works = tdist.exchange_start(sbuf, rbuf, sc, rc, host_staging=True)
-    ctx.eval_interior(xd, vd, h, H)
-    tdist.exchange_wait(works)
+    if lib_transport:
+        ctx.eval_exchange(sbuf, rbuf)   # NCCL on the context's stream; finish waits for it
+        ctx.eval_interior(xd, vd, h, H)
+    else:
+        works = tdist.exchange_start(sbuf, rbuf, sc, rc, host_staging=True)
+        ctx.eval_interior(xd, vd, h, H)
+        tdist.exchange_wait(works)
     ctx.eval_finish(rbuf, vd, vnd, fed, h, g, H, f)
     torch.cuda.synchronize()
     rowptr, cols, _, _, owned = [t.cpu().numpy().astype(np.int64) for t in ctx.export_pattern()]
@@ -59,7 +71,7 @@ def main():
                     Hh[b0:b1] = r["H"][a0:a1]
         rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
         owned_all = np.sort(np.concatenate([r["owned"] for r in allr]))
-        print(json.dumps({"world": world, "pattern_ok": pattern_ok,
+        print(json.dumps({"world": world, "transport": "lib" if lib_transport else "gloo", "pattern_ok": pattern_ok,
                           "rows_partition": bool(np.array_equal(owned_all, np.arange(mesh.n_coef))),
                           "rel_g": rel(G, g0), "rel_H": rel(Hh, H0), "rel_f": rel(F, f0)}), flush=True)
     dist.barrier()
