@@ -255,7 +255,7 @@ tlfea_status tlfea_eval(tlfea_ctx ctx, const double* x, const double* v, const d
   TRY(use_device(c));
   const cudaStream_t s = as_stream(stream);
   c.last_stream = s;
-  c.kvc_inv_h = 1.0 / h;
+  c.eval_inv_h = 1.0 / h;
   TIMED(0, launch_element_kernel(&c, x, v, true, s));
   TIMED(1, launch_gather_H(&c, h, H_out, s));
   TIMED(2, launch_gather_f(&c, v, v_n, f_ext, h, g_out, f_int_out, false, s));
@@ -322,10 +322,30 @@ tlfea_status tlfea_adamw_iteration(tlfea_ctx ctx, const double* q_n, const doubl
   const cudaStream_t s = as_stream(stream);
   c.last_stream = s;
   // (i) velocity update and step map
-  TIMED(2, launch_adamw_update(&c, l, *params, g, m, s_mom, v, q_n, h, q_out, s));
+  const bool inr = !f_int_out && force_inertia_capable(&c);
+  if (inr && !c.dvscr) TRY(c.alloc(&c.dvscr, (size_t)3 * c.n_coef));
+  TIMED(2, launch_adamw_update(&c, l, *params, g, m, s_mom, v, q_n, h, q_out, s, inr ? v_n : nullptr,
+                               inr ? c.dvscr : nullptr));
   // (iii)-(iv) Stage 1 + Stage 2 at q, (vi) gradient
-  TIMED(0, launch_element_kernel(&c, q_out, v, false, s));
-  TIMED(2, launch_gather_f(&c, v, v_n, f_ext, h, g, f_int_out, false, s));
+  if (inr) {
+    // straight-sided T10 SVK with classes: the element kernel adds each element's
+    // inertia m_e (v - v_n)_e / h to its nodal forces (v - v_n written by the
+    // update), so the gradient is the force-scratch sum minus f_ext, f_ff (no
+    // mass-row SpMV; f_int is not formed)
+    c.inr = true;
+    c.eval_inv_h = 1.0 / h;
+    tlfea_status st;
+    {
+      Timed t__(c, 0, s);
+      st = launch_element_kernel(&c, q_out, c.dvscr, false, s);
+    }
+    c.inr = false;
+    TRY(st);
+    TIMED(2, launch_gradient_inertia(&c, f_ext, g, s));
+  } else {
+    TIMED(0, launch_element_kernel(&c, q_out, v, false, s));
+    TIMED(2, launch_gather_f(&c, v, v_n, f_ext, h, g, f_int_out, false, s));
+  }
   // (v) constraint residual and its gradient term
   TIMED(2, launch_constraint_terms(&c, q_out, lambda, rho, h, g, nullptr, s));
   // device ||g||, ||v|| for the inner stopping test
@@ -454,7 +474,7 @@ tlfea_status tlfea_eval_begin(tlfea_ctx ctx, const double* x, const double* v, i
   TRY(use_device(c));
   const cudaStream_t s = as_stream(stream);
   c.last_stream = s;
-  c.kvc_inv_h = 1.0 / h;
+  c.eval_inv_h = 1.0 / h;
   // the boundary elements (local [0, n_el_bnd)) and the send buffer
   TIMED(0, launch_element_kernel(&c, x, v, !force_only, s, 0, c.nranks > 1 ? c.n_el_bnd : c.n_el));
   if (c.nranks > 1) {

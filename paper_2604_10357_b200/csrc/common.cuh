@@ -123,10 +123,14 @@ struct Context {
   // consistent Kelvin-Voigt tangent (options.kv_consistent_tangent with damping,
   // NEXT-4): each gather-sorted scratch slot holds 18 values, the unit's (I,J)
   // and (J,I) contributions in their own orientation (non-symmetric blocks);
-  // kvc_inv_h = 1/h of the evaluation in flight (the element kernel scales the
+  // eval_inv_h = 1/h of the evaluation in flight (the element kernel scales the
   // df/dv part by 1/h so the gather's h * acc + M/h gives h df/dx + df/dv).
   int kvc = 0;
-  double kvc_inv_h = 0.0;
+  double eval_inv_h = 0.0;
+  // element-level inertia request of the AdamW gradient (launch_element_kernel,
+  // force only, T10 SVK affine kernel with classes; v then holds v - v_n)
+  bool inr = false;
+  double* dvscr = nullptr;        // [n_dof] v - v_n of the AdamW iteration (lazily allocated)
   int64_t nnz_H = 0;           // values of H as stored
   int32_t* ubase = nullptr;    // [n_own + 1] UPPER offsets of coefficient rows
 
@@ -157,7 +161,8 @@ struct Context {
   // affine (min) layout of straight-sided T10 without classes: [n_el][13] =
   // grad_X z_0..3 (barycentric gradients), J0 (SURVEY §8(d) min layout)
   double* aff = nullptr;
-  double* cls_aff = nullptr;      // [n_cls][13] the same per class (straight-sided T10 with classes)
+  double* cls_aff = nullptr;
+  double* cls_mass = nullptr;     // [n_cls][nen][nen] element mass per class (single rank, classes)      // [n_cls][13] the same per class (straight-sided T10 with classes)
   std::vector<int64_t> cls_rep;   // representative (first) element of each class
   // symmetric H gather units (upper blocks + blocks whose transpose is not owned)
   int64_t n_units = 0;
@@ -267,7 +272,8 @@ tlfea_status launch_force_from_stress(Context* c, const double* P, cudaStream_t 
 tlfea_status launch_residual(Context* c, const double* fint, const double* v, const double* vn,
                              const double* fext, double h, double* g, cudaStream_t s);
 tlfea_status launch_adamw_update(Context* c, int l, const tlfea_adamw_params& p, const double* g, double* m,
-                                 double* s, double* v, const double* q_n, double h, double* q, cudaStream_t st);
+                                 double* s, double* v, const double* q_n, double h, double* q, cudaStream_t st,
+                                 const double* vn = nullptr, double* dv = nullptr);
 tlfea_status launch_norms2(Context* c, const double* a, const double* b, double* out, cudaStream_t st);
 tlfea_status launch_constraint_residual(Context* c, const double* q, double* c_out, cudaStream_t st);
 tlfea_status launch_constraint_terms(Context* c, const double* q, const double* lam, double rho, double h,
@@ -275,6 +281,8 @@ tlfea_status launch_constraint_terms(Context* c, const double* q, const double* 
 tlfea_status launch_dual_update(Context* c, const double* q, double rho, double* lam, double* c_out,
                                 cudaStream_t st);
 tlfea_status launch_pack_send(Context* c, double* send, bool force_only, cudaStream_t s);
+tlfea_status launch_gradient_inertia(Context* c, const double* fext, double* g, cudaStream_t s);
+bool force_inertia_capable(const Context* c);
 tlfea_status nccl_get_unique_id(void* id_out);
 tlfea_status nccl_attach(Context* c, const void* id);
 void nccl_detach(Context* c);

@@ -131,6 +131,8 @@ struct ElArgs {
   const int32_t* fdest;
   unsigned long long* err;
   double inv_h;  // consistent KV tangent only: 1/h of the evaluation (k_element_kvc)
+  // element-level inertia (k_force_t10_aff<.., INR>, v = v - v_n): f_a += (1/h) sum_b m_ab (v - v_n)_b
+  const double* cls_mass;
 };
 
 __device__ __forceinline__ void pf_cp4(void* smem, const void* gmem) {
@@ -1415,12 +1417,18 @@ __global__ void __launch_bounds__(kFW * 32, NQ == 4 ? TLFEA_FW_MINB4 : TLFEA_FW_
 #define TLFEA_FA_MINB 3  // config 5: 0.263 ms at 3 CTAs/SM (166 registers) vs 0.283 at 4 (128, spills), 0.320 at 2
 #endif
 constexpr int kFABlock = 128;
-template <int NQ, bool CLS>
+// INR (the AdamW gradient, classes only): each element also adds its inertia
+// (1/h) sum_b m_ab (v - v_n)_b (Eq. residual P:101-113 element by element, the
+// class element mass of setup) to its nodal forces, so the gradient gather
+// sums the force scratch without the mass-row SpMV.
+template <int NQ, bool CLS, bool INR = false>
 __global__ void __launch_bounds__(kFABlock, TLFEA_FA_MINB) k_force_t10_aff(ElArgs A, int64_t e_begin,
                                                                            const double* __restrict__ cls_aff) {
-  extern __shared__ double s_aff[];  // CLS: [n_cls][13]
+  extern __shared__ double s_aff[];  // CLS: [n_cls][13] (INR: then [n_cls][100] element masses)
   if (CLS) {
     for (int t = threadIdx.x; t < A.n_cls * 13; t += blockDim.x) s_aff[t] = cls_aff[t];
+    if (INR)
+      for (int t = threadIdx.x; t < A.n_cls * 100; t += blockDim.x) s_aff[A.n_cls * 13 + t] = A.cls_mass[t];
     __syncthreads();
   }
   const int64_t e = e_begin + (int64_t)blockIdx.x * kFABlock + threadIdx.x;
@@ -1536,6 +1544,26 @@ __global__ void __launch_bounds__(kFABlock, TLFEA_FA_MINB) k_force_t10_aff(ElArg
       }
       f[4 + m][r] = 4.0 * s;
     }
+  if constexpr (INR) {
+    const double* me = s_aff + A.n_cls * 13 + 100 * A.cls[e];
+    double dv[10][3];
+#pragma unroll
+    for (int b = 0; b < 10; ++b)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) dv[b][i] = A.v[3 * (int64_t)nd[b] + i];  // v - v_n (the AdamW update wrote it)
+#pragma unroll
+    for (int a = 0; a < 10; ++a) {
+      double r[3] = {0, 0, 0};
+#pragma unroll
+      for (int b = 0; b < 10; ++b) {
+        const double mab = me[10 * a + b];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) r[i] = fma(mab, dv[b][i], r[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) f[a][i] = fma(r[i], A.inv_h, f[a][i]);
+    }
+  }
 #pragma unroll
   for (int a = 0; a < 10; ++a) {
     const int64_t fp = A.fdest ? (int64_t)A.fdest[e * 10 + a] : e * 10 + a;
@@ -2621,7 +2649,8 @@ static ElArgs el_args(const Context* c, const double* x, const double* v) {
   A.dest = c->dest;
   A.fdest = c->fdest;
   A.err = c->err_flag;
-  A.inv_h = c->kvc_inv_h;
+  A.inv_h = c->eval_inv_h;
+  A.cls_mass = c->cls_mass;
   return A;
 }
 
@@ -2636,7 +2665,10 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
       ElArgs A = el_args(c, x, v);
       A.n_el = e_end;
       const unsigned grid = (unsigned)((e_end - e_begin + kFABlock - 1) / kFABlock);
-      if (c->n_cls > 0) {
+      if (c->n_cls > 0 && c->inr) {  // the AdamW gradient with element-level inertia (v holds v - v_n)
+        const size_t smem = sizeof(double) * c->n_cls * (13 + 100);
+        k_force_t10_aff<NQ, true, true><<<grid, kFABlock, smem, s>>>(A, e_begin, c->cls_aff);
+      } else if (c->n_cls > 0) {
         const size_t smem = sizeof(double) * c->n_cls * 13;
         k_force_t10_aff<NQ, true><<<grid, kFABlock, smem, s>>>(A, e_begin, c->cls_aff);
       } else {
@@ -2756,6 +2788,12 @@ tlfea_status launch_element_kernel(Context* c, const double* x, const double* v,
   }
   if (c->element == TLFEA_ANCF3243) return launch_el_model<2, 12>(c, x, v, tangent, s, e_begin, e_end);
   return launch_el_model<1, 48>(c, x, v, tangent, s, e_begin, e_end);
+}
+
+// k_force_t10_aff with element-level inertia serves this context (AdamW gradient)
+bool force_inertia_capable(const Context* c) {
+  return TLFEA_FORCE_AFF && c->element == TLFEA_T10 && c->mat.model == TLFEA_SVK && !c->mat.kv && c->nranks == 1 &&
+         c->n_cls > 0 && c->cls_aff && c->cls_mass;
 }
 
 static GatherArgs gather_args(const Context* c, double h, double* H) {

@@ -172,6 +172,16 @@ __global__ void k_constitutive(int64_t n, MatDev m, const double* __restrict__ F
 
 // ------------------------------------------------------------- launchers
 
+// The AdamW gradient from a force scratch that already holds the element
+// inertia (k_force_t10_aff<.., INR>): g = sum - f_ext - f_ff, no f_int.
+tlfea_status launch_gradient_inertia(Context* c, const double* fext, double* g, cudaStream_t s) {
+  if (c->n_own == 0) return TLFEA_OK;
+  k_gather_f_dof<<<grid_for(3 * c->n_own, kFgBlock), kFgBlock, 0, s>>>(
+      f_args(c, c->fscr, nullptr, nullptr, nullptr, fext, 1.0, 3, g, nullptr));
+  TL_CHECK_LAUNCH();
+  return TLFEA_OK;
+}
+
 tlfea_status launch_gather_f(Context* c, const double* v, const double* vn, const double* fext, double h,
                              double* g, double* fint, bool partial_only, cudaStream_t s) {
   if (c->n_own == 0) return TLFEA_OK;
@@ -264,7 +274,8 @@ tlfea_status launch_dual_update(Context* c, const double* q, double rho, double*
 __global__ void k_adamw_update(int64_t n, double c1, double c2, double alpha, double b1, double b2, double eps,
                                double wd, const double* __restrict__ g, double* __restrict__ m,
                                double* __restrict__ s, double* __restrict__ v, const double* __restrict__ q_n,
-                               double h, double* __restrict__ q) {
+                               double h, double* __restrict__ q, const double* __restrict__ vn,
+                               double* __restrict__ dv) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double gi = g[i];
@@ -275,6 +286,7 @@ __global__ void k_adamw_update(int64_t n, double c1, double c2, double alpha, do
   s[i] = si;
   v[i] = vi;
   q[i] = q_n[i] + h * vi;
+  if (dv) dv[i] = vi - vn[i];  // the element-level inertia input of the gradient
 }
 
 // ||a||^2 and ||b||^2 in a fixed reduction order: kNormBlocks blocks of
@@ -327,12 +339,13 @@ __global__ void __launch_bounds__(kNormThreads) k_sumsq_final(const double* __re
 }
 
 tlfea_status launch_adamw_update(Context* c, int l, const tlfea_adamw_params& p, const double* g, double* m,
-                                 double* s, double* v, const double* q_n, double h, double* q, cudaStream_t st) {
+                                 double* s, double* v, const double* q_n, double h, double* q, cudaStream_t st,
+                                 const double* vn, double* dv) {
   const int64_t n = 3 * c->n_coef;
   if (n == 0) return TLFEA_OK;
   const double c1 = 1.0 - std::pow(p.beta1, l), c2 = 1.0 - std::pow(p.beta2, l);
   k_adamw_update<<<grid_for(n, 256), 256, 0, st>>>(n, c1, c2, p.alpha, p.beta1, p.beta2, p.eps, p.weight_decay, g,
-                                                     m, s, v, q_n, h, q);
+                                                     m, s, v, q_n, h, q, vn, dv);
   TL_CHECK_LAUNCH();
   return TLFEA_OK;
 }

@@ -27,7 +27,8 @@ struct FArgs {
   const double* vn;
   const double* fext;
   double h;
-  int mode;                  // 0 full (f + residual), 1 f only, 2 residual from fpart_in
+  int mode;                  // 0 full (f + residual), 1 f only, 2 residual from fpart_in,
+                             // 3 residual from a scratch that includes the element inertia
   double* g;
   double* fint;
 };
@@ -46,6 +47,11 @@ __device__ __forceinline__ void gather_f_dof_one(int64_t t, const FArgs& A) {
   }
   if (A.fint) A.fint[t] = f;
   if (A.mode == 1 || !A.g) return;
+  if (A.mode == 3) {  // the scratch already holds f_a + (1/h) (m_e (v - v_n))_a per element
+    const int64_t I = A.own_nodes[i];
+    A.g[t] = f - (A.fext ? A.fext[3 * I + d] : 0.0) - A.fff[t];
+    return;
+  }
   double m = 0.0;
   const int32_t p0 = A.rowptr_c[i], p1 = A.rowptr_c[i + 1];
 #pragma unroll kFgUnroll

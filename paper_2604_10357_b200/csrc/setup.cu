@@ -1457,6 +1457,10 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
                                                       nen * nen, c->M);
       TL_CHECK_LAUNCH();
     }
+    if (per_class) {  // the class element masses, for the element-level inertia of the AdamW gradient
+      TL_TRY(c->alloc(&c->cls_mass, (size_t)c->n_cls * nen * nen));
+      TL_CUDA(cudaMemcpy(c->cls_mass, me.p, sizeof(double) * c->n_cls * nen * nen, cudaMemcpyDeviceToDevice));
+    }
     if (c->n_own > 0) {
       k_force_field<<<grid_for(c->n_own, 256), 256>>>(c->n_own, c->rowptr_c, c->M, c->gravity[0],
                                                       c->gravity[1], c->gravity[2], c->fff);

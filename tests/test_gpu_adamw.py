@@ -32,6 +32,10 @@ CASES = {
     "t10_4x3x2_mr_kv_keast5": lambda: (synth.kuhn_t10_box(4, 3, 2, 0.8, 0.6, 0.4),
                                        dict(synth.MR_PAPER, **synth.KV_TIRE), 1, synth.H_T10),
     "ancf_4x4_svk_kv": lambda: (synth.ancf_plate(4), dict(synth.SVK_PAPER, **synth.KV_TIRE), 2, synth.H_ANCF),
+    "t10_100el_svk_keast5_ragged": lambda: (synth.Mesh(0, synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).X,
+                                                       synth.kuhn_t10_box(5, 3, 2, 1.0, 0.6, 0.4).conn[:100]),
+                                            dict(synth.SVK_PAPER), 1, synth.H_T10),
+    "many_body_svk_keast5": lambda: (synth.many_body(12)[0], dict(synth.TIRE_DROP), 1, synth.H_T10),
 }
 
 
@@ -44,8 +48,12 @@ def start_state(mesh, h):
     return x - h * v, vn, fext, v.copy()
 
 
+@pytest.mark.parametrize("with_f", [True, False], ids=["with_fint", "no_fint"])
 @pytest.mark.parametrize("case", list(CASES))
-def test_adamw_iteration_parity(torch_cuda, case):
+def test_adamw_iteration_parity(torch_cuda, case, with_f):
+    """with_f = False: straight-sided T10 SVK meshes with classes (cfg1) take the
+    element-level inertia path (the gradient gather sums f_a + m_e (v - v_n)_e / h
+    per element, no mass-row SpMV)."""
     torch = torch_cuda
     import paper_2604_10357_b200 as T
     mesh, mat, rule, h = CASES[case]()
@@ -64,14 +72,15 @@ def test_adamw_iteration_parity(torch_cuda, case):
     for l in range(1, 16):
         # per-iteration parity from the oracle's state
         sv, sm, ss, sg = d(v), d(m), d(s), d(g)
-        q1, nrm = ctx.adamw_iteration(qn_d, vn_d, fe_d, h, l, PRM, sv, sm, ss, sg, f_int=f_d)
+        q1, nrm = ctx.adamw_iteration(qn_d, vn_d, fe_d, h, l, PRM, sv, sm, ss, sg, f_int=f_d if with_f else None)
         v, m, s, g, q, f, gn, vnorm = oracle.adamw_iteration(pr, l, PRM, qn, vn, fext, h, v, m, s, g)
         torch.cuda.synchronize()
         assert rel(sm.cpu().numpy(), m) <= 1e-13
         assert rel(ss.cpu().numpy(), s) <= 1e-13
         assert rel(sv.cpu().numpy(), v) <= 1e-13
         assert rel(q1.cpu().numpy(), q) <= 1e-14
-        assert rel(f_d.cpu().numpy(), f) <= 1e-11
+        if with_f:
+            assert rel(f_d.cpu().numpy(), f) <= 1e-11
         assert rel(sg.cpu().numpy(), g) <= 1e-11
         nh = nrm.cpu().numpy()
         assert nh[0] == pytest.approx(gn, rel=1e-11) and nh[1] == pytest.approx(vnorm, rel=1e-13)
