@@ -80,10 +80,15 @@ def test_constrained_eval_parity(torch_cuda, case):
     assert np.allclose(c.cpu().numpy(), c_ref, rtol=0, atol=1e-14 * max(1.0, np.abs(x).max()))
     assert np.array_equal(c.cpu().numpy(), c2.cpu().numpy())
     assert rel(lam_d.cpu().numpy(), lam + rho * c_ref) <= 1e-12
-    # determinism
-    g3, H3, _ = ctx.eval(d(x), d(v), d(vn), d(fext), h, lam=d(lam), rho=rho)
+    # determinism (same outputs requested: with f_int)
+    f3 = torch.empty_like(f)
+    g3, H3, _ = ctx.eval(d(x), d(v), d(vn), d(fext), h, None, None, f3, lam=d(lam), rho=rho)
     torch.cuda.synchronize()
     assert np.array_equal(g3.cpu().numpy(), g.cpu().numpy()) and np.array_equal(H3.cpu().numpy(), H.cpu().numpy())
+    # without f_int
+    g4, H4, _ = ctx.eval(d(x), d(v), d(vn), d(fext), h, lam=d(lam), rho=rho)
+    torch.cuda.synchronize()
+    assert rel(g4.cpu().numpy(), g0) <= TOL and np.array_equal(H4.cpu().numpy(), H.cpu().numpy())
 
 
 def test_alm_loop_with_adamw_inner_iterations(torch_cuda):

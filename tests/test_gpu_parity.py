@@ -319,3 +319,36 @@ def test_affine_layout_on_kuhn_boxes(torch_cuda, case):
     assert rel(g.cpu().numpy(), g0) <= TOL and rel(H.cpu().numpy(), H0) <= TOL and rel(f.cpu().numpy(), f0) <= TOL
     if not mat.get("eta_damp"):
         assert rel(fo, f0) <= TOL
+
+
+@pytest.mark.parametrize("case", ["cfg1_svk_4pt", "t10_5x3x1_svk_keast5_ragged", "t10_single_element_svk",
+                                  "t10_100el_svk_keast5_ragged", "t10_5x3x2_straight_svk_keast5"])
+def test_eval_parity_without_fint(torch_cuda, case):
+    """tlfea_eval with f_int_out = NULL (the north star's outputs g and H
+    only): g and H against the oracle at the same bar, bitwise repeatable, H
+    bitwise equal to the f_int path's, and v_n = NULL."""
+    import paper_2604_10357_b200 as T
+    torch = torch_cuda
+    mesh, mat, rule = CASES[case]()
+    h = synth.H_T10
+    grav = (0.0, -9.81, 0.3)
+    x, v, vn, fext = state(mesh)
+    pr = oracle.Problem(mesh, mat, rule, gravity=grav)
+    g0, H0, _ = pr.eval(x, v, vn, fext, h)
+    ctx = T.Context.from_mesh(mesh, mat, rule, gravity=grav)
+    outs = []
+    for _ in range(2):
+        g, H, _ = ctx.eval(dev(torch, x), dev(torch, v), dev(torch, vn), dev(torch, fext), h)
+        torch.cuda.synchronize()
+        outs.append((g.cpu().numpy(), H.cpu().numpy()))
+    (g, H), (g2, H2) = outs
+    assert rel(g, g0) <= TOL, rel(g, g0)
+    assert rel(H, H0) <= TOL, rel(H, H0)
+    assert np.array_equal(g, g2) and np.array_equal(H, H2)
+    _, gf, Hf, _ = gpu_eval(torch, mesh, mat, rule, x, v, vn, fext, h, gravity=grav)
+    assert np.array_equal(H, Hf)
+    # v_n = NULL (= 0) on the same path
+    g0n, _, _ = pr.eval(x, v, None, fext, h)
+    gn, _, _ = ctx.eval(dev(torch, x), dev(torch, v), None, dev(torch, fext), h)
+    torch.cuda.synchronize()
+    assert rel(gn.cpu().numpy(), g0n) <= TOL
