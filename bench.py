@@ -424,7 +424,7 @@ def run_ours(args):
     tfl = flops_launch / (avg_ms / 1e3) / 1e12
     fp64_meas, fp64_src = fp64_peak()
     f_hbm, f_fp64 = gbs / hbm_peak, tfl / FP64_NOMINAL_TFLOPS
-    mode = "force_only" if force_only else "force+tangent"
+    mode = "force_only" if force_only else ("force+tangent+kvc" if info.get("kv_consistent_tangent") else "force+tangent")
     layout = ["classes", "tables", "affine"][info.get("reference_layout", 1)]
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
