@@ -2363,6 +2363,321 @@ __device__ __forceinline__ void element_group_kvc(int64_t grp, const ElArgs& A, 
   }
 }
 
+
+// T10 two-phase consistent-KV tangent (SVK or MR). Phase A, two lanes per
+// (element, q): F and Fdot over 5 nodes each plus one shuffle, then S (the
+// elastic stress), S_v (reading Q7) and, for Mooney-Rivlin, the w-scaled 6x6
+// Voigt tangent (3 columns per lane), once per (element, q) into shared
+// memory. Phase B, one lane per (element, node a), in T10KVC_NPASS passes over
+// its partners: g, gd of both nodes from F, Fdot and the gradients, the
+// elastic block plus K^vv / h and K^vx for K_ab and K_ba (as element_group_kvc)
+// and f_a. The lane-per-node kernel (element_group_kvc) recomputed the F
+// reduction, the MR state and the MR tangent on every lane in every pass.
+#ifndef TLFEA_T10KVC_2PH
+#define TLFEA_T10KVC_2PH 1
+#endif
+#ifndef TLFEA_T10KVC_NPASS
+#define TLFEA_T10KVC_NPASS 3
+#endif
+template <int NQ, int MODEL>
+__device__ __forceinline__ void element_group_t10kvc(int64_t grp, const ElArgs& A, const double* __restrict__ s_tab,
+                                                     bool table_mode) {
+  constexpr int NEN = 10, GROUP = 10, EPW = 3, NUB = 55, NB = 6, TABW = 3 * NEN + 1;
+  constexpr int KQ = MODEL == 1 ? 51 : 30;  // F (9), Fd (9), S (6), S_v (6) [, w C (21, upper Voigt)]
+  constexpr int NPASS = TLFEA_T10KVC_NPASS, NBP = (NB + NPASS - 1) / NPASS;
+  static_assert(EPW * NQ * 2 <= 32, "phase A: two lanes per (element, q)");
+  __shared__ double s_k[kWarps][EPW][NQ][KQ];
+  __shared__ double s_x[kWarps][EPW][3 * NEN];
+  __shared__ double s_v[kWarps][EPW][3 * NEN];
+  __shared__ double s_st[kWarps][9][kLD];  // store staging
+  __shared__ int32_t s_pos[kWarps][32];
+  __shared__ int32_t s_cls[kWarps][EPW];
+  const int64_t n_el = A.n_el;
+  const MatDev& mat = A.mat;
+  const double ih = A.inv_h;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const bool lane_active = lane < EPW * GROUP;
+  const int g = lane_active ? lane / GROUP : 0;
+  const int a = lane_active ? lane % GROUP : 0;
+  const int64_t e = grp * EPW + g;
+  const bool valid = lane_active && e < n_el;
+  int32_t fd = 0;
+  if (lane_active) {
+    double xa[3] = {0, 0, 0}, va[3] = {0, 0, 0};
+    int ce = 0;
+    if (valid) {
+      fd = A.fdest ? A.fdest[e * NEN + a] : (int32_t)(e * NEN + a);
+      const int64_t I = A.conn[e * NEN + a];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        xa[i] = A.x[3 * I + i];
+        va[i] = A.v[3 * I + i];
+      }
+      if (!table_mode && a == 0) ce = A.cls[e];
+    }
+    if (table_mode) ce = wib * EPW + g;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      s_x[wib][g][3 * a + i] = xa[i];
+      s_v[wib][g][3 * a + i] = va[i];
+    }
+    if (a == 0) s_cls[wib][g] = ce;
+  }
+  __syncwarp();
+  {  // ---- phase A
+    const bool act = lane < EPW * NQ * 2;
+    const int pr = act ? lane >> 1 : 0, hf = lane & 1;
+    const int ge = pr / NQ, q = pr - NQ * (pr / NQ);
+    const double* t = s_tab + (s_cls[wib][ge] * NQ + q) * TABW;
+    double F[9], Fd[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) F[r] = Fd[r] = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < NEN / 2; ++bb) {
+      const int b = hf * (NEN / 2) + bb;
+      const double n0 = t[3 * b], n1 = t[3 * b + 1], n2 = t[3 * b + 2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double xi = s_x[wib][ge][3 * b + i], vi = s_v[wib][ge][3 * b + i];
+        F[3 * i] = fma(xi, n0, F[3 * i]);
+        F[3 * i + 1] = fma(xi, n1, F[3 * i + 1]);
+        F[3 * i + 2] = fma(xi, n2, F[3 * i + 2]);
+        Fd[3 * i] = fma(vi, n0, Fd[3 * i]);
+        Fd[3 * i + 1] = fma(vi, n1, Fd[3 * i + 1]);
+        Fd[3 * i + 2] = fma(vi, n2, Fd[3 * i + 2]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      const double o = __shfl_xor_sync(0xffffffffu, F[r], 1), od = __shfl_xor_sync(0xffffffffu, Fd[r], 1);
+      F[r] = hf ? o + F[r] : F[r] + o;
+      Fd[r] = hf ? od + Fd[r] : Fd[r] + od;
+    }
+    const double w = t[3 * NEN];
+    MRState ms;
+    if (MODEL == 1) mr_state(F, ms);
+    if (act) {
+      double* kq = s_k[wib][ge][q];
+      if (hf == 0) {
+        double S[6], Sv[6];
+        if (MODEL == 0) {
+          svk_S(F, mat.lam, mat.mu, S);
+        } else {
+          if (grp * EPW + ge < n_el && !(ms.J > 0.0)) atomicMin(A.err, (unsigned long long)((grp * EPW + ge) * 64 + q));
+          mr_S(ms, mat.C10, mat.C01, mat.kappa, S);
+        }
+        kv_S(F, Fd, mat.eta, mat.lamd, Sv);
+#pragma unroll
+        for (int r = 0; r < 9; ++r) {
+          kq[r] = F[r];
+          kq[9 + r] = Fd[r];
+        }
+#pragma unroll
+        for (int r = 0; r < 6; ++r) {
+          kq[18 + r] = S[r];
+          kq[24 + r] = Sv[r];
+        }
+      }
+      if constexpr (MODEL == 1) {
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          const int col = 3 * hf + cc;
+          double cv[6];
+          mr_Cv_column_dispatch(ms, mat.C10, mat.C01, mat.kappa, col, cv);
+#pragma unroll
+          for (int vv = 0; vv < 6; ++vv)
+            if (vv <= col) kq[30 + cs_idx(vv, col)] = w * cv[vv];
+        }
+      }
+    }
+  }
+  __syncwarp();
+  // ---- phase B
+  const int ce = s_cls[wib][g];
+  double fa[3] = {0, 0, 0};
+  const double lwe = MODEL == 0 ? mat.lam + mat.lamd * ih : mat.lamd * ih;  // x w below
+  const double mwe = MODEL == 0 ? mat.mu + mat.eta * ih : mat.eta * ih;
+#pragma unroll 1
+  for (int pass = 0; pass < NPASS; ++pass) {
+    double KA[NBP][9], KB[NBP][9];
+#pragma unroll
+    for (int j = 0; j < NBP; ++j)
+#pragma unroll
+      for (int r = 0; r < 9; ++r) KA[j][r] = KB[j][r] = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < NQ; ++q) {
+      const double* t = s_tab + (ce * NQ + q) * TABW;
+      const double* kq = s_k[wib][g][q];
+      const double gN[3] = {t[3 * a], t[3 * a + 1], t[3 * a + 2]};
+      const double w = t[3 * NEN];
+      double F[9], Fd[9], S[6], Sv[6];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) {
+        F[r] = kq[r];
+        Fd[r] = kq[9 + r];
+      }
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        S[r] = kq[18 + r];
+        Sv[r] = kq[24 + r];
+      }
+      double tw[3], twv[3], ga[3], gda[3];
+#pragma unroll
+      for (int I = 0; I < 3; ++I) {
+        tw[I] = w * (sget(S, I, 0) * gN[0] + sget(S, I, 1) * gN[1] + sget(S, I, 2) * gN[2]);
+        twv[I] = w * (sget(Sv, I, 0) * gN[0] + sget(Sv, I, 1) * gN[1] + sget(Sv, I, 2) * gN[2]);
+        ga[I] = F[3 * I] * gN[0] + F[3 * I + 1] * gN[1] + F[3 * I + 2] * gN[2];
+        gda[I] = Fd[3 * I] * gN[0] + Fd[3 * I + 1] * gN[1] + Fd[3 * I + 2] * gN[2];
+      }
+      if (pass == 0) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          fa[i] = fma(F[3 * i], tw[0] + twv[0], fma(F[3 * i + 1], tw[1] + twv[1], fma(F[3 * i + 2], tw[2] + twv[2], fa[i])));
+      }
+      double B[6], Cd[9];  // F F^T (Voigt), F Fdot^T
+#pragma unroll
+      for (int vv = 0; vv < 6; ++vv) {
+        int i, k;
+        voigt_pair(vv, i, k);
+        B[vv] = F[3 * i] * F[3 * k] + F[3 * i + 1] * F[3 * k + 1] + F[3 * i + 2] * F[3 * k + 2];
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          Cd[3 * i + k] = F[3 * i] * Fd[3 * k] + F[3 * i + 1] * Fd[3 * k + 1] + F[3 * i + 2] * Fd[3 * k + 2];
+      double CB[MODEL == 1 ? 6 : 1][3];
+      if constexpr (MODEL == 1) {
+        double Ba[6][3];
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv) {
+          int I, J;
+          voigt_pair(vv, I, J);
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+            Ba[vv][i] = (I == J) ? F[3 * i + I] * gN[I] : F[3 * i + I] * gN[J] + F[3 * i + J] * gN[I];
+        }
+#pragma unroll
+        for (int vv = 0; vv < 6; ++vv)
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < 6; ++ww)
+              sacc = fma(kq[30 + (vv <= ww ? cs_idx(vv, ww) : cs_idx(ww, vv))], Ba[ww][i], sacc);
+            CB[vv][i] = sacc;
+          }
+      }
+      const double lw = lwe * w, mw = mwe * w, ew = w * mat.eta, ldw = w * mat.lamd;
+#pragma unroll
+      for (int jj = 0; jj < NBP; ++jj) {
+        const int j = pass * NBP + jj;
+        const int b = j < NB ? partner<0>(a, 0, j) : -1;
+        if (b < 0) continue;
+        const double nb[3] = {t[3 * b], t[3 * b + 1], t[3 * b + 2]};
+        double gb[3], gdb[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          gb[i] = F[3 * i] * nb[0] + F[3 * i + 1] * nb[1] + F[3 * i + 2] * nb[2];
+          gdb[i] = Fd[3 * i] * nb[0] + Fd[3 * i + 1] * nb[1] + Fd[3 * i + 2] * nb[2];
+        }
+        const double sab = tw[0] * nb[0] + tw[1] * nb[1] + tw[2] * nb[2];
+        const double sv = twv[0] * nb[0] + twv[1] * nb[1] + twv[2] * nb[2];
+        const double dd = gN[0] * nb[0] + gN[1] * nb[1] + gN[2] * nb[2];
+        double E[9];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            E[3 * i + k] = lw * ga[i] * gb[k] + mw * gb[i] * ga[k] + mw * dd * B[vidx(i, k)] + (i == k ? sab : 0.0);
+        if constexpr (MODEL == 1) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            double bb[6];
+#pragma unroll
+            for (int vv = 0; vv < 6; ++vv) {
+              int I, J;
+              voigt_pair(vv, I, J);
+              bb[vv] = (I == J) ? F[3 * k + I] * nb[I] : F[3 * k + I] * nb[J] + F[3 * k + J] * nb[I];
+            }
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              double acc = 0.0;
+#pragma unroll
+              for (int vv = 0; vv < 6; ++vv) acc = fma(CB[vv][i], bb[vv], acc);
+              E[3 * i + k] += acc;
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const double c = ew * dd * Cd[3 * i + k] + (i == k ? sv : 0.0);
+            KA[jj][3 * i + k] += E[3 * i + k] + c + ew * gb[i] * gda[k] + ldw * ga[i] * gdb[k];
+            KB[jj][3 * i + k] += E[3 * k + i] + c + ew * ga[i] * gdb[k] + ldw * gb[i] * gda[k];
+          }
+      }
+    }
+    if (valid && pass == 0) {
+      double* fo = A.fscr + (int64_t)fd * 3;
+      fo[0] = fa[0];
+      fo[1] = fa[1];
+      fo[2] = fa[2];
+    }
+    // blocks -> 18-value scratch slots: [H(I,J) part | H(J,I) part]
+    constexpr int NLB = EPW * GROUP, NIT = (NLB + 2) / 3;
+    const int bi = lane / 9, rr = lane - 9 * (lane / 9);
+#pragma unroll
+    for (int jj = 0; jj < NBP; ++jj) {
+      const int j = pass * NBP + jj;
+      const int b = (valid && j < NB) ? partner<0>(a, 0, j) : -1;
+      int32_t pos = -1;
+      bool flip = false;
+      if (b >= 0) {
+        const int ub = a <= b ? ublk(NEN, a, b) : ublk(NEN, b, a);
+        const int32_t d = A.dest[e * NUB + ub];
+        pos = d >> 1;
+        flip = a != b && ((a > b) != ((d & 1) != 0));
+      }
+      s_pos[wib][lane] = pos;
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        if (b >= 0) {
+#pragma unroll
+          for (int r = 0; r < 9; ++r) s_st[wib][r][lane] = (flip != (part == 1)) ? KB[jj][r] : KA[jj][r];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+          const int blk = 3 * it + bi;
+          if (lane < 27 && blk < NLB) {
+            const int32_t p = s_pos[wib][blk];
+            if (p >= 0) k_store(A.Kscr + (int64_t)p * 18 + 9 * part + rr, s_st[wib][rr][blk]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+template <int NQ, int MODEL, bool CLS, bool AFF>
+__global__ void __launch_bounds__(kWarps * 32, 2) k_element_t10kvc(ElArgs A) {
+  extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][31]; else the warp's staged tables
+  const int64_t grp = A.g0 + (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if constexpr (CLS) {
+    const int tot = A.n_cls * NQ * 31;
+    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_tab[t] = A.cls_tab[t];
+    __syncthreads();
+  } else if constexpr (AFF) {
+    t10_stage_affine<NQ>(grp, A, s_tab);
+  } else {
+    t10_stage_tables<NQ>(grp, A, s_tab);
+  }
+  element_group_t10kvc<NQ, MODEL>(grp, A, s_tab, !CLS);
+}
+
 template <int ELEM, int NQ, int MODEL, bool CLS>
 __global__ void __launch_bounds__(kWarps * 32, 2) k_element_kvc(ElArgs A) {
   extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
@@ -2743,6 +3058,21 @@ static tlfea_status launch_el_kvc(Context* c, const double* x, const double* v, 
   ElArgs A = el_args(c, x, v);
   A.n_el = e_end;
   A.g0 = e_begin / G::EPW;
+  if constexpr (ELEM == 0 && TLFEA_T10KVC_2PH) {  // the two-phase T10 group
+    if (c->n_cls > 0) {
+      const size_t smem = sizeof(double) * c->n_cls * NQ * 31;
+      auto kern = k_element_t10kvc<NQ, MODEL, true, false>;
+      TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
+      kern<<<grid, kWarps * 32, smem, s>>>(A);
+    } else {
+      const size_t smem = sizeof(double) * kWarps * 3 * NQ * 31;
+      auto kern = c->aff ? k_element_t10kvc<NQ, MODEL, false, true> : k_element_t10kvc<NQ, MODEL, false, false>;
+      TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
+      kern<<<grid, kWarps * 32, smem, s>>>(A);
+    }
+    TL_CHECK_LAUNCH();
+    return TLFEA_OK;
+  }
   if (c->n_cls > 0) {
     const size_t smem = sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
     auto kern = k_element_kvc<ELEM, NQ, MODEL, true>;
