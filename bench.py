@@ -441,6 +441,10 @@ def run_ours(args):
     if f_hbm >= f_fp64:
         roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": f_hbm,
                 "peak_source": hbm_src, **common}
+        if f_hbm > 1.0:
+            roof["note"] = ("frac > 1: the numerator is SURVEY §8(d)'s paper-layout bytes (per-(e,q) tables); this "
+                            "path reads no tables (geometry classes / affine layout), so it beats that roofline; "
+                            "hbm_frac_min_layout is the fraction against the bytes it must move")
     else:
         roof = {"bound": "alu", "achieved": tfl, "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s", "frac": f_fp64,
                 "peak_source": "DFMA unit count: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md)", **common}

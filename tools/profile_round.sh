@@ -49,6 +49,6 @@ done <<'EOF'
 --config 3 --hessian upper|^k_gather_units_v3$|3|cfg3_t10_144x96x48_svk_keast5|force+tangent|upper|classes
 --config 3 --tables|^k_element$|3|cfg3_t10_144x96x48_svk_keast5|force+tangent|full|tables
 --config 3 --mesh straight|^k_element$|3|cfg3_t10_144x96x48_svk_keast5|force+tangent|full|affine
---config 2 --kv-consistent|k_element_kvc|3|cfg2_t10_42x28x14_mr_kv_keast5|force+tangent+kvc|full|classes
+--config 2 --kv-consistent|k_element_t10kvc|3|cfg2_t10_42x28x14_mr_kv_keast5|force+tangent+kvc|full|classes
 EOF
 ls -la $OUT | head -60
