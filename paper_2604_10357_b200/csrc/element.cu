@@ -55,8 +55,31 @@ constexpr int kWarps = kElWarps;  // warps per CTA
 // Tangent scratch stores carry the streaming hint (st.global.cs): measured
 // on config 3, 10.93 vs 11.21 ms for the element kernel; the same hint on the
 // H writes of the gather changes nothing (8.06 vs 8.06 ms), so those stay plain.
-__device__ __forceinline__ void k_store(double* p, double v) { __stcs(p, v); }
-__device__ __forceinline__ void h_store(double* p, double v) { *p = v; }
+// TLFEA_CHECK builds (the bounds-checked library of tests/ and tools/, in place
+// of compute-sanitizer): every store into the tangent scratch, the force
+// scratch and H, and every TMA window of the gather, is checked against the
+// buffer the host registered for the launch (g_rng: [lo, hi) of Kscr, fscr,
+// H); a miss prints the address and traps.
+#ifndef TLFEA_CHECK
+#define TLFEA_CHECK 0
+#endif
+__device__ const double* g_rng[6];
+__device__ __forceinline__ void tl_chk(const double* p, int which, int line) {
+  if (TLFEA_CHECK && (p < g_rng[2 * which] || p >= g_rng[2 * which + 1])) {
+    printf("tlfea bounds check: buffer %d, line %d: %p outside [%p, %p)\n", which, line, (const void*)p,
+           (const void*)g_rng[2 * which], (const void*)g_rng[2 * which + 1]);
+    __trap();
+  }
+}
+#define TL_FCHK(fo) tl_chk((fo) + 2, 1, __LINE__), tl_chk((fo), 1, __LINE__)
+__device__ __forceinline__ void k_store(double* p, double v) {
+  if (TLFEA_CHECK) tl_chk(p, 0, __LINE__);
+  __stcs(p, v);
+}
+__device__ __forceinline__ void h_store(double* p, double v) {
+  if (TLFEA_CHECK) tl_chk(p, 2, __LINE__);
+  *p = v;
+}
 constexpr int kLD = 33;    // padded lane stride of the per-warp shared tables
 
 // Blocks owned by a lane: index j -> partner b (-1 when none).
@@ -429,6 +452,7 @@ __device__ __forceinline__ void element_group(int64_t grp, const ElArgs& A, cons
   if (valid && pass == 0 && (MULTI || half == 0)) {
     const int64_t fp = fdest ? (int64_t)fdest[e * NEN + a] : e * NEN + a;
     double* fo = fscr + fp * 3;
+    if (TLFEA_CHECK) TL_FCHK(fo);
     fo[0] = fa[0];
     fo[1] = fa[1];
     fo[2] = fa[2];
@@ -863,6 +887,7 @@ __device__ __forceinline__ void element_group_t10svk(int64_t grp, const ElArgs& 
     }
     if (valid && pass == 0) {
       double* fo = A.fscr + (int64_t)pre.fd * 3;
+      if (TLFEA_CHECK) TL_FCHK(fo);
       fo[0] = fa[0];
       fo[1] = fa[1];
       fo[2] = fa[2];
@@ -1115,6 +1140,7 @@ __device__ __forceinline__ void element_group_t10mr(int64_t grp, const ElArgs& A
   }
   if (valid) {
     double* fo = A.fscr + (int64_t)fd * 3;
+    if (TLFEA_CHECK) TL_FCHK(fo);
     fo[0] = fa[0];
     fo[1] = fa[1];
     fo[2] = fa[2];
@@ -1228,6 +1254,7 @@ __device__ __forceinline__ void element_group_t10svk_force(int64_t grp, const El
     for (int i = 0; i < 3; ++i) fa[i] = fma(pw[3 * i], n0, fma(pw[3 * i + 1], n1, fma(pw[3 * i + 2], n2, fa[i])));
   }
   double* fo = A.fscr + (int64_t)pre.fd * 3;
+  if (TLFEA_CHECK) TL_FCHK(fo);
   fo[0] = fa[0];
   fo[1] = fa[1];
   fo[2] = fa[2];
@@ -1384,6 +1411,7 @@ __global__ void __launch_bounds__(kFW * 32, NQ == 4 ? TLFEA_FW_MINB4 : TLFEA_FW_
         for (int i = 0; i < 3; ++i) fa[i] = fma(pw[3 * i], n0, fma(pw[3 * i + 1], n1, fma(pw[3 * i + 2], n2, fa[i])));
       }
       double* fo = A.fscr + (int64_t)fd[r] * 3;
+      if (TLFEA_CHECK) TL_FCHK(fo);
       fo[0] = fa[0];
       fo[1] = fa[1];
       fo[2] = fa[2];
@@ -1568,6 +1596,7 @@ __global__ void __launch_bounds__(kFABlock, TLFEA_FA_MINB) k_force_t10_aff(ElArg
   for (int a = 0; a < 10; ++a) {
     const int64_t fp = A.fdest ? (int64_t)A.fdest[e * 10 + a] : e * 10 + a;
     double* fo = A.fscr + 3 * fp;
+    if (TLFEA_CHECK) TL_FCHK(fo);
     fo[0] = f[a][0];
     fo[1] = f[a][1];
     fo[2] = f[a][2];
@@ -1740,6 +1769,7 @@ __device__ __forceinline__ void element_group_ancf_svk(int64_t e, const ElArgs& 
   }
   if (half == 0 && pass == 0) {
     double* fo = A.fscr + (int64_t)fd * 3;
+    if (TLFEA_CHECK) TL_FCHK(fo);
     fo[0] = fa[0];
     fo[1] = fa[1];
     fo[2] = fa[2];
@@ -1937,6 +1967,7 @@ __device__ __forceinline__ void element_group_beam_svk(int64_t grp, const ElArgs
   }
   if (valid) {
     double* fo = A.fscr + (int64_t)fd * 3;
+    if (TLFEA_CHECK) TL_FCHK(fo);
     fo[0] = fa[0];
     fo[1] = fa[1];
     fo[2] = fa[2];
@@ -2320,6 +2351,7 @@ __device__ __forceinline__ void element_group_kvc(int64_t grp, const ElArgs& A, 
     if (valid && pass == 0 && (MULTI || half == 0)) {
       const int64_t fp = A.fdest ? (int64_t)A.fdest[e * NEN + a] : e * NEN + a;
       double* fo = A.fscr + fp * 3;
+      if (TLFEA_CHECK) TL_FCHK(fo);
       fo[0] = fa[0];
       fo[1] = fa[1];
       fo[2] = fa[2];
@@ -2621,6 +2653,7 @@ __device__ __forceinline__ void element_group_t10kvc(int64_t grp, const ElArgs& 
     }
     if (valid && pass == 0) {
       double* fo = A.fscr + (int64_t)fd * 3;
+      if (TLFEA_CHECK) TL_FCHK(fo);
       fo[0] = fa[0];
       fo[1] = fa[1];
       fo[2] = fa[2];
@@ -2775,6 +2808,10 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
     const uintptr_t a = (uintptr_t)(Kscr + w0 * 9) & ~(uintptr_t)15;
     const uintptr_t b = ((uintptr_t)(Kscr + w1 * 9) + 15) & ~(uintptr_t)15;
     const uint32_t wi = wk0 + k;
+    if (TLFEA_CHECK) {
+      tl_chk(Kscr + w0 * 9, 0, __LINE__);
+      tl_chk(Kscr + w1 * 9 - 1, 0, __LINE__);
+    }
     bulk_load(W.buf[wi & 1], (const void*)a, (unsigned)(b - a), &W.bar[wi & 1]);
   };
   if (lane == 0 && nwin > 0) issue(0);
@@ -2824,7 +2861,10 @@ __device__ __forceinline__ void gather_units_warp(int64_t u0, const GatherArgs& 
       const bool diag = (dgl >> 16) != 0;
 #pragma unroll
       for (int d = 0; d < 3; ++d)
-        if (vl && (!diag || f >= d)) H[o + f + d * (2 + 3 * L) - d * (d - 1) / 2] = st[sl * 9 + 3 * d + f];
+        if (vl && (!diag || f >= d)) {
+          if (TLFEA_CHECK) tl_chk(&H[o + f + d * (2 + 3 * L) - d * (d - 1) / 2], 2, __LINE__);
+          H[o + f + d * (2 + 3 * L) - d * (d - 1) / 2] = st[sl * 9 + 3 * d + f];
+        }
     } else {
       const int dl = dgl & 0xffff, dT = dgl >> 16;
 #pragma unroll
@@ -2893,6 +2933,10 @@ __device__ __forceinline__ void gather_units_warp_kvc(int64_t u0, const GatherAr
   auto issue = [&](int k) {
     const int64_t w0 = P0 + (int64_t)k * kG3WB2, w1 = min(w0 + (int64_t)kG3WB2, P1);
     const uint32_t wi = wk0 + k;  // 144-byte slots: always 16-byte aligned
+    if (TLFEA_CHECK) {
+      tl_chk(Kscr + w0 * 18, 0, __LINE__);
+      tl_chk(Kscr + w1 * 18 - 1, 0, __LINE__);
+    }
     bulk_load(W.buf[wi & 1], (const void*)(Kscr + w0 * 18), (unsigned)((w1 - w0) * 144), &W.bar[wi & 1]);
   };
   if (lane == 0 && nwin > 0) issue(0);
@@ -3109,9 +3153,20 @@ static tlfea_status launch_el_model(Context* c, const double* x, const double* v
 
 // Local elements [e_begin, e_end) (e_end < 0: all); e_begin a multiple of
 // the element-kernel CTA tile.
+// TLFEA_CHECK: register the launch's buffers for the device bounds checks
+static tlfea_status check_ranges(const Context* c, const double* H, cudaStream_t s) {
+  if (!TLFEA_CHECK) return TLFEA_OK;
+  const size_t kb = (size_t)c->n_el * n_ublk_of(c->nen) * (c->kvc ? 18 : 9);
+  const double* r[6] = {c->Kscr, c->Kscr + kb, c->fscr, c->fscr + (size_t)c->n_el * c->nen * 3,
+                        H, H ? H + c->nnz_H : nullptr};
+  TL_CUDA(cudaMemcpyToSymbolAsync(g_rng, r, sizeof(r), 0, cudaMemcpyHostToDevice, s));
+  return TLFEA_OK;
+}
+
 tlfea_status launch_element_kernel(Context* c, const double* x, const double* v, bool tangent, cudaStream_t s,
                                    int64_t e_begin, int64_t e_end) {
   if (e_end < 0) e_end = c->n_el;
+  TL_TRY(check_ranges(c, nullptr, s));
   if (c->element == TLFEA_T10) {
     if (c->nq == 4) return launch_el_model<0, 4>(c, x, v, tangent, s, e_begin, e_end);
     return launch_el_model<0, 5>(c, x, v, tangent, s, e_begin, e_end);
@@ -3143,6 +3198,7 @@ static GatherArgs gather_args(const Context* c, double h, double* H) {
 
 tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
   if (c->n_units == 0) return TLFEA_OK;
+  TL_TRY(check_ranges(c, H, s));
   const int64_t per = (int64_t)kG3Warps * 32;
   if (c->kvc) {
     k_gather_units_kvc<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(gather_args(c, h, H));

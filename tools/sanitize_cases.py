@@ -38,7 +38,8 @@ cases = [("cfg1", synth.config(1).mesh, dict(synth.SVK_PAPER), 0),
          ("t10_100_svk_kv", small, dict(synth.SVK_PAPER, **synth.KV_TIRE), 1),
          ("ancf_4x4", synth.ancf_plate(4), dict(synth.SVK_PAPER), 2),
          ("ancf_5x5_graded", synth.ancf_plate_graded(5), dict(synth.SVK_PAPER), 2),
-         ("beam_9", synth.ancf_beam(9), dict(synth.SVK_PAPER), 3)]
+         ("beam_9", synth.ancf_beam(9), dict(synth.SVK_PAPER), 3),
+         ("t10_100_straight_svk", synth.perturbed_straight(small), dict(synth.SVK_PAPER), 1)]
 worst = 0.0
 for name, mesh, mat, rule in cases:
     x, v, vn, fe = state(mesh)
@@ -53,13 +54,40 @@ for name, mesh, mat, rule in cases:
     e = max(rel(g.cpu().numpy(), g0), rel(H.cpu().numpy(), H0), rel(f.cpu().numpy(), f0), rel(fo.cpu().numpy(), f0))
     worst = max(worst, e)
     print(f"{name}: max rel err {e:.2e}", flush=True)
-# one AdamW inner iteration (NEXT-2) on config 1
+# the consistent Kelvin-Voigt tangent (NEXT-4): T10 two-phase (classes, tables), ANCF, beam
+KVS = dict(eta_damp=2.0e6, lambda_damp=1.0e6)
+for name, mesh, mat, rule in [("kvc_t10_svk", small, dict(synth.SVK_PAPER, **KVS), 1),
+                              ("kvc_t10_perturbed_mr", synth.perturbed(small), dict(synth.MR_PAPER, **KVS), 0),
+                              ("kvc_ancf_4x4", synth.ancf_plate(4), dict(synth.SVK_PAPER, **KVS), 2),
+                              ("kvc_beam_5", synth.ancf_beam(5), dict(synth.MR_PAPER, **KVS), 3)]:
+    x, v, vn, fe = state(mesh)
+    h = synth.H_T10 if mesh.element == 0 else synth.H_ANCF
+    ctx = T.Context.from_mesh(mesh, mat, rule, kv_consistent=True)
+    g, H, f = ctx.empty_outputs()
+    ctx.eval(d(x), d(v), d(vn), d(fe), h, g, H, f)
+    torch.cuda.synchronize()
+    pr = oracle.Problem(mesh, mat, rule)
+    g0, H0, f0 = pr.eval(x, v, vn, fe, h, kv_consistent=True)
+    e = max(rel(g.cpu().numpy(), g0), rel(H.cpu().numpy(), H0), rel(f.cpu().numpy(), f0))
+    worst = max(worst, e)
+    print(f"{name}: max rel err {e:.2e}", flush=True)
+# one AdamW inner iteration (NEXT-2) on config 1 (no f_int: the element-inertia gradient path)
 mesh = synth.config(1).mesh
 x, v, vn, fe = state(mesh)
 ctx = T.Context.from_mesh(mesh, dict(synth.SVK_PAPER), 0)
 prm = dict(alpha=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0)
 vd, m, s, gd = d(v.copy()), torch.zeros_like(d(v)), torch.zeros_like(d(v)), torch.zeros_like(d(v))
 ctx.adamw_iteration(d(x), d(vn), d(fe), 1e-3, 1, prm, vd, m, s, gd)
+torch.cuda.synchronize()
+# the library NCCL transport on a one-rank communicator (begin / exchange / interior / finish)
+ctx1 = T.Context.from_mesh(mesh, dict(synth.SVK_PAPER), 0)
+ctx1.nccl_attach(T.nccl_unique_id())
+g1, H1, f1 = ctx1.empty_outputs()
+buf = torch.zeros(1, dtype=torch.float64, device="cuda")
+ctx1.eval_begin(d(x), d(v), 1e-3, H1, buf)
+ctx1.eval_exchange(buf, buf)
+ctx1.eval_interior(d(x), d(v), 1e-3, H1)
+ctx1.eval_finish(buf, d(v), d(vn), d(fe), 1e-3, g1, H1, f1)
 torch.cuda.synchronize()
 # 2-way virtual partition (eval_begin / device copies / eval_finish)
 P = 2
