@@ -1603,6 +1603,140 @@ __global__ void __launch_bounds__(kFABlock, TLFEA_FA_MINB) k_force_t10_aff(ElArg
   }
 }
 
+
+// ------------------------------------ ANCF force only, one lane per point
+// ANCF3443 (16 coefficients, 48 points) and ANCF3243 (8, 12) force only
+// (tlfea_force_only, the AdamW inner evaluation, Alg. 2): one lane
+// per (element, quadrature point) computes F (and Fdot) = sum_a (x_a, v_a) (x)
+// grad N_a (Eq. F_assembly), the stress (SVK / MR, + Kelvin-Voigt) and
+// accumulates its point's f_a += w P grad N_a for all the element's
+// coefficients (Eq. fint_local); the partials are summed over the element's
+// lanes through shared memory in ascending lane order (deterministic). The
+// lane-per-coefficient group reduced F through shared memory and evaluated
+// the stress on every lane at every point.
+#ifndef TLFEA_FORCE_LPQ
+#define TLFEA_FORCE_LPQ 1
+#endif
+template <int ELEM, int NQ, int MODEL, bool KV, bool CLS>
+__global__ void __launch_bounds__(kWarps * 32) k_force_lpq(ElArgs A, int64_t e_begin) {
+  constexpr int NEN = Geo<ELEM>::NEN, TABW = 3 * NEN + 1, ND = 3 * NEN, LDF = ND + 1;
+  constexpr int EPW = NQ >= 32 ? 1 : 32 / NQ, NR = (NQ + 31) / 32;
+  extern __shared__ double s_dyn[];  // [kWarps][32][LDF] lane partials, then (CLS) [n_cls][NQ][TABW]
+  __shared__ double s_x[kWarps][EPW][ND];
+  __shared__ double s_v[kWarps][KV ? EPW : 1][KV ? ND : 1];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* s_f = s_dyn + (size_t)wib * 32 * LDF;
+  const double* s_tab = s_dyn + (size_t)kWarps * 32 * LDF;
+  if (CLS) {
+    double* st = s_dyn + (size_t)kWarps * 32 * LDF;
+    for (int t = threadIdx.x; t < A.n_cls * NQ * TABW; t += blockDim.x) st[t] = A.cls_tab[t];
+  }
+  const int64_t e0 = e_begin + ((int64_t)blockIdx.x * kWarps + wib) * EPW;
+  for (int t = lane; t < EPW * NEN; t += 32) {
+    const int g = t / NEN, a = t - NEN * g;
+    const int64_t e = e0 + g;
+    double xa[3] = {0, 0, 0}, va[3] = {0, 0, 0};
+    if (e < A.n_el) {
+      const int64_t I = A.conn[e * NEN + a];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        xa[i] = A.x[3 * I + i];
+        if (KV) va[i] = A.v[3 * I + i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      s_x[wib][g][3 * a + i] = xa[i];
+      if (KV) s_v[wib][g][3 * a + i] = va[i];
+    }
+  }
+  __syncthreads();
+  const int g = NQ >= 32 ? 0 : lane / NQ;
+  const int64_t e = e0 + g;
+  const bool act = (NQ >= 32 || lane < EPW * NQ) && e < A.n_el;
+  const int ce = (CLS && act) ? A.cls[e] : 0;
+  double f[ND];
+#pragma unroll
+  for (int r = 0; r < ND; ++r) f[r] = 0.0;
+#pragma unroll
+  for (int rnd = 0; rnd < NR; ++rnd) {
+    const int q = NQ >= 32 ? lane + 32 * rnd : lane - NQ * g;
+    if (!act || q >= NQ) continue;
+    const double* gN;
+    double w;
+    if (CLS) {
+      gN = s_tab + (ce * NQ + q) * TABW;
+      w = gN[ND];
+    } else {
+      gN = A.gradN + (e * NQ + q) * ND;
+      w = A.J0w[e * NQ + q];
+    }
+    double F[9], Fd[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) F[r] = Fd[r] = 0.0;
+#pragma unroll
+    for (int b = 0; b < NEN; ++b) {
+      const double n0 = gN[3 * b], n1 = gN[3 * b + 1], n2 = gN[3 * b + 2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double xi = s_x[wib][g][3 * b + i];
+        F[3 * i] = fma(xi, n0, F[3 * i]);
+        F[3 * i + 1] = fma(xi, n1, F[3 * i + 1]);
+        F[3 * i + 2] = fma(xi, n2, F[3 * i + 2]);
+        if (KV) {
+          const double vi = s_v[wib][g][3 * b + i];
+          Fd[3 * i] = fma(vi, n0, Fd[3 * i]);
+          Fd[3 * i + 1] = fma(vi, n1, Fd[3 * i + 1]);
+          Fd[3 * i + 2] = fma(vi, n2, Fd[3 * i + 2]);
+        }
+      }
+    }
+    double S[6];
+    if (MODEL == 0) {
+      svk_S(F, A.mat.lam, A.mat.mu, S);
+    } else {
+      MRState ms;
+      mr_state(F, ms);
+      if (!(ms.J > 0.0)) atomicMin(A.err, (unsigned long long)(e * 64 + q));
+      mr_S(ms, A.mat.C10, A.mat.C01, A.mat.kappa, S);
+    }
+    if (KV) {
+      double Sv[6];
+      kv_S(F, Fd, A.mat.eta, A.mat.lamd, Sv);
+#pragma unroll
+      for (int r = 0; r < 6; ++r) S[r] += Sv[r];
+    }
+    double P[9];  // w F S
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int J = 0; J < 3; ++J)
+        P[3 * i + J] = w * (F[3 * i] * sget(S, 0, J) + F[3 * i + 1] * sget(S, 1, J) + F[3 * i + 2] * sget(S, 2, J));
+#pragma unroll
+    for (int b = 0; b < NEN; ++b) {
+      const double n0 = gN[3 * b], n1 = gN[3 * b + 1], n2 = gN[3 * b + 2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) f[3 * b + i] = fma(P[3 * i], n0, fma(P[3 * i + 1], n1, fma(P[3 * i + 2], n2, f[3 * b + i])));
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < ND; ++r) s_f[lane * LDF + r] = f[r];
+  __syncwarp();
+  // f of (element g2, value r) = sum over the element's lanes in ascending order
+  for (int t = lane; t < EPW * ND; t += 32) {
+    const int g2 = t / ND, r = t - ND * g2;
+    const int64_t e2 = e0 + g2;
+    if (e2 >= A.n_el) continue;
+    const int l0 = NQ >= 32 ? 0 : g2 * NQ, l1 = NQ >= 32 ? 32 : l0 + NQ;
+    double sum = 0.0;
+    for (int l = l0; l < l1; ++l) sum += s_f[l * LDF + r];
+    const int a = r / 3, i = r - 3 * a;
+    const int64_t fp = A.fdest ? (int64_t)A.fdest[e2 * NEN + a] : e2 * NEN + a;
+    if (TLFEA_CHECK) tl_chk(A.fscr + 3 * fp + i, 1, __LINE__);
+    A.fscr[3 * fp + i] = sum;
+  }
+}
+
 #ifndef TLFEA_ANCF_NPASS
 #define TLFEA_ANCF_NPASS 1  // block passes (each re-runs phase A per chunk)
 #endif
@@ -3057,6 +3191,20 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
       TL_CHECK_LAUNCH();
       return TLFEA_OK;
     }
+  }
+  if constexpr (ELEM != 0 && !TAN && TLFEA_FORCE_LPQ) {  // ANCF force only: one lane per point
+    constexpr int EPWq = NQ >= 32 ? 1 : 32 / NQ;
+    const int64_t per = (int64_t)kWarps * EPWq;
+    ElArgs A = el_args(c, x, v);
+    A.n_el = e_end;
+    const unsigned grid = (unsigned)((e_end - e_begin + per - 1) / per);
+    const size_t smem = sizeof(double) * ((size_t)kWarps * 32 * (3 * G::NEN + 1) +
+                                          (c->n_cls > 0 ? (size_t)c->n_cls * NQ * (3 * G::NEN + 1) : 0));
+    auto kern = c->n_cls > 0 ? k_force_lpq<ELEM, NQ, MODEL, KV, true> : k_force_lpq<ELEM, NQ, MODEL, KV, false>;
+    TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
+    kern<<<grid, kWarps * 32, smem, s>>>(A, e_begin);
+    TL_CHECK_LAUNCH();
+    return TLFEA_OK;
   }
   if (e_begin % per_cta != 0) return fail(TLFEA_E_INVALID, "internal: element range not tile aligned");
   const unsigned grid = (unsigned)((e_end - e_begin + per_cta - 1) / per_cta);

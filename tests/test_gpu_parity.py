@@ -215,7 +215,10 @@ def test_constitutive_hook(torch_cuda, model):
 @pytest.mark.parametrize("case", ["ancf_6x6_graded_svk", "ancf_4x4_perturbed_svk", "ancf_5x5_graded_svk_kv",
                                   "ancf_4x4_svk_kv", "ancf_3x3_svk", "t10_100el_perturbed_svk_keast5",
                                   "t10_5x3x2_straight_svk_keast5", "t10_4x3x2_straight_svk_4pt",
-                                  "t10_5x3x1_svk_keast5_ragged", "cfg1_svk_4pt"])
+                                  "t10_5x3x1_svk_keast5_ragged", "cfg1_svk_4pt",
+                                  "ancf_5x5_mr_kv", "ancf_6x6_graded_svk", "ancf_4x4_perturbed_svk",
+                                  "ancf_5x5_graded_svk_kv", "beam_16_svk", "beam_9_mr_kv",
+                                  "beam_5_perturbed_svk_kv"])
 def test_force_only_parity(torch_cuda, case):
     """tlfea_force_only (the AdamW inner evaluation) on the class and the
     per-(e,q) table paths, with and without Kelvin-Voigt."""
