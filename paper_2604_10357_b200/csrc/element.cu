@@ -1604,8 +1604,9 @@ __global__ void __launch_bounds__(kFABlock, TLFEA_FA_MINB) k_force_t10_aff(ElArg
 }
 
 
-// ------------------------------------ ANCF force only, one lane per point
-// ANCF3443 (16 coefficients, 48 points) and ANCF3243 (8, 12) force only
+// ------------------------------------ force only, one lane per point
+// ANCF3443 (16 coefficients, 48 points), ANCF3243 (8, 12) and T10 with
+// Mooney-Rivlin or Kelvin-Voigt (10, 4 or 5: 6-8 elements per warp) force only
 // (tlfea_force_only, the AdamW inner evaluation, Alg. 2): one lane
 // per (element, quadrature point) computes F (and Fdot) = sum_a (x_a, v_a) (x)
 // grad N_a (Eq. F_assembly), the stress (SVK / MR, + Kelvin-Voigt) and
@@ -3192,7 +3193,9 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
       return TLFEA_OK;
     }
   }
-  if constexpr (ELEM != 0 && !TAN && TLFEA_FORCE_LPQ) {  // ANCF force only: one lane per point
+  // force only, one lane per point: ANCF, and T10 with Mooney-Rivlin or Kelvin-Voigt
+  // (T10 SVK without damping has the affine and two-phase kernels)
+  if constexpr ((ELEM != 0 || MODEL != 0 || KV) && !TAN && TLFEA_FORCE_LPQ) {
     constexpr int EPWq = NQ >= 32 ? 1 : 32 / NQ;
     const int64_t per = (int64_t)kWarps * EPWq;
     ElArgs A = el_args(c, x, v);

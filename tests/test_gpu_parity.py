@@ -218,7 +218,9 @@ def test_constitutive_hook(torch_cuda, model):
                                   "t10_5x3x1_svk_keast5_ragged", "cfg1_svk_4pt",
                                   "ancf_5x5_mr_kv", "ancf_6x6_graded_svk", "ancf_4x4_perturbed_svk",
                                   "ancf_5x5_graded_svk_kv", "beam_16_svk", "beam_9_mr_kv",
-                                  "beam_5_perturbed_svk_kv"])
+                                  "beam_5_perturbed_svk_kv", "t10_4x3x2_mr_kv_keast5", "t10_100el_perturbed_mr_kv_4pt",
+                                  "t10_100el_svk_kv_keast5", "t10_4x3x2_perturbed_svk_kv_keast5",
+                                  "t10_100el_mr_kv_keast5"])
 def test_force_only_parity(torch_cuda, case):
     """tlfea_force_only (the AdamW inner evaluation) on the class and the
     per-(e,q) table paths, with and without Kelvin-Voigt."""
