@@ -207,9 +207,11 @@ typedef struct {
   int32_t n_geometry_classes; /* > 0: congruent elements share reference
                                  tables (staged in shared memory); 0: the
                                  per-(e,q) tables of §4.1 are read from HBM */
-  int32_t fused_eval;      /* reserved: 0 (tlfea_eval = element kernel + H
-                              gather + f/g gather; DESIGN.md §6 records the
-                              one-kernel variants measured). */
+  int32_t fused_eval;      /* 1: tlfea_eval runs as ONE cooperative launch
+                              (small class-mode T10 SVK meshes, <= 3,000
+                              elements: element groups, grid barrier, H and
+                              f / g gathers; bitwise the three-launch path);
+                              0: element kernel + H gather + f/g gather. */
   int64_t n_constraints;   /* rows m of the context's constraint set (0: none) */
   int32_t reference_layout;/* in use: 0 geometry classes, 1 per-(e,q) tables,
                               2 affine (min) layout */

@@ -115,7 +115,7 @@ tlfea_status tlfea_info(tlfea_ctx ctx, tlfea_info_t* o) {
   o->nranks = c.nranks;
   o->device_bytes = c.device_bytes;
   o->n_geometry_classes = c.n_cls;
-  o->fused_eval = 0;
+  o->fused_eval = eval_small_ok(&c) ? 1 : 0;
   o->n_constraints = c.n_con;
   o->reference_layout = c.n_cls > 0 ? 0 : (c.aff ? 2 : 1);
   o->kv_consistent_tangent = c.kvc;
@@ -256,6 +256,10 @@ tlfea_status tlfea_eval(tlfea_ctx ctx, const double* x, const double* v, const d
   const cudaStream_t s = as_stream(stream);
   c.last_stream = s;
   c.eval_inv_h = 1.0 / h;
+  if (eval_small_ok(&c)) {  // small class-mode T10 SVK meshes: one cooperative launch
+    TIMED(4, launch_eval_small(&c, x, v, v_n, f_ext, h, g_out, H_out, f_int_out, s));
+    return TLFEA_OK;
+  }
   TIMED(0, launch_element_kernel(&c, x, v, true, s));
   TIMED(1, launch_gather_H(&c, h, H_out, s));
   TIMED(2, launch_gather_f(&c, v, v_n, f_ext, h, g_out, f_int_out, false, s));

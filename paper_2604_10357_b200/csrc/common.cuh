@@ -283,6 +283,9 @@ tlfea_status launch_dual_update(Context* c, const double* q, double rho, double*
 tlfea_status launch_pack_send(Context* c, double* send, bool force_only, cudaStream_t s);
 tlfea_status launch_gradient_inertia(Context* c, const double* fext, double* g, cudaStream_t s);
 bool force_inertia_capable(const Context* c);
+bool eval_small_ok(const Context* c);
+tlfea_status launch_eval_small(Context* c, const double* x, const double* v, const double* vn, const double* fext,
+                               double h, double* g, double* H, double* fint, cudaStream_t s);
 tlfea_status nccl_get_unique_id(void* id_out);
 tlfea_status nccl_attach(Context* c, const void* id);
 void nccl_detach(Context* c);

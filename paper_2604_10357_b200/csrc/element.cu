@@ -21,6 +21,8 @@
 //   element blocks in ascending element order through the inverse slot map,
 //   writes h K + M/h to (I,J) and its transpose to (J,I); every H value is
 //   written exactly once and every scratch block is read exactly once.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "fgather.cuh"
 #include "material.cuh"
@@ -3122,6 +3124,63 @@ __global__ void __launch_bounds__(kG3Warps * 32) k_gather_units_kvc(GatherArgs A
   gather_units_warp_kvc(((int64_t)blockIdx.x * kG3Warps + (threadIdx.x >> 5)) * 32, A, W);
 }
 
+
+// ------------------------------------------- small meshes: one launch
+// For small T10 SVK meshes with geometry classes (the paper's low ladder
+// rungs, BASELINE config 1) the three launches of tlfea_eval are bound by
+// kernel boundaries, not by work. k_eval_small runs the same device code in
+// one cooperative launch: the class-mode two-phase element groups (grid-
+// stride over warp groups), a grid-wide barrier, then the TMA unit gather of
+// H and the per-DOF f / g gather (grid-stride). Results are bitwise those of
+// the three-kernel path (same arithmetic, same summation orders).
+#ifndef TLFEA_SMALL_MAX_EL
+#define TLFEA_SMALL_MAX_EL 3000  // ladder: faster up to ~1k elements (RES0-RES4), even at 4.5k, slower at 18k
+#endif
+template <int NQ>
+__global__ void __launch_bounds__(kWarps * 32, TLFEA_T10_2PH_MINB) k_eval_small(ElArgs A, GatherArgs G, FArgs F) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) double s_dyn[];  // class tables, then the gather windows + mbarriers
+  const int wib = threadIdx.x >> 5;
+  {
+    const int tot = A.n_cls * NQ * 31;
+    for (int t = threadIdx.x; t < tot; t += blockDim.x) s_dyn[t] = A.cls_tab[t];
+    __syncthreads();
+  }
+  const int64_t ngrp = (A.n_el + 2) / 3;
+  for (int64_t base = (int64_t)blockIdx.x * kWarps; base < ngrp; base += (int64_t)gridDim.x * kWarps) {
+    const int64_t grp = base + wib;
+    T10Pre pre;
+    t10_preload<true>(grp, A, pre);
+    element_group_t10svk<NQ, false, false>(grp, A, s_dyn, pre);
+  }
+  // the scratch written through the generic proxy is read by TMA (async proxy)
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+  cg::this_grid().sync();
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // s_dyn: class tables -> TMA windows
+  __syncthreads();
+  G3Warp W;
+  {
+    double* bufs = s_dyn + (size_t)wib * 2 * kG3Buf;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_dyn + (size_t)kWarps * 2 * kG3Buf) + 2 * wib;
+    if ((threadIdx.x & 31) == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    W.buf[0] = bufs;
+    W.buf[1] = bufs + kG3Buf;
+    W.bar = bars;
+    W.wk = 0;
+  }
+  for (int64_t ug = (int64_t)blockIdx.x * kWarps + wib; ug * 32 < G.n_units; ug += (int64_t)gridDim.x * kWarps)
+    gather_units_warp(ug * 32, G, W);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 3 * F.n_own;
+       t += (int64_t)gridDim.x * blockDim.x)
+    gather_f_dof_one(t, F);
+}
+
 // ------------------------------------------------------------- launchers
 
 static ElArgs el_args(const Context* c, const double* x, const double* v) {
@@ -3359,6 +3418,62 @@ tlfea_status launch_gather_H(Context* c, double h, double* H, cudaStream_t s) {
   k_gather_units_v3<<<(unsigned)((c->n_units + per - 1) / per), kG3Warps * 32, 0, s>>>(gather_args(c, h, H));
   TL_CHECK_LAUNCH();
   return TLFEA_OK;
+}
+
+}  // namespace tlfea
+
+namespace tlfea {
+
+bool eval_small_ok(const Context* c) {
+  return TLFEA_SMALL_MAX_EL > 0 && TLFEA_T10_2PH && c->element == TLFEA_T10 && c->mat.model == TLFEA_SVK &&
+         !c->mat.kv && !c->kvc && c->nranks == 1 && c->n_cls > 0 && c->dest && c->n_el <= TLFEA_SMALL_MAX_EL &&
+         c->n_units > 0;
+}
+
+template <int NQ>
+static tlfea_status launch_small_t(Context* c, const double* x, const double* v, const double* vn, const double* fext,
+                                   double h, double* g, double* H, double* fint, cudaStream_t s) {
+  ElArgs A = el_args(c, x, v);
+  GatherArgs G = gather_args(c, h, H);
+  FArgs F;
+  F.n_own = c->n_own;
+  F.node_ptr = c->node_ptr;
+  F.fscr = c->fscr;
+  F.fpart_in = nullptr;
+  F.own_nodes = c->own_nodes;
+  F.rowptr_c = c->rowptr_c;
+  F.cols_c = c->cols_c;
+  F.M = c->M;
+  F.fff = c->fff;
+  F.v = v;
+  F.vn = vn;
+  F.fext = fext;
+  F.h = h;
+  F.mode = 0;
+  F.g = g;
+  F.fint = fint;
+  auto kern = k_eval_small<NQ>;
+  const size_t smem = std::max(sizeof(double) * c->n_cls * NQ * 31,
+                               sizeof(double) * kWarps * 2 * kG3Buf + sizeof(uint64_t) * kWarps * 2);
+  TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
+  TL_TRY(check_ranges(c, H, s));
+  int dev = 0, nsm = 0, occ = 0;
+  TL_CUDA(cudaGetDevice(&dev));
+  TL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  TL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kWarps * 32, smem));
+  const int64_t need = std::max(((c->n_el + 2) / 3 + kWarps - 1) / kWarps,
+                                (c->n_units / 32 + kWarps) / kWarps);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)nsm * std::max(occ, 1)));
+  void* args[] = {&A, &G, &F};
+  TL_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kWarps * 32), args, smem, s));
+  count_launch();
+  return TLFEA_OK;
+}
+
+tlfea_status launch_eval_small(Context* c, const double* x, const double* v, const double* vn, const double* fext,
+                               double h, double* g, double* H, double* fint, cudaStream_t s) {
+  if (c->nq == 4) return launch_small_t<4>(c, x, v, vn, fext, h, g, H, fint, s);
+  return launch_small_t<5>(c, x, v, vn, fext, h, g, H, fint, s);
 }
 
 }  // namespace tlfea
