@@ -22,6 +22,7 @@ for v in "--config 3 --mesh straight" "--config 3 --tables" "--config 3 --hessia
   line $OUT/bench_$n.json $n
 done
 python tools/bench_adamw.py --config 3 > $OUT/adamw_cfg3.json 2> $OUT/adamw.err; tail -c 400 $OUT/adamw_cfg3.json
+for c in 2 4 5 6; do python tools/bench_force_only.py --config $c > $OUT/force_only_cfg$c.json 2> $OUT/force_only_cfg$c.err; tail -c 250 $OUT/force_only_cfg$c.json; done
 timeout 900 python bench.py --ladder > $OUT/ladder.jsonl 2> $OUT/ladder.err; wc -l $OUT/ladder.jsonl
 timeout 600 python bench.py --impl reference --config 3 --steps 2 --warmup 3 > $OUT/reference_cfg3.json 2> $OUT/reference_cfg3.err; tail -c 300 $OUT/reference_cfg3.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_cfg3.csv \
