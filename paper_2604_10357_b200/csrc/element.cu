@@ -3174,8 +3174,13 @@ __global__ void __launch_bounds__(kWarps * 32, TLFEA_T10_2PH_MINB) k_eval_small(
     W.bar = bars;
     W.wk = 0;
   }
-  for (int64_t ug = (int64_t)blockIdx.x * kWarps + wib; ug * 32 < G.n_units; ug += (int64_t)gridDim.x * kWarps)
+  for (int64_t ug = (int64_t)blockIdx.x * kWarps + wib; ug * 32 < G.n_units; ug += (int64_t)gridDim.x * kWarps) {
     gather_units_warp(ug * 32, G, W);
+    // the next group's first TMA window lands in the buffer this group's
+    // cooperative stores just read through the generic proxy (WAR across proxies)
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 3 * F.n_own;
        t += (int64_t)gridDim.x * blockDim.x)
     gather_f_dof_one(t, F);
