@@ -54,6 +54,8 @@ def check_pattern(ctx, pr):
 CASES = {
     "cfg1_svk_4pt": lambda: (synth.config(1).mesh, dict(synth.SVK_PAPER), 0),
     "t10_5x3x1_svk_keast5_ragged": lambda: (synth.kuhn_t10_box(5, 3, 1, 1.0, 0.6, 0.2), dict(synth.SVK_PAPER), 1),
+    # 2,940 elements: the one-launch small-mesh path with warps taking several unit groups
+    "t10_10x7x7_svk_keast5_small_fused": lambda: (synth.kuhn_t10_box(10, 7, 7, 1.0, 0.7, 0.7), dict(synth.SVK_PAPER), 1),
     "t10_4x3x2_mr_kv_keast5": lambda: (synth.kuhn_t10_box(4, 3, 2, 0.8, 0.6, 0.4),
                                        dict(synth.MR_PAPER, **synth.KV_TIRE), 1),
     "t10_3x2x2_svk_kv_4pt_morton": lambda: (synth.kuhn_t10_box(3, 2, 2, 0.3, 0.2, 0.2, order="morton"),
