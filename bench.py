@@ -132,6 +132,11 @@ def workload(cfg_idx: int, variant: str = "kuhn"):
         # elements congruent): the affine (min) layout path
         mesh = synth.perturbed_straight(mesh)
         cfg = dataclasses.replace(cfg, name=cfg.name + "_straight", mesh=mesh)
+    if variant == "curved" and mesh.element == 0 and cfg_idx != 5:
+        # every node (mid-edge nodes too) randomly displaced: curved, non-congruent
+        # isoparametric T10, the per-(e,q) J^-1 layout path
+        mesh = synth.perturbed(mesh)
+        cfg = dataclasses.replace(cfg, name=cfg.name + "_curved", mesh=mesh)
     if cfg_idx == 5:
         mesh, x, v = synth.many_body()
         vn, fext = v.copy(), None
@@ -425,7 +430,7 @@ def run_ours(args):
     fp64_meas, fp64_src = fp64_peak()
     f_hbm, f_fp64 = gbs / hbm_peak, tfl / FP64_NOMINAL_TFLOPS
     mode = "force_only" if force_only else ("force+tangent+kvc" if info.get("kv_consistent_tangent") else "force+tangent")
-    layout = ["classes", "tables", "affine"][info.get("reference_layout", 1)]
+    layout = ["classes", "tables", "affine", "jinv"][info.get("reference_layout", 1)]
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -488,7 +493,8 @@ def run_ours(args):
                        "tangent": "consistent_kv (NEXT-4)" if info.get("kv_consistent_tangent") else "elastic (Q8)",
                        "parallelism": f"element-partition x{world} ({args.transport} transport)" if world > 1 else "1 GPU",
                        "geometry_classes": info["n_geometry_classes"],
-                       "reference_layout": ["classes", "per-(e,q) tables", "affine min layout"][info["reference_layout"]],
+                       "reference_layout": ["classes", "per-(e,q) tables", "affine min layout",
+                                            "per-(e,q) J^-1 (curved T10)"][info["reference_layout"]],
                        "l2": "inputs/outputs larger than L2 (no flush needed)",
                        "nnz_per_s": ginfo["nnz"] / (ms_step / 1e3) if not force_only else None,
                        "path_hbm_frac": path_b / (ms_step / 1e3) / 1e9 / hbm_peak,
@@ -639,9 +645,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--hessian", choices=["full", "upper"], default="full",
                     help="H storage (full DOF CSR = the headline; upper = NEXT-4 variant)")
-    ap.add_argument("--mesh", choices=["kuhn", "straight"], default="kuhn",
+    ap.add_argument("--mesh", choices=["kuhn", "straight", "curved"], default="kuhn",
                     help="straight: the T10 mesh with randomly displaced corners (straight-sided, non-congruent: "
-                         "the affine min layout instead of geometry classes)")
+                         "the affine min layout instead of geometry classes); curved: every node displaced "
+                         "(isoparametric, non-congruent: the per-(e,q) J^-1 layout)")
     ap.add_argument("--transport", choices=["torch", "lib"], default="torch",
                     help="N>1 exchange: torch.distributed P2P (NCCL) or the library's own NCCL transport "
                          "(tlfea_nccl_attach / tlfea_eval_exchange)")

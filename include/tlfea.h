@@ -162,7 +162,9 @@ typedef struct {
                              reference shapes; else, for straight-sided T10,
                              the affine "min" layout (13 fp64 per element:
                              grad_X z_0..3 and J0); else the
-                             per-(e,q) tables of §4.1.
+                             per-(e,q) J^-1 and J0 w_q of curved T10 (10 fp64
+                             per point, grad N rebuilt from the T10 basis);
+                             else the per-(e,q) tables of §4.1.
                              1: the per-(e,q) tables always (the paper's
                              layout, on any mesh). 2: the affine layout
                              whenever the T10 mesh is straight-sided (no
@@ -214,7 +216,8 @@ typedef struct {
                               0: element kernel + H gather + f/g gather. */
   int64_t n_constraints;   /* rows m of the context's constraint set (0: none) */
   int32_t reference_layout;/* in use: 0 geometry classes, 1 per-(e,q) tables,
-                              2 affine (min) layout */
+                              2 affine (min) layout, 3 per-(e,q) J^-1 + J0 w
+                              (curved T10, 10 fp64 per point) */
   int32_t kv_consistent_tangent; /* 1 if H is the consistent Kelvin-Voigt
                               tangent (options.kv_consistent_tangent with
                               damping), else 0 */

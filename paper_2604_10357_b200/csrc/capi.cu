@@ -117,7 +117,7 @@ tlfea_status tlfea_info(tlfea_ctx ctx, tlfea_info_t* o) {
   o->n_geometry_classes = c.n_cls;
   o->fused_eval = eval_small_ok(&c) ? 1 : 0;
   o->n_constraints = c.n_con;
-  o->reference_layout = c.n_cls > 0 ? 0 : (c.aff ? 2 : 1);
+  o->reference_layout = c.n_cls > 0 ? 0 : (c.aff ? 2 : (c.jinv ? 3 : 1));
   o->kv_consistent_tangent = c.kvc;
   return TLFEA_OK;
 }

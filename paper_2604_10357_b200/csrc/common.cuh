@@ -161,6 +161,7 @@ struct Context {
   // affine (min) layout of straight-sided T10 without classes: [n_el][13] =
   // grad_X z_0..3 (barycentric gradients), J0 (SURVEY §8(d) min layout)
   double* aff = nullptr;
+  double* jinv = nullptr;         // [n_el][nq][10] J^-1 (row-major) and J0 w_q (curved T10 without classes)
   double* cls_aff = nullptr;
   double* cls_mass = nullptr;     // [n_cls][nen][nen] element mass per class (single rank, classes)      // [n_cls][13] the same per class (straight-sided T10 with classes)
   std::vector<int64_t> cls_rep;   // representative (first) element of each class

@@ -146,6 +146,7 @@ struct ElArgs {
   const double* cls_tab;
   int n_cls;
   const double* aff;  // affine (min) layout: [n_el][13] = grad_X z_0..3, J0 (straight-sided T10)
+  const double* jinv;  // curved T10: [n_el][NQ][10] = J^-1 (row-major), J0 w_q
   int64_t g0;         // first warp group of the launch (element range [EPW g0, n_el))
   const double* x;
   const double* v;
@@ -643,7 +644,7 @@ __device__ __forceinline__ void t10_affine_load(int64_t grp, const ElArgs& A, T1
   f.J0 = ok ? a[12] : 0.0;
 }
 // Expand half: the lane's table row (grad N_a of the 10 nodes, J0 w_q).
-template <int NQ>
+template <int NQ, bool JW = false>  // JW: f.J0 already holds J0 w_q (jinv layout)
 __device__ __forceinline__ void t10_affine_expand(const T10Aff& f, double* __restrict__ s_tab) {
   constexpr int NEN = 10, EPW = 3, TABW = 3 * NEN + 1;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -661,9 +662,35 @@ __device__ __forceinline__ void t10_affine_expand(const T10Aff& f, double* __res
     for (int m = 0; m < 6; ++m)
 #pragma unroll
       for (int k = 0; k < 3; ++k) t[3 * (4 + m) + k] = 4.0 * (z[ea[m]] * f.gz[eb[m]][k] + z[eb[m]] * f.gz[ea[m]][k]);
-    t[3 * NEN] = f.J0 * w;
+    t[3 * NEN] = JW ? f.J0 : f.J0 * w;
   }
   __syncwarp();
+}
+// Curved T10 ("jinv" layout, 10 fp64 per (e,q)): lane (element g, point q)
+// loads J^-1 and J0 w_q of its point; grad_X z_{j+1} = row j of J^-1 and
+// grad_X z_0 = -(their sum) at that point, so t10_affine_expand<NQ, true>
+// rebuilds the same table row (grad N = d N / d xi J^-1).
+template <int NQ>
+__device__ __forceinline__ void t10_jinv_load(int64_t grp, const ElArgs& A, T10Aff& f) {
+  constexpr int EPW = 3;
+  const int lane = threadIdx.x & 31;
+  const int g = lane / NQ, q = lane - NQ * (lane / NQ);
+  const int64_t e = grp * EPW + g;
+  const bool ok = lane < EPW * NQ && e < A.n_el;
+  const double* p = A.jinv + 10 * ((ok ? e : 0) * NQ + (ok ? q : 0));
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) f.gz[1 + j][k] = ok ? p[3 * j + k] : 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) f.gz[0][k] = -(f.gz[1][k] + f.gz[2][k] + f.gz[3][k]);
+  f.J0 = ok ? p[9] : 0.0;  // J0 w_q
+}
+template <int NQ>
+__device__ __forceinline__ void t10_stage_jinv(int64_t grp, const ElArgs& A, double* __restrict__ s_tab) {
+  T10Aff f;
+  t10_jinv_load<NQ>(grp, A, f);
+  t10_affine_expand<NQ, true>(f, s_tab);
 }
 template <int NQ>
 __device__ __forceinline__ void t10_stage_affine(int64_t grp, const ElArgs& A, double* __restrict__ s_tab) {
@@ -2181,7 +2208,8 @@ __host__ __device__ constexpr int el_minb_k() {
 }
 
 // AFF: table mode with the tables generated from the affine (min) layout.
-template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS, bool AFF = false>
+// JNV: table mode with the tables generated from the per-(e,q) J^-1 layout (curved T10).
+template <int ELEM, int NQ, int MODEL, bool KV, bool TAN, bool CLS, int NPASS, bool AFF = false, bool JNV = false>
 __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV, TAN, CLS>()) k_element(ElArgs A) {
   extern __shared__ double s_tab[];  // CLS: [n_cls][NQ][3 NEN + 1]
   // (SVK in table mode measured slower two-phase: config 3 without classes 13.97 vs 12.61 ms, force only
@@ -2193,11 +2221,13 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
   constexpr bool V2PH = TLFEA_T10_2PH && ELEM == 0 && MODEL == 0 && KV && TAN && CLS;  // SVK + Kelvin-Voigt
   const int64_t grp = A.g0 + (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);  // this warp's element group
   T10Pre pre;
-  if constexpr (T2PH && !CLS && !AFF) t10_stage_tables_async<NQ>(grp, A, s_tab);
+  if constexpr (T2PH && !CLS && !AFF && !JNV) t10_stage_tables_async<NQ>(grp, A, s_tab);
   T10Aff aff;
   if constexpr (T2PH && AFF) t10_affine_load<NQ>(grp, A, aff);
+  if constexpr (T2PH && JNV) t10_jinv_load<NQ>(grp, A, aff);
   if constexpr (T2PH) t10_preload<CLS>(grp, A, pre);
   if constexpr (T2PH && AFF) t10_affine_expand<NQ>(aff, s_tab);
+  if constexpr (T2PH && JNV) t10_affine_expand<NQ, true>(aff, s_tab);
   if (CLS) {
     // all loads of a thread in flight at once (one L2 round trip, not one per element)
     const int tot = A.n_cls * NQ * (Geo<ELEM>::NEN * 3 + 1);
@@ -2216,9 +2246,9 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
     if constexpr (!CLS) pre.ce = (threadIdx.x >> 5) * 3 + (threadIdx.x & 31) / 10;  // staged slot
     // (affine tables are written synchronously: no cp.async wait before phase A)
     if constexpr (TAN)
-      element_group_t10svk<NQ, false, !CLS && !AFF>(grp, A, s_tab, pre);
+      element_group_t10svk<NQ, false, !CLS && !AFF && !JNV>(grp, A, s_tab, pre);
     else
-      element_group_t10svk_force<NQ, !CLS && !AFF>(grp, A, s_tab, pre);
+      element_group_t10svk_force<NQ, !CLS && !AFF && !JNV>(grp, A, s_tab, pre);
   } else if constexpr (A2PH) {
     element_group_ancf_svk<NQ>(grp, A, s_tab);
   } else if constexpr (B2PH) {
@@ -2230,6 +2260,8 @@ __global__ void __launch_bounds__(kWarps * 32, el_minb_k<ELEM, MODEL, NPASS, KV,
   } else if constexpr (M2PH) {
     if constexpr (!CLS && AFF)
       t10_stage_affine<NQ>(grp, A, s_tab);
+    else if constexpr (!CLS && JNV)
+      t10_stage_jinv<NQ>(grp, A, s_tab);
     else if constexpr (!CLS)
       t10_stage_tables<NQ>(grp, A, s_tab);
     element_group_t10mr<NQ, KV>(grp, A, s_tab, !CLS);
@@ -3198,6 +3230,7 @@ static ElArgs el_args(const Context* c, const double* x, const double* v) {
   A.cls_tab = c->cls_tab;
   A.n_cls = c->n_cls;
   A.aff = c->aff;
+  A.jinv = c->jinv;
   A.g0 = 0;
   A.x = x;
   A.v = v;
@@ -3290,6 +3323,13 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
     if constexpr (stage) {
       if (c->aff) {  // tables generated from the affine (min) layout
         auto kern = k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>(), true>;
+        TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
+        kern<<<grid, kWarps * 32, smem, s>>>(A);
+        TL_CHECK_LAUNCH();
+        return TLFEA_OK;
+      }
+      if (c->jinv) {  // tables generated from the per-(e,q) J^-1 layout (curved T10)
+        auto kern = k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>(), false, true>;
         TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
         kern<<<grid, kWarps * 32, smem, s>>>(A);
         TL_CHECK_LAUNCH();

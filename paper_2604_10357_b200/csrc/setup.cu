@@ -121,7 +121,7 @@ __global__ void k_precompute(int element, int64_t n_el, int nq, int nen, const i
                              const double* __restrict__ X, const double* __restrict__ dims,
                              const double* __restrict__ qxi, const double* __restrict__ qw,
                              double* __restrict__ gradN, double* __restrict__ J0w,
-                             unsigned long long* __restrict__ bad) {
+                             unsigned long long* __restrict__ bad, double* __restrict__ jinv = nullptr) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n_el * nq) return;
   const int64_t e = t / nq;
@@ -172,6 +172,11 @@ __global__ void k_precompute(int element, int64_t n_el, int nq, int nen, const i
     for (int k = 0; k < 3; ++k)
       out[3 * a + k] = dN[a][0] * Ji[k] + dN[a][1] * Ji[3 + k] + dN[a][2] * Ji[6 + k];
   J0w[t] = det * qw[q];
+  if (jinv) {  // the compressed curved-T10 layout: J^-1 (9) and J0 w_q per (e,q)
+#pragma unroll
+    for (int r = 0; r < 9; ++r) jinv[10 * t + r] = Ji[r];
+    jinv[10 * t + 9] = det * qw[q];
+  }
 }
 
 // Straight-sided T10 test: every mid-edge node at the midpoint of its edge.
@@ -1250,6 +1255,18 @@ tlfea_status setup_context(Context* c, const tlfea_mesh* mesh, const tlfea_mater
   if (c->element == TLFEA_T10 && c->affine && c->n_cls == 0 && c->force_tables != 1 && c->n_el > 0) {
     TL_TRY(c->alloc(&c->aff, (size_t)c->n_el * 13));
     k_affine_layout<<<grid_for(c->n_el, 256), 256>>>(c->n_el, c->conn, dX, c->aff);
+    TL_CHECK_LAUNCH();
+  }
+  // curved T10 without classes: per (e,q) the inverse Jacobian and J0 w_q (10
+  // fp64 instead of the 31 of the paper's grad N + J0 w tables);
+  // the kernels rebuild grad N from the T10 basis at the rule's points
+  if (c->element == TLFEA_T10 && !c->affine && c->n_cls == 0 && c->force_tables == 0 && c->n_el > 0) {
+    TL_TRY(c->alloc(&c->jinv, (size_t)c->n_el * nq * 10));
+    TmpArr<double> g2, w2;
+    TL_TRY(g2.get((size_t)c->n_el * nq * nen * 3));
+    TL_TRY(w2.get((size_t)c->n_el * nq));
+    k_precompute<<<grid_for(c->n_el * nq, 128), 128>>>(c->element, c->n_el, nq, nen, c->conn, dX, ddims, dq.p, dw.p,
+                                                       g2.p, w2.p, c->err_flag, c->jinv);
     TL_CHECK_LAUNCH();
   }
 

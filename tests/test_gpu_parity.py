@@ -139,6 +139,8 @@ def test_eval_parity(torch_cuda, case):
         assert ctx.info["n_geometry_classes"] == 0 and ctx.info["reference_layout"] == 2
     elif "perturbed" in case or "graded" in case:
         assert ctx.info["n_geometry_classes"] == 0
+        if mesh.element == 0:   # curved T10: the per-(e,q) J^-1 layout
+            assert ctx.info["reference_layout"] == 3
     elif mesh.element == 0 and mesh.n_el >= 6:
         assert ctx.info["n_geometry_classes"] == 6
     else:
@@ -326,6 +328,36 @@ def test_affine_layout_on_kuhn_boxes(torch_cuda, case):
     assert rel(g.cpu().numpy(), g0) <= TOL and rel(H.cpu().numpy(), H0) <= TOL and rel(f.cpu().numpy(), f0) <= TOL
     if not mat.get("eta_damp"):
         assert rel(fo, f0) <= TOL
+
+
+@pytest.mark.parametrize("case", ["t10_100el_perturbed_svk_keast5", "t10_4x3x2_perturbed_svk_kv_keast5",
+                                  "t10_3x3x2_perturbed_mr_4pt", "t10_100el_perturbed_mr_kv_4pt"])
+def test_jinv_layout_vs_tables(torch_cuda, case):
+    """Curved T10 (every node displaced): the per-(e,q) J^-1 layout (10 fp64 per
+    point, grad N rebuilt from the T10 basis) against the paper's per-(e,q)
+    tables forced by options.reference_layout = 1 (to rounding, 1e-12) and the oracle,
+    for force + H + g and force only."""
+    import paper_2604_10357_b200 as T
+    torch = torch_cuda
+    mesh, mat, rule = CASES[case]()
+    h = synth.H_T10
+    x, v, vn, fext = state(mesh)
+    cj = T.Context.from_mesh(mesh, mat, rule)
+    ct = T.Context.from_mesh(mesh, mat, rule, reference_layout="tables")
+    assert cj.info["reference_layout"] == 3 and ct.info["reference_layout"] == 1
+    outs = []
+    for c in (cj, ct):
+        g, H, f = c.eval(dev(torch, x), dev(torch, v), dev(torch, vn), dev(torch, fext), h, f_int=c.empty_outputs()[2])
+        fo = c.force_only(dev(torch, x), dev(torch, v))
+        torch.cuda.synchronize()
+        outs.append([t.cpu().numpy() for t in (g, H, f, fo)])
+    pr = oracle.Problem(mesh, mat, rule)
+    g0, H0, f0 = pr.eval(x, v, vn, fext, h)
+    for a, b in zip(outs[0], outs[1]):   # g carries cancellation (f - f_ext - f_ff + M dv/h)
+        assert rel(a, b) <= 1e-12
+    for a, b in zip(outs[0][:3], (g0, H0, f0)):
+        assert rel(a, b) <= TOL
+    assert rel(outs[0][3], f0) <= TOL
 
 
 @pytest.mark.parametrize("case", ["cfg1_svk_4pt", "t10_5x3x1_svk_keast5_ragged", "t10_single_element_svk",
