@@ -18,7 +18,9 @@ void count_launch(int n = 1);
 // Dynamic shared memory (and static + dynamic above 48 KB) needs the
 // per-device, per-kernel opt-in attribute: applied once per (kernel, current
 // device, size), thread-safe.
-tlfea_status ensure_dynamic_smem(const void* kernel, size_t bytes);
+tlfea_status ensure_dynamic_smem(const void* kernel, size_t bytes, int block_threads = 128);
+// the maximum shared-memory carveout for a kernel (once per kernel and device)
+tlfea_status ensure_carveout(const void* kernel);
 
 #define TL_CUDA(call)                                                          \
   do {                                                                         \

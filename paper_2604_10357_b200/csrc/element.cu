@@ -3276,7 +3276,7 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
       ElArgs A = el_args(c, x, v);
       A.n_el = e_end;
       auto kern = k_force_t10svk_wide<NQ>;
-      TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
+      TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem, kFW * 32));
       int64_t grid = (e_end - e_begin + per - 1) / per;
       if (TLFEA_FW_PERSIST) {  // one resident wave of persistent CTAs
         int dev = 0, nsm = 0, occ = 0;
@@ -3314,6 +3314,7 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
   if (c->n_cls > 0) {
     const size_t smem = sizeof(double) * c->n_cls * NQ * (G::NEN * 3 + 1);
     auto kern = k_element<ELEM, NQ, MODEL, KV, TAN, true, el_npass<ELEM, MODEL>()>;
+    if constexpr (ELEM == 0 && MODEL == 0 && !KV && TAN) TL_TRY_LAUNCH(ensure_carveout((const void*)kern));
     TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
     kern<<<grid, kWarps * 32, smem, s>>>(A);
   } else {
@@ -3323,6 +3324,7 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
     if constexpr (stage) {
       if (c->aff) {  // tables generated from the affine (min) layout
         auto kern = k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>(), true>;
+        if constexpr (MODEL == 0 && !KV && TAN) TL_TRY_LAUNCH(ensure_carveout((const void*)kern));
         TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
         kern<<<grid, kWarps * 32, smem, s>>>(A);
         TL_CHECK_LAUNCH();
@@ -3330,6 +3332,7 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
       }
       if (c->jinv) {  // tables generated from the per-(e,q) J^-1 layout (curved T10)
         auto kern = k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>(), false, true>;
+        if constexpr (MODEL == 0 && !KV && TAN) TL_TRY_LAUNCH(ensure_carveout((const void*)kern));
         TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
         kern<<<grid, kWarps * 32, smem, s>>>(A);
         TL_CHECK_LAUNCH();
@@ -3337,6 +3340,7 @@ static tlfea_status launch_el(Context* c, const double* x, const double* v, cuda
       }
     }
     auto kern = k_element<ELEM, NQ, MODEL, KV, TAN, false, el_npass<ELEM, MODEL>()>;
+    if constexpr (ELEM == 0 && MODEL == 0 && !KV && TAN) TL_TRY_LAUNCH(ensure_carveout((const void*)kern));
     TL_TRY_LAUNCH(ensure_dynamic_smem((const void*)kern, smem));
     kern<<<grid, kWarps * 32, smem, s>>>(A);
   }

@@ -27,8 +27,20 @@ tlfea_status fail(tlfea_status st, const std::string& msg) {
 }
 void count_launch(int n) { g_launches += n; }
 
-tlfea_status ensure_dynamic_smem(const void* kernel, size_t bytes) {
+// Shared-memory carveout of the T10 SVK tangent groups (3 CTAs x ~50 KB per
+// SM): the maximum. Left to the driver, the carveout is sometimes rounded to a
+// configuration that fits only 2 of them per SM: config 3 element kernel
+// 10.58-10.63 ms with the default vs 9.97 ms at a 75 / 100 % carveout (10.62
+// at 60 %) — the "box-to-box spread" of earlier rounds. Other kernels keep the
+// driver's choice (a fixed 100 % costs the beam and Mooney-Rivlin kernels
+// 1-2 %; sizing the carveout to the register-limited CTAs rounded down to too
+// small a configuration: 16 ms).
+#ifndef TLFEA_CARVEOUT
+#define TLFEA_CARVEOUT 100
+#endif
+tlfea_status ensure_dynamic_smem(const void* kernel, size_t bytes, int block_threads) {
   // (set even below 48 KB: static + dynamic above 48 KB needs the opt-in too)
+  (void)block_threads;
   if (bytes == 0) return TLFEA_OK;
   int dev = 0;
   TL_CUDA(cudaGetDevice(&dev));
@@ -38,7 +50,24 @@ tlfea_status ensure_dynamic_smem(const void* kernel, size_t bytes) {
   size_t& have = applied[{kernel, dev}];
   if (bytes > have) {
     TL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+#if TLFEA_CARVEOUT >= 0
+    TL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, TLFEA_CARVEOUT));
+#endif
     have = bytes;
+  }
+  return TLFEA_OK;
+}
+tlfea_status ensure_carveout(const void* kernel) {
+  if (TLFEA_CARVEOUT < 0) return TLFEA_OK;
+  int dev = 0;
+  TL_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, bool> done;
+  std::lock_guard<std::mutex> lock(mu);
+  bool& d = done[{kernel, dev}];
+  if (!d) {
+    TL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, TLFEA_CARVEOUT));
+    d = true;
   }
   return TLFEA_OK;
 }
