@@ -27,16 +27,18 @@ tlfea_status fail(tlfea_status st, const std::string& msg) {
 }
 void count_launch(int n) { g_launches += n; }
 
-// Shared-memory carveout of the T10 SVK tangent groups (3 CTAs x ~50 KB per
-// SM): the maximum. Left to the driver, the carveout is sometimes rounded to a
-// configuration that fits only 2 of them per SM: config 3 element kernel
-// 10.58-10.63 ms with the default vs 9.97 ms at a 75 / 100 % carveout (10.62
-// at 60 %) — the "box-to-box spread" of earlier rounds. Other kernels keep the
-// driver's choice (a fixed 100 % costs the beam and Mooney-Rivlin kernels
-// 1-2 %; sizing the carveout to the register-limited CTAs rounded down to too
-// small a configuration: 16 ms).
+// Shared-memory carveout (TLFEA_CARVEOUT, percent; -1 = the driver's choice,
+// the default). On some boxes of the pool the driver's choice for the T10 SVK
+// tangent groups (3 CTAs x ~50 KB per SM) fits only 2 of them: config 3
+// element kernel 10.4-10.6 ms instead of ~9.97 ms, where a forced 75 / 100 %
+// restored 9.97 ms on such a box. A forced 100 % was not a robust fix: it cost
+// the lane-per-point force kernels up to 40 % (200x200 ANCF force only 0.214
+// vs 0.154 ms), the beam / Mooney-Rivlin tangent kernels 1-2 %, and on
+// another box the curved-mesh T10 group 10.57 vs 10.02 ms; sizing it to the
+// register-limited CTA count rounded to too small a configuration (16 ms).
+// Left at the driver's choice; recorded as an open item.
 #ifndef TLFEA_CARVEOUT
-#define TLFEA_CARVEOUT 100
+#define TLFEA_CARVEOUT -1
 #endif
 tlfea_status ensure_dynamic_smem(const void* kernel, size_t bytes, int block_threads) {
   // (set even below 48 KB: static + dynamic above 48 KB needs the opt-in too)
@@ -50,9 +52,6 @@ tlfea_status ensure_dynamic_smem(const void* kernel, size_t bytes, int block_thr
   size_t& have = applied[{kernel, dev}];
   if (bytes > have) {
     TL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-#if TLFEA_CARVEOUT >= 0
-    TL_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, TLFEA_CARVEOUT));
-#endif
     have = bytes;
   }
   return TLFEA_OK;
