@@ -159,6 +159,7 @@ struct ElArgs {
   double inv_h;  // consistent KV tangent only: 1/h of the evaluation (k_element_kvc)
   // element-level inertia (k_force_t10_aff<.., INR>, v = v - v_n): f_a += (1/h) sum_b m_ab (v - v_n)_b
   const double* cls_mass;
+  int mass_closed;   // 1: exact consistent mass (mass_rule 0) of straight-sided T10 -> closed form
 };
 
 __device__ __forceinline__ void pf_cp4(void* smem, const void* gmem) {
@@ -1470,6 +1471,9 @@ __global__ void __launch_bounds__(kFW * 32, NQ == 4 ? TLFEA_FW_MINB4 : TLFEA_FW_
 #ifndef TLFEA_FORCE_AFF
 #define TLFEA_FORCE_AFF 1
 #endif
+#ifndef TLFEA_INR_CLOSED
+#define TLFEA_INR_CLOSED 1  // AdamW element inertia: closed-form T10 mass (mass_rule 0) instead of the class rows
+#endif
 #ifndef TLFEA_FA_MINB
 #define TLFEA_FA_MINB 3  // config 5: 0.263 ms at 3 CTAs/SM (166 registers) vs 0.283 at 4 (128, spills), 0.320 at 2
 #endif
@@ -1602,12 +1606,42 @@ __global__ void __launch_bounds__(kFABlock, TLFEA_FA_MINB) k_force_t10_aff(ElArg
       f[4 + m][r] = 4.0 * s;
     }
   if constexpr (INR) {
-    const double* me = s_aff + A.n_cls * 13 + 100 * A.cls[e];
     double dv[10][3];
 #pragma unroll
     for (int b = 0; b < 10; ++b)
 #pragma unroll
       for (int i = 0; i < 3; ++i) dv[b][i] = A.v[3 * (int64_t)nd[b] + i];  // v - v_n (the AdamW update wrote it)
+#if TLFEA_INR_CLOSED
+    if (A.mass_closed) {
+      // the exact consistent mass of a straight-sided T10 (reading Q4):
+      // m_ab = rho V / 420 C_ab, C = {corner-corner 6 | 1; corner-edge -4 on the
+      // edge, else -6; edge-edge 32 | 16 sharing a vertex | 8 opposite}, so with
+      // S_c, S_e the corner / edge sums of v - v_n:
+      //   corner i: 5 dv_i + S_c - 6 S_e + 2 (sum of the edges at i)
+      //   edge (a,b): 2 (dv_a + dv_b) - 6 S_c + 16 S_e + 16 dv_m - 8 dv_opposite
+      const double sc = A.mat.rho0 * J0 / 2520.0 * A.inv_h;  // rho V / 420 / h, V = J0 / 6
+      constexpr int EA2[6] = {0, 1, 2, 0, 1, 2}, EB2[6] = {1, 2, 0, 3, 3, 3}, OPP[6] = {9, 7, 8, 5, 6, 4};
+      constexpr int AT[4][3] = {{4, 6, 7}, {4, 5, 8}, {5, 6, 9}, {7, 8, 9}};  // edges at corner i
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double Sc = (dv[0][i] + dv[1][i]) + (dv[2][i] + dv[3][i]);
+        const double Se = ((dv[4][i] + dv[5][i]) + (dv[6][i] + dv[7][i])) + (dv[8][i] + dv[9][i]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double r = 5.0 * dv[c][i] + Sc - 6.0 * Se + 2.0 * ((dv[AT[c][0]][i] + dv[AT[c][1]][i]) + dv[AT[c][2]][i]);
+          f[c][i] = fma(r, sc, f[c][i]);
+        }
+#pragma unroll
+        for (int m = 0; m < 6; ++m) {
+          const double r = 2.0 * (dv[EA2[m]][i] + dv[EB2[m]][i]) - 6.0 * Sc + 16.0 * Se + 16.0 * dv[4 + m][i] -
+                           8.0 * dv[OPP[m]][i];
+          f[4 + m][i] = fma(r, sc, f[4 + m][i]);
+        }
+      }
+    } else
+#endif
+    {
+    const double* me = s_aff + A.n_cls * 13 + 100 * A.cls[e];
 #pragma unroll
     for (int a = 0; a < 10; ++a) {
       double r[3] = {0, 0, 0};
@@ -1619,6 +1653,7 @@ __global__ void __launch_bounds__(kFABlock, TLFEA_FA_MINB) k_force_t10_aff(ElArg
       }
 #pragma unroll
       for (int i = 0; i < 3; ++i) f[a][i] = fma(r[i], A.inv_h, f[a][i]);
+    }
     }
   }
 #pragma unroll
@@ -3242,6 +3277,7 @@ static ElArgs el_args(const Context* c, const double* x, const double* v) {
   A.err = c->err_flag;
   A.inv_h = c->eval_inv_h;
   A.cls_mass = c->cls_mass;
+  A.mass_closed = (c->mass_rule == 0 && c->affine) ? 1 : 0;
   return A;
 }
 
