@@ -125,8 +125,9 @@ struct Context {
   // consistent Kelvin-Voigt tangent (options.kv_consistent_tangent with damping,
   // NEXT-4): each gather-sorted scratch slot holds 18 values, the unit's (I,J)
   // and (J,I) contributions in their own orientation (non-symmetric blocks);
-  // eval_inv_h = 1/h of the evaluation in flight (the element kernel scales the
-  // df/dv part by 1/h so the gather's h * acc + M/h gives h df/dx + df/dv).
+  // eval_inv_h = 1/h of the evaluation in flight (the consistent-KV element
+  // kernels scale the df/dv part by 1/h so the gather's h * acc + M/h gives
+  // h df/dx + df/dv; the AdamW element inertia m_e (v - v_n)_e is scaled by it).
   int kvc = 0;
   double eval_inv_h = 0.0;
   // element-level inertia request of the AdamW gradient (launch_element_kernel,
